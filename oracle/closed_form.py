@@ -1,0 +1,141 @@
+"""ORACLE (test infrastructure only): closed-form HHL final state (SURVEY §8(c) eq. CF).
+
+An analytic pin on the gate-level oracle, derived independently of it: for the
+textbook circuit (H layer, c-U^{2^j}, IQFT, reciprocal RY, QFT, c-U^{2^j}†, H
+layer) and |b> = sum_s beta_s |v_s>,
+
+    alpha_m(phi) = N_c^-1 sum_k e^{2 pi i k (phi - m/N_c)}        (QPE amplitude)
+    psi[a, k, .] = sum_s beta_s v_s · y_{s,a}[k],
+    y_{s,a} = H^{⊗n_c} · diag(e^{-2 pi i phi_s k}) · F · (r_a ⊙ alpha(phi_s)),
+    F|m> = N_c^-1/2 sum_k e^{+2 pi i k m/N_c}|k>,  r_1 = s, r_0 = sqrt(1 - s^2),
+
+and the post-selected vector x~ = sum_s beta_s v_s sum_m |alpha_m(phi_s)|^2 s_m
+with P_succ = ||x~||^2. The phases e^{2 pi i phi k} are formed as products of
+e^{2 pi i frac(2^j phi)} over the set bits of k (R13), like the circuit does.
+
+The reciprocal s_m is re-derived here from its definition
+vectorised in numpy; tests/test_oracle_pins.py checks it against sv_oracle.c.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def recip_table(n_c: int, delta: float, signed: int = 1, snap: float = 0.0) -> np.ndarray:
+    """s_m for m = 0..2^n_c - 1 (definition in SURVEY §8(a) a7 / DESIGN.md R6)."""
+    Nc = 1 << n_c
+    m = np.arange(Nc, dtype=np.float64)
+    sign = np.ones(Nc)
+    mp = m.copy()
+    if signed:
+        neg = np.arange(Nc) >= (Nc >> 1)
+        mp[neg] = Nc - m[neg]
+        sign[neg] = -1.0
+    L = 2.0 ** (n_c - (1 if signed else 0))
+    with np.errstate(divide="ignore"):
+        r = np.where(mp > 0, delta * L / np.where(mp > 0, mp, 1.0), np.inf)
+    s = np.where(np.abs(r - 1.0) <= snap, 1.0, np.where(r < 1.0, r, 0.0))
+    s[0] = 0.0
+    return sign * s
+
+
+def phase_vector(phi: float, n_c: int) -> np.ndarray:
+    """e^{2 pi i phi k} for k < 2^n_c, as prod_j e^{2 pi i frac(2^j phi)}^{k_j}."""
+    ph = np.ones(1, dtype=np.complex128)
+    for j in range(n_c):
+        x = np.ldexp(phi, j)
+        f = x - np.floor(x)
+        ph = np.concatenate([ph, ph * np.exp(2j * np.pi * f)])
+    return ph
+
+
+def fwht(v: np.ndarray) -> np.ndarray:
+    """Normalised Walsh–Hadamard transform H^{⊗n} v (little-endian, any bit order is the same)."""
+    v = v.copy()
+    n = v.size
+    h = 1
+    while h < n:
+        v = v.reshape(-1, 2, h)
+        a = v[:, 0, :].copy()
+        b = v[:, 1, :]
+        v[:, 0, :] = a + b
+        v[:, 1, :] = a - b
+        v = v.reshape(n)
+        h *= 2
+    return v / np.sqrt(n)
+
+
+def _y_vectors(phi: float, n_c: int, s_tab: np.ndarray):
+    Nc = 1 << n_c
+    ph = phase_vector(phi, n_c)
+    alpha = np.fft.fft(ph) / Nc                       # alpha_m = N^-1 sum_k e^{2 pi i k phi} e^{-2 pi i k m/N}
+    r1 = s_tab
+    r0 = np.sqrt(1.0 - s_tab ** 2)
+    out = []
+    for r in (r0, r1):
+        z = np.fft.ifft(r * alpha) * np.sqrt(Nc)       # F (r ⊙ alpha)
+        out.append(np.conj(ph) * z)                    # controlled-U^† phases, before the final H layer
+    return out
+
+
+def full_state(p) -> np.ndarray:
+    """Whole 2^n state vector for an oracle.hhl.HHLPlan (n_c <= ~20)."""
+    nb, nc = p.n_b, p.n_c
+    Nc = 1 << nc
+    N = 1 << nb
+    s_tab = recip_table(nc, p.delta, 1, p.snap)
+    beta = p.V.T @ p.b_hat
+    psi = np.zeros((2, Nc, N), dtype=np.complex128)      # [ancilla, clock, sys]
+    for s in range(N):
+        if beta[s] == 0.0:
+            continue
+        w0, w1 = _y_vectors(p.phi[s], nc, s_tab)
+        y0, y1 = fwht(w0), fwht(w1)
+        psi[0] += beta[s] * np.outer(y0, p.V[:, s])
+        psi[1] += beta[s] * np.outer(y1, p.V[:, s])
+    return psi.reshape(-1)
+
+
+def postselected(p):
+    """x~ = sum_s beta_s v_s sum_m |alpha_m(phi_s)|^2 s_m and P_succ = ||x~||^2."""
+    nc = p.n_c
+    Nc = 1 << nc
+    s_tab = recip_table(nc, p.delta, 1, p.snap)
+    beta = p.V.T @ p.b_hat
+    x = np.zeros(p.A.shape[0])
+    for s in range(beta.size):
+        alpha = np.fft.fft(phase_vector(p.phi[s], nc)) / Nc
+        x += beta[s] * p.V[:, s] * float(np.sum(np.abs(alpha) ** 2 * s_tab))
+    return x, float(x @ x)
+
+
+def sampled_amplitudes(p, indices) -> np.ndarray:
+    """psi[i] for selected logical indices i, for any n_c (cost O(N · 2^n_c) per eigen-component
+    plus O(2^n_c) per distinct clock value): the Walsh row of clock value k is contracted bit by bit."""
+    nb, nc = p.n_b, p.n_c
+    idx = np.asarray(indices, dtype=np.int64)
+    sys_i = idx & ((1 << nb) - 1)
+    k_i = (idx >> nb) & ((1 << nc) - 1)
+    a_i = (idx >> (nb + nc)) & 1
+    ks = np.unique(k_i)
+    s_tab = recip_table(nc, p.delta, 1, p.snap)
+    beta = p.V.T @ p.b_hat
+    Nc = 1 << nc
+    yk = np.zeros((2, ks.size, beta.size), dtype=np.complex128)   # y_{s,a}[k]
+    for s in range(beta.size):
+        if beta[s] == 0.0:
+            continue
+        ws = _y_vectors(p.phi[s], nc, s_tab)
+        for a in (0, 1):
+            for ki, k in enumerate(ks):
+                v = ws[a]
+                for j in range(nc):                 # contract bit j (LSB first) with (1, (-1)^{k_j})
+                    v = v.reshape(-1, 2)
+                    v = v[:, 0] + v[:, 1] if not ((int(k) >> j) & 1) else v[:, 0] - v[:, 1]
+                yk[a, ki, s] = v[0] / np.sqrt(Nc)
+    out = np.empty(idx.size, dtype=np.complex128)
+    kpos = {int(k): i for i, k in enumerate(ks)}
+    for t in range(idx.size):
+        y = yk[a_i[t], kpos[int(k_i[t])]]
+        out[t] = np.sum(beta * y * p.V[sys_i[t], :])
+    return out
