@@ -1,0 +1,238 @@
+/*
+ * sv.h — C ABI of the B200-native HHL state-vector hot path (arXiv 2402.08136).
+ *
+ * The library (paper_2402_08136_b200/libhhlsv.so) simulates the HHL circuit of the
+ * paper by full state-vector evolution on sm_100a GPUs: "the most significant time
+ * sink is the unitary evolution of the state" (§II-C). Everything on
+ * the data path runs in the library's own CUDA kernels; there is NO CPU fallback —
+ * without a usable CUDA device every compute entry point returns SV_E_CUDA.
+ *
+ * Conventions (apply to every call):
+ *  - Amplitudes are complex128 stored interleaved (re, im) = CUDA double2.
+ *  - Qubit q is bit q of the LOGICAL amplitude index (little-endian; R1).
+ *    The library may keep a permuted physical layout internally (qubit relabelling,
+ *    global-qubit sharding) but every read/probability/slice is reported in logical
+ *    order.
+ *  - For a k-qubit matrix, targets[0] is the least-significant bit of its row and
+ *    column index; matrices are row-major 2^k × 2^k interleaved complex.
+ *  - The caller owns every buffer it passes; the library copies what it needs
+ *    (matrices, tables) before the call returns. Objects returned through `out`
+ *    pointers are owned by the library until the matching *_destroy call.
+ *  - Every call returns sv_status (0 = OK), never throws, never exits;
+ *    sv_last_error() gives a thread-local message for the last failure.
+ *  - Work is enqueued on the CUDA stream given to sv_create (NULL = legacy default
+ *    stream). Calls returning host data synchronise that stream; sv_apply_* and
+ *    sv_program_run are asynchronous.
+ */
+#ifndef HHLSV_SV_H
+#define HHLSV_SV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SV_OK = 0,
+    SV_E_ARG = 1,          /* bad argument: n < 1, qubit out of range/duplicated, k too large, null ptr, zero b */
+    SV_E_RANGE = 2,        /* index range outside the state */
+    SV_E_NOTUNITARY = 3,   /* ||U U^† - I||_max > 1e-10 (SPEC S:33 gate invariant) */
+    SV_E_NOTHERMITIAN = 4, /* A not symmetric within 1e-10 (Hermitian embedding is NEXT f3) */
+    SV_E_CLOCK = 5,        /* delta = 0: clock register too small for kappa (R5) */
+    SV_E_ZEROPROB = 6,     /* post-selection probability < 1e-12 */
+    SV_E_OOM = 7,          /* state or workspace does not fit in device memory */
+    SV_E_CUDA = 8,         /* CUDA error, or no CUDA device: there is no CPU fallback */
+    SV_E_NCCL = 9          /* NCCL error in a multi-GPU exchange/reduction */
+} sv_status;
+
+/* Thread-local human-readable message for the last non-OK status on this thread. */
+const char *sv_last_error(void);
+/* Library version string ("hhlsv <semver> sm_100a"). */
+const char *sv_version(void);
+
+/* ------------------------------------------------------------------ state ---- */
+typedef struct sv_state sv_state;   /* opaque; library-owned until sv_destroy */
+
+/* Multi-GPU descriptor: one process per GPU. The state of n qubits is
+ * sharded by its top log2(world) PHYSICAL qubits; rank r holds the 2^(n-g) amplitudes
+ * whose top g physical bits equal r. `nccl_id` points at the 128-byte ncclUniqueId
+ * that rank 0 created with sv_nccl_unique_id() and broadcast to all ranks (e.g. with
+ * torch.distributed). world must be a power of two. NULL dist = 1 GPU, no NCCL. */
+typedef struct {
+    int world;
+    int rank;
+    int device;
+    const unsigned char *nccl_id;
+} sv_dist;
+
+/* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only). SV_E_NCCL if NCCL cannot be loaded. */
+sv_status sv_nccl_unique_id(unsigned char out_id[128]);
+
+/* Allocate the (local shard of the) state on `dist->device` (or the current device)
+ * and initialise it to |0...0>. cuda_stream: a cudaStream_t (NULL = default stream).
+ * SV_E_ARG if n_qubits < 1 or n_qubits - log2(world) < 1; SV_E_OOM if it does not fit. */
+sv_status sv_create(int n_qubits, const sv_dist *dist, void *cuda_stream, sv_state **out);
+sv_status sv_destroy(sv_state *sv);
+/* Re-initialise to |0...0> and reset the logical->physical qubit map to identity. */
+sv_status sv_reset(sv_state *sv);
+/* Number of qubits / local amplitudes of this rank / the device pointer of the local shard
+ * (interleaved double2, PHYSICAL order; valid until sv_destroy). */
+sv_status sv_info(sv_state *sv, int *n_qubits, uint64_t *local_amps, void **device_ptr);
+/* Current logical->physical qubit map (n ints). */
+sv_status sv_qubit_map(sv_state *sv, int *phys_of_logical);
+/* Synchronise the library stream. */
+sv_status sv_sync(sv_state *sv);
+
+/* Read/write `count` amplitudes starting at LOGICAL index `first` to/from HOST memory
+ * (interleaved re,im; 2*count doubles). Multi-GPU: collective — every rank must call it;
+ * the values land on every rank. SV_E_RANGE if first+count > 2^n. Synchronous. */
+sv_status sv_read(sv_state *sv, uint64_t first, uint64_t count, double *interleaved_out);
+sv_status sv_write(sv_state *sv, uint64_t first, uint64_t count, const double *interleaved_in);
+
+/* ------------------------------------------------------------------ gates ---- */
+/* Fused-gate IR (SURVEY §2.2 D-FG; the paper's "single fused gate", Fig. 4).
+ *  SV_DENSE       targets (1..5): data = 2^k × 2^k matrix.
+ *  SV_CONTROLLED  targets (1..5) + controls (1..20) with required values `control_values`
+ *                 (bit i = value of controls[i]): data = 2^k × 2^k matrix applied where the
+ *                 controls match, identity elsewhere (QPE c-U^(2^j), Fig. 5).
+ *  SV_DIAGONAL    targets (1..12): data = 2^k diagonal entries (CP ladders of the (I)QFT).
+ *  SV_RECIP_RY    targets[0] = ancilla; controls = the clock register, LSB first (n_c = n_controls);
+ *                 data unused. Eigenvalue-inversion rotation (Fig. 5, settings of [qlsarepo],
+ *                 PAPER.md:225; R4/R6): for clock value m, L = 2^(n_c - recip_signed),
+ *                 m' = m, or 2^n_c - m with sign -1 when recip_signed and m >= 2^(n_c-1);
+ *                 r = recip_delta * L / m'; s = 1 if |r-1| <= recip_snap, r if r < 1, else 0
+ *                 (s = 0 at m = 0); the ancilla pair gets RY(2 asin(sign*s)).
+ *  SV_SWAP        targets = {a, b}: SWAP gate. Executed by relabelling (no data movement).
+ */
+typedef enum { SV_DENSE = 0, SV_CONTROLLED = 1, SV_DIAGONAL = 2, SV_RECIP_RY = 3, SV_SWAP = 4 } sv_kind;
+
+typedef struct {
+    int kind;                  /* sv_kind */
+    int n_targets;
+    const int *targets;
+    int n_controls;
+    const int *controls;
+    uint64_t control_values;
+    const double *data;        /* interleaved complex, see sv_kind */
+    double recip_delta;
+    int recip_signed;
+    double recip_snap;
+} sv_gate;
+
+/* Apply gates in order, each as ONE fused operation (no further matrix fusion; the engine
+ * may still execute several of them in one HBM pass — DESIGN.md §Passes). Matrices are
+ * validated (unitary to 1e-10) and copied. Asynchronous on the library stream. */
+sv_status sv_apply_fused(sv_state *sv, const sv_gate *gates, size_t n_gates);
+
+/* Fusion options. fusion_kmax: max dense/controlled target count after
+ * fusion (0 = no fusion, 2 = the paper's Fig. 4 mode, 1..5). diag_kmax: max diagonal width
+ * (<= 12). tile_qubits: qubits per shared-memory tile pass (0 = library default, -1 =
+ * one HBM pass per fused op). */
+typedef struct {
+    int fusion_kmax;
+    int diag_kmax;
+    int tile_qubits;
+} sv_fuse_options;
+
+typedef struct {
+    uint64_t n_logical;        /* gates in */
+    uint64_t n_fused;          /* fused ops out (excluding swaps, which relabel) */
+    uint64_t n_passes;         /* kernel launches over the state the schedule needs */
+    double alg_bytes;          /* sum over fused ops of their algorithmic bytes */
+    double pass_bytes;         /* HBM bytes the scheduled passes move (read + write) */
+} sv_plan_report;
+
+/* Run the a2 fusion pass on a LOGICAL gate list, then apply it (sv_apply_fused semantics). */
+sv_status sv_apply_circuit(sv_state *sv, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
+                           sv_plan_report *rep);
+
+/* ------------------------------------------------------------- programs ---- */
+/* A program is a fused, scheduled gate list resident in device memory (matrices uploaded
+ * once), bound to the state it was created for. Running it is stream-ordered and does no
+ * host work beyond kernel launches, so it can be timed or captured in a CUDA graph. */
+typedef struct sv_program sv_program;
+sv_status sv_program_create(sv_state *sv, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
+                            sv_program **out, sv_plan_report *rep);
+/* Runs the program. A program that starts with a state initialisation (hhl programs) resets
+ * the qubit map itself; otherwise the state's qubit map must equal the one at creation. */
+sv_status sv_program_run(sv_state *sv, sv_program *prog);
+sv_status sv_program_destroy(sv_program *prog);
+/* Text dump of the scheduled program (one step per line), for debugging/golden tests. */
+sv_status sv_program_dump(sv_program *prog, char *buf, size_t buf_len);
+/* Per-launch timing: when enabled, sv_program_run records a CUDA event pair around every
+ * kernel launch / exchange on the library stream; sv_program_timings returns the durations
+ * (ms) of the last run (synchronises the stream) with each step's kind (0 init-zero,
+ * 1 init-product, 2 dense/controlled, 3 diagonal, 4 recip-RY, 5 tile pass, 6 exchange),
+ * its HBM bytes per launch and how many kernel launches it made. */
+sv_status sv_program_set_timing(sv_program *prog, int enable);
+sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, int *launches, size_t cap,
+                             size_t *n_out);
+/* Number of kernel launches one sv_program_run makes on this rank, and the host->device
+ * bytes uploaded when the program was created. */
+sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_bytes);
+
+/* HOST-ONLY planning (no GPU needed): fuse + schedule a LOGICAL gate list for an n-qubit
+ * state sharded over `world` ranks (power of two), and dump the schedule text. Used to test
+ * the fusion pass and the global-qubit swap scheduler without a device. */
+sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t n_gates,
+                           const sv_fuse_options *opt, char *buf, size_t buf_len, sv_plan_report *rep);
+
+/* --------------------------------------------------------------- readout ---- */
+/* Marginal probabilities over LOGICAL `qubits` (bit j of the output index = qubits[j]):
+ * out[v] = sum |a_i|^2 over i with bits(i, qubits) = v. out has 2^n_q doubles (n_q <= 26).
+ * Deterministic fixed-order reduction (no fp64 atomics). Synchronous; collective when sharded. */
+sv_status sv_probabilities(sv_state *sv, const int *qubits, int n_q, double *out);
+/* Squared norm sum_i |a_i|^2 (deterministic). Synchronous; collective when sharded. */
+sv_status sv_norm2(sv_state *sv, double *out);
+/* Post-selection slice ("measure ancilla and get 1", read per DESIGN.md R7):
+ * the amplitudes whose LOGICAL qubits fixed_q[i] equal fixed_v[i], in increasing logical
+ * order of the remaining qubits. n_out must equal 2^(n - n_fixed) (<= 2^26). amps_out gets
+ * 2*n_out doubles, idx_out (optional) the logical indices, prob_out (optional) the summed
+ * probability. Synchronous; collective when sharded (results on every rank). */
+sv_status sv_postselect_slice(sv_state *sv, const int *fixed_q, const int *fixed_v, int n_fixed,
+                              double *amps_out, uint64_t *idx_out, uint64_t n_out, double *prob_out);
+
+/* ------------------------------------------------------------------- HHL ---- */
+/* HHL front end + solve ("Practical HHL procedures", Fig. 5, resources
+ * PAPER.md:225-242 read per DESIGN.md R2/R3). */
+typedef struct {
+    int clock_qubits;   /* n_c including the sign qubit; <= 0: max(n_b+1, ceil(log2(kappa+1))) + 1 */
+    int fusion_kmax;    /* 0 -> library default (4) ; -1 -> no fusion */
+    int tile_qubits;    /* 0 -> library default ; -1 -> one pass per fused op */
+    double recip_snap;  /* reciprocal snapping tolerance (qlsarepo: 1e-5); < 0 -> default 1e-5 */
+    int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; -1: don't */
+} hhl_options;
+
+typedef struct {
+    double p_success;   /* P(ancilla = 1 and clock = 0) (R7) */
+    double norm2;       /* ||psi||^2 after the circuit (should be 1) */
+    double lambda_min, lambda_max, kappa, delta, t_evol;
+    int n_data, n_clock, n_total;
+    uint64_t n_logical, n_fused, n_passes;
+    double alg_bytes, pass_bytes;
+    double t_frontend_s, t_sim_s;
+    double h2d_bytes, d2h_bytes;   /* host<->device bytes of one solve (program upload, slice read) */
+} hhl_report;
+
+/* Build the HHL circuit for A (N×N, row-major, real symmetric) and b (N) and return it as a
+ * program for `sv` (which must have n_b + n_c + 1 qubits; call hhl_plan_size first).
+ * On return *b_norm, *lambda_min are what hhl_recover needs. */
+sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_options *opt, int *n_data,
+                        int *n_clock, int *n_total);
+sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
+                            sv_program **out, hhl_report *rep);
+/* Read out and recover x (PAPER.md:193-198 read per F3/R8): x = ||b|| sqrt(P)/lambda_min |x>,
+ * |x> = slice / sqrt(P), padding stripped; x_out has N doubles (real part). */
+sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out,
+                      double *p_success);
+/* Everything at once: create the state, build, run, read out, recover, destroy.
+ * A, b, x_out are HOST buffers. dist = NULL for 1 GPU. */
+sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, const hhl_options *opt,
+                    const sv_dist *dist, void *cuda_stream, double *x_out, hhl_report *rep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HHLSV_SV_H */

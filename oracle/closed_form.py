@@ -20,6 +20,14 @@ from __future__ import annotations
 
 import numpy as np
 
+try:                                   # multi-threaded FFT for the 2^25-point transforms at S30
+    import scipy.fft as _fft
+
+    def _ifft(x):
+        return _fft.ifft(x, workers=-1)
+except Exception:                      # pragma: no cover
+    _ifft = np.fft.ifft
+
 
 def recip_table(n_c: int, delta: float, signed: int = 1, snap: float = 0.0) -> np.ndarray:
     """s_m for m = 0..2^n_c - 1 (definition in SURVEY §8(a) a7 / DESIGN.md R6)."""
@@ -49,6 +57,41 @@ def phase_vector(phi: float, n_c: int) -> np.ndarray:
     return ph
 
 
+def alpha_geometric(phi: float, n_c: int) -> np.ndarray:
+    """alpha_m(phi) for all m by the geometric series N^-1 (e^{2 pi i N d} - 1)/(e^{2 pi i d} - 1),
+    d = phi - m/N, with e^{2 pi i N d} = e^{2 pi i frac(N phi)} and e^{2 pi i d} - 1 =
+    2i sin(pi d) e^{i pi d}. phi - m/N is exact near the peak (Sterbenz), so this is accurate
+    where alpha is large. Equal to fft(phase_vector)/N (pinned in tests)."""
+    Nc = 1 << n_c
+    d = phi - np.arange(Nc, dtype=np.float64) / Nc
+    x = np.ldexp(phi, n_c)
+    F = x - np.floor(x)
+    num = complex(np.cos(2 * np.pi * F) - 1.0, np.sin(2 * np.pi * F))
+    pd = np.pi * d
+    sd = np.sin(pd)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / (2.0 * Nc * sd)
+    # num / (2i sd e^{i pi d} N) = num * (-i) e^{-i pi d} / (2 sd N)
+    w = num * -1j
+    with np.errstate(invalid="ignore"):
+        a = (w * inv) * (np.cos(pd) - 1j * sd)
+    a[sd == 0.0] = 1.0
+    return a
+
+
+def alpha_abs2(phi: float, n_c: int) -> np.ndarray:
+    """|alpha_m(phi)|^2 = sin^2(pi N d) / (N^2 sin^2(pi d)) (Fejér kernel), sin(pi N d) = ±sin(pi frac(N phi))."""
+    Nc = 1 << n_c
+    d = phi - np.arange(Nc, dtype=np.float64) / Nc
+    x = np.ldexp(phi, n_c)
+    sF = np.sin(np.pi * (x - np.floor(x)))
+    sd = np.sin(np.pi * d)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = (sF / Nc) ** 2 / (sd * sd)
+    r[sd == 0.0] = 1.0
+    return r
+
+
 def fwht(v: np.ndarray) -> np.ndarray:
     """Normalised Walsh–Hadamard transform H^{⊗n} v (little-endian, any bit order is the same)."""
     v = v.copy()
@@ -68,12 +111,12 @@ def fwht(v: np.ndarray) -> np.ndarray:
 def _y_vectors(phi: float, n_c: int, s_tab: np.ndarray):
     Nc = 1 << n_c
     ph = phase_vector(phi, n_c)
-    alpha = np.fft.fft(ph) / Nc                       # alpha_m = N^-1 sum_k e^{2 pi i k phi} e^{-2 pi i k m/N}
+    alpha = alpha_geometric(phi, n_c) if n_c > 16 else np.fft.fft(ph) / Nc                      # alpha_m = N^-1 sum_k e^{2 pi i k phi} e^{-2 pi i k m/N}
     r1 = s_tab
     r0 = np.sqrt(1.0 - s_tab ** 2)
     out = []
     for r in (r0, r1):
-        z = np.fft.ifft(r * alpha) * np.sqrt(Nc)       # F (r ⊙ alpha)
+        z = _ifft(r * alpha) * np.sqrt(Nc)       # F (r ⊙ alpha)
         out.append(np.conj(ph) * z)                    # controlled-U^† phases, before the final H layer
     return out
 
@@ -104,8 +147,8 @@ def postselected(p):
     beta = p.V.T @ p.b_hat
     x = np.zeros(p.A.shape[0])
     for s in range(beta.size):
-        alpha = np.fft.fft(phase_vector(p.phi[s], nc)) / Nc
-        x += beta[s] * p.V[:, s] * float(np.sum(np.abs(alpha) ** 2 * s_tab))
+        a2 = alpha_abs2(p.phi[s], nc) if nc > 16 else np.abs(np.fft.fft(phase_vector(p.phi[s], nc)) / Nc) ** 2
+        x += beta[s] * p.V[:, s] * float(np.sum(a2 * s_tab))
     return x, float(x @ x)
 
 

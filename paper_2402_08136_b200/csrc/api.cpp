@@ -1,0 +1,403 @@
+// The extern "C" boundary declared in include/sv.h. Argument marshalling and error
+// translation only; all data-path work happens in the CUDA kernels behind engine.cu.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "engine.h"
+
+using namespace hhlsv;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+sv_status guard(F &&f) {
+    try {
+        f();
+        return SV_OK;
+    } catch (const Error &e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_last_error = "host out of memory";
+        return SV_E_OOM;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return SV_E_ARG;
+    }
+}
+
+std::vector<Gate> gates_in_n(int nq, const sv_gate *g, size_t n) {
+    if (n && !g) fail(SV_E_ARG, "null gate array");
+    std::vector<Gate> out;
+    out.reserve(n);
+    for (size_t i = 0; i < n; i++) out.push_back(gate_from_abi(g[i], nq));
+    return out;
+}
+
+std::vector<Gate> gates_in(const sv_state *sv, const sv_gate *g, size_t n) { return gates_in_n(sv->n, g, n); }
+
+FuseOptions fuse_opts(const sv_fuse_options *o) {
+    FuseOptions f;
+    if (o) {
+        f.kmax = o->fusion_kmax;
+        if (o->diag_kmax > 0) f.diag_kmax = o->diag_kmax;
+    }
+    if (f.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
+    if (f.diag_kmax > 12) fail(SV_E_ARG, "diag_kmax must be <= 12");
+    return f;
+}
+
+CompileOptions compile_opts(const sv_fuse_options *o) {
+    CompileOptions c;
+    if (o && o->tile_qubits != 0) c.tile_qubits = o->tile_qubits;
+    return c;
+}
+
+void fill_plan_report(const sv_program *p, sv_plan_report *rep) {
+    if (!rep) return;
+    rep->n_logical = p->n_logical;
+    rep->n_fused = p->sched.n_fused;
+    rep->n_passes = p->sched.n_passes;
+    rep->alg_bytes = p->sched.alg_bytes;
+    rep->pass_bytes = p->sched.pass_bytes;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+extern "C" {
+
+const char *sv_last_error(void) { return g_last_error.c_str(); }
+const char *sv_version(void) { return "hhlsv 0.1.0 sm_100a"; }
+
+sv_status sv_nccl_unique_id(unsigned char out_id[128]) {
+    return guard([&] {
+        if (!out_id) fail(SV_E_ARG, "null id buffer");
+        if (nccl_unique_id(out_id)) fail(SV_E_NCCL, std::string("ncclGetUniqueId: ") + nccl_last_error());
+    });
+}
+
+sv_status sv_create(int n_qubits, const sv_dist *dist, void *cuda_stream, sv_state **out) {
+    return guard([&] {
+        if (!out) fail(SV_E_ARG, "null out");
+        *out = nullptr;
+        *out = state_create(n_qubits, dist, (cudaStream_t)cuda_stream);
+    });
+}
+
+sv_status sv_destroy(sv_state *sv) {
+    return guard([&] { state_destroy(sv); });
+}
+
+sv_status sv_reset(sv_state *sv) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_reset(sv);
+    });
+}
+
+sv_status sv_info(sv_state *sv, int *n, uint64_t *local_amps, void **ptr) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        if (n) *n = sv->n;
+        if (local_amps) *local_amps = sv->local_amps();
+        if (ptr) *ptr = sv->psi;
+    });
+}
+
+sv_status sv_qubit_map(sv_state *sv, int *phys) {
+    return guard([&] {
+        if (!sv || !phys) fail(SV_E_ARG, "null argument");
+        for (int q = 0; q < sv->n; q++) phys[q] = sv->phys[q];
+    });
+}
+
+sv_status sv_sync(sv_state *sv) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        cuda_check(cudaStreamSynchronize(sv->stream), "sync");
+    });
+}
+
+sv_status sv_read(sv_state *sv, uint64_t first, uint64_t count, double *out) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_read(sv, first, count, out);
+    });
+}
+
+sv_status sv_write(sv_state *sv, uint64_t first, uint64_t count, const double *in) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_write(sv, first, count, in);
+    });
+}
+
+sv_status sv_apply_fused(sv_state *sv, const sv_gate *gates, size_t n_gates) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        auto g = gates_in(sv, gates, n_gates);
+        sv_program *p = program_create(sv, g, nullptr, CompileOptions{}, n_gates);
+        try {
+            program_run(sv, p);
+        } catch (...) {
+            program_destroy(p);
+            throw;
+        }
+        program_destroy(p);
+    });
+}
+
+sv_status sv_apply_circuit(sv_state *sv, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
+                           sv_plan_report *rep) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        auto g = fuse(gates_in(sv, gates, n_gates), fuse_opts(opt));
+        sv_program *p = program_create(sv, g, nullptr, compile_opts(opt), n_gates);
+        fill_plan_report(p, rep);
+        try {
+            program_run(sv, p);
+        } catch (...) {
+            program_destroy(p);
+            throw;
+        }
+        program_destroy(p);
+    });
+}
+
+sv_status sv_program_create(sv_state *sv, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
+                            sv_program **out, sv_plan_report *rep) {
+    return guard([&] {
+        if (!sv || !out) fail(SV_E_ARG, "null argument");
+        *out = nullptr;
+        auto g = fuse(gates_in(sv, gates, n_gates), fuse_opts(opt));
+        *out = program_create(sv, g, nullptr, compile_opts(opt), n_gates);
+        fill_plan_report(*out, rep);
+    });
+}
+
+sv_status sv_program_run(sv_state *sv, sv_program *prog) {
+    return guard([&] {
+        if (!sv || !prog) fail(SV_E_ARG, "null argument");
+        program_run(sv, prog);
+    });
+}
+
+sv_status sv_program_destroy(sv_program *prog) {
+    return guard([&] { program_destroy(prog); });
+}
+
+sv_status sv_program_dump(sv_program *prog, char *buf, size_t len) {
+    return guard([&] {
+        if (!prog || !buf || len == 0) fail(SV_E_ARG, "null argument");
+        std::string s = dump_schedule(prog->sched);
+        size_t n = std::min(len - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    });
+}
+
+sv_status sv_program_set_timing(sv_program *prog, int enable) {
+    return guard([&] {
+        if (!prog) fail(SV_E_ARG, "null program");
+        prog->timing = enable != 0;
+    });
+}
+
+sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, int *launches, size_t cap,
+                             size_t *n_out) {
+    return guard([&] {
+        if (!prog) fail(SV_E_ARG, "null program");
+        program_timings(prog, ms, kind, bytes, launches, cap, n_out);
+    });
+}
+
+sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_bytes) {
+    return guard([&] {
+        if (!prog) fail(SV_E_ARG, "null program");
+        if (launches) *launches = prog->launches();
+        if (h2d_bytes) *h2d_bytes = (uint64_t)prog->h2d_bytes;
+    });
+}
+
+sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
+                           char *buf, size_t buf_len, sv_plan_report *rep) {
+    return guard([&] {
+        if (world < 1 || (world & (world - 1))) fail(SV_E_ARG, "world must be a power of two");
+        int g = 0;
+        while ((1 << g) < world) g++;
+        if (n_qubits < 1 || n_qubits - g < 1 || n_qubits > 62) fail(SV_E_ARG, "n_qubits out of range");
+        auto gl = fuse(gates_in_n(n_qubits, gates, n_gates), fuse_opts(opt));
+        std::vector<int> phys(n_qubits);
+        for (int q = 0; q < n_qubits; q++) phys[q] = q;
+        CompileOptions co = compile_opts(opt);
+        if (co.tile_qubits > 14) co.tile_qubits = 14;
+        Schedule s = compile(gl, nullptr, n_qubits, n_qubits - g, phys, co);
+        if (rep) {
+            rep->n_logical = n_gates;
+            rep->n_fused = s.n_fused;
+            rep->n_passes = s.n_passes;
+            rep->alg_bytes = s.alg_bytes;
+            rep->pass_bytes = s.pass_bytes;
+        }
+        if (buf && buf_len) {
+            std::string t = dump_schedule(s);
+            std::string perm = "FINAL_MAP";
+            for (int q = 0; q < n_qubits; q++) perm += " " + std::to_string(s.phys_out[q]);
+            t += perm + "\n";
+            size_t n = std::min(buf_len - 1, t.size());
+            std::memcpy(buf, t.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+sv_status sv_probabilities(sv_state *sv, const int *qubits, int n_q, double *out) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_probabilities(sv, qubits, n_q, out);
+    });
+}
+
+sv_status sv_norm2(sv_state *sv, double *out) {
+    return guard([&] {
+        if (!sv || !out) fail(SV_E_ARG, "null argument");
+        *out = state_norm2(sv);
+    });
+}
+
+sv_status sv_postselect_slice(sv_state *sv, const int *fixed_q, const int *fixed_v, int n_fixed, double *amps_out,
+                              uint64_t *idx_out, uint64_t n_out, double *prob_out) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_postselect(sv, fixed_q, fixed_v, n_fixed, amps_out, idx_out, n_out, prob_out);
+    });
+}
+
+// ------------------------------------------------------------------- HHL ----
+static double opt_snap(const hhl_options *o) { return (o && o->recip_snap >= 0.0) ? o->recip_snap : 1e-5; }
+
+sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_options *opt, int *n_data, int *n_clock,
+                        int *n_total) {
+    return guard([&] {
+        HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+        if (n_data) *n_data = p.n_b;
+        if (n_clock) *n_clock = p.n_c;
+        if (n_total) *n_total = p.n;
+    });
+}
+
+static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
+                             hhl_report *rep, double *b_norm_out) {
+    const double t0 = now_s();
+    HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+    if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
+    std::vector<Gate> gates = hhl_build(p);
+    const bool fold = !opt || opt->init_fold >= 0;
+    std::vector<ProductFactor> factors;
+    size_t nf = fold ? fold_product_prefix(gates, p.n, factors) : 0;
+    std::vector<Gate> rest(gates.begin() + nf, gates.end());
+    FuseOptions fo;
+    if (opt && opt->fusion_kmax != 0) fo.kmax = opt->fusion_kmax < 0 ? 0 : opt->fusion_kmax;
+    if (fo.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
+    std::vector<Gate> fused = fuse(rest, fo);
+    CompileOptions co;
+    if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
+    sv_program *prog = program_create(sv, fused, &factors, co, gates.size());
+    if (rep) {
+        std::memset(rep, 0, sizeof(*rep));
+        rep->lambda_min = p.lam_min;
+        rep->lambda_max = p.lam_max;
+        rep->kappa = p.kappa;
+        rep->delta = p.delta;
+        rep->t_evol = p.t;
+        rep->n_data = p.n_b;
+        rep->n_clock = p.n_c;
+        rep->n_total = p.n;
+        rep->n_logical = gates.size();
+        rep->n_fused = prog->sched.n_fused;
+        rep->n_passes = prog->sched.n_passes;
+        rep->alg_bytes = prog->sched.alg_bytes;
+        rep->pass_bytes = prog->sched.pass_bytes;
+        rep->h2d_bytes = prog->h2d_bytes;
+        rep->d2h_bytes = 16.0 * (double)(1ull << p.n_b) + 8.0;
+        rep->t_frontend_s = now_s() - t0;
+    }
+    if (b_norm_out) *b_norm_out = p.b_norm;
+    return prog;
+}
+
+sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
+                            sv_program **out, hhl_report *rep) {
+    return guard([&] {
+        if (!sv || !out) fail(SV_E_ARG, "null argument");
+        *out = nullptr;
+        *out = build_hhl(sv, A, b, N, opt, rep, nullptr);
+    });
+}
+
+static void readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_out) {
+    const int nb = rep->n_data, nc = rep->n_clock, n = rep->n_total;
+    if (n != sv->n) fail(SV_E_ARG, "report does not match the state");
+    std::vector<int> fq, fv;
+    for (int j = 0; j < nc; j++) {
+        fq.push_back(nb + j);
+        fv.push_back(0);
+    }
+    fq.push_back(n - 1);
+    fv.push_back(1);
+    const uint64_t m = 1ull << nb;
+    std::vector<double> amps(2 * m);
+    double P = 0.0;
+    state_postselect(sv, fq.data(), fv.data(), (int)fq.size(), amps.data(), nullptr, m, &P);
+    if (p_out) *p_out = P;
+    if (P < 1e-12) fail(SV_E_ZEROPROB, "post-selection probability below 1e-12");
+    // x = ||b|| sqrt(P)/lambda_min * slice/sqrt(P)   (PAPER.md:193-198 read per F3/R8)
+    if (x_out)
+        for (int i = 0; i < N; i++) x_out[i] = b_norm * amps[2 * i] / rep->lambda_min;
+}
+
+sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_success) {
+    return guard([&] {
+        if (!sv || !rep) fail(SV_E_ARG, "null argument");
+        readout(sv, rep, N, b_norm, x_out, p_success);
+    });
+}
+
+sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, const hhl_options *opt,
+                    const sv_dist *dist, void *cuda_stream, double *x_out, hhl_report *rep) {
+    return guard([&] {
+        if (!x_out) fail(SV_E_ARG, "null x_out");
+        hhl_options o{};
+        if (opt) o = *opt;
+        if (clock_qubits > 0) o.clock_qubits = clock_qubits;
+        if (!opt) o.recip_snap = -1.0;
+        HHLPlanHost p = hhl_plan(A, b, N, o.clock_qubits, opt_snap(&o));
+        sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream);
+        sv_program *prog = nullptr;
+        try {
+            hhl_report r{};
+            double bn = 0.0;
+            prog = build_hhl(sv, A, b, N, &o, &r, &bn);
+            const double t0 = now_s();
+            program_run(sv, prog);
+            r.norm2 = state_norm2(sv);
+            readout(sv, &r, N, bn, x_out, &r.p_success);
+            r.t_sim_s = now_s() - t0;
+            if (rep) *rep = r;
+        } catch (...) {
+            program_destroy(prog);
+            state_destroy(sv);
+            throw;
+        }
+        program_destroy(prog);
+        state_destroy(sv);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// Scheduler: logical fused ops -> physical steps (§Multi-GPU).
+//
+//  * SWAP ops are executed by relabelling the logical->physical qubit map (no data
+//    movement; SURVEY §8(c) item 12 allows the GPU to drop IQFT swaps this way as long
+//    as the final logical state is identical — all readout goes through the map).
+//  * Multi-GPU ("PGAS-based SHMEM", "minimize unnecessary data
+//    migration"): the top g physical bits are global. An op whose
+//    non-diagonal target sits on a global bit first gets an Exchange step that swaps
+//    that global bit with a local bit chosen by farthest next use (Belady); controls,
+//    diagonal qubits and reciprocal clock bits on global bits never move data.
+//  * Tile passes: consecutive ops whose non-diagonal targets fit in a
+//    T-qubit local set are executed in ONE HBM pass: each CTA stages the 2^T amplitudes
+//    spanned by the set (padded with the lowest bits for coalescing) in shared memory,
+//    applies all ops, and writes back. Without tiles, every op is one streaming pass.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <sstream>
+
+#include "sv_internal.h"
+
+namespace hhlsv {
+
+// Non-diagonal targets of an op (the bits whose values it mixes).
+static std::vector<int> nd_targets(const Gate &g) {
+    switch (g.kind) {
+        case Kind::Dense:
+        case Kind::Controlled:
+        case Kind::RecipRY: return g.targets;
+        default: return {};
+    }
+}
+
+static Gate to_physical(const Gate &g, const std::vector<int> &phys) {
+    Gate p = g;
+    for (int &q : p.targets) q = phys[q];
+    for (int &q : p.controls) q = phys[q];
+    return p;
+}
+
+Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> *init, int n, int nloc,
+                 const std::vector<int> &phys_in, const CompileOptions &o) {
+    Schedule s;
+    std::vector<int> phys = phys_in;
+    const double local_amps = std::ldexp(1.0, nloc);
+    if (init) {
+        Step st;
+        st.kind = StepKind::InitProduct;
+        st.factors = *init;
+        for (auto &f : st.factors)
+            for (int &q : f.qubits) q = phys[q];
+        st.bytes = 16.0 * local_amps;
+        s.steps.push_back(std::move(st));
+        s.pass_bytes += 16.0 * local_amps;
+        s.n_passes++;
+    }
+    const int T = std::min(o.tile_qubits, nloc);
+    const bool tiles = o.tile_qubits > 0;
+
+    // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.
+    std::vector<std::vector<size_t>> uses(n);
+    for (size_t i = 0; i < ops.size(); i++)
+        for (int q : nd_targets(ops[i])) uses[q].push_back(i);
+    auto next_use = [&](int logical, size_t from) -> size_t {
+        auto &u = uses[logical];
+        auto it = std::lower_bound(u.begin(), u.end(), from);
+        return it == u.end() ? SIZE_MAX : *it;
+    };
+
+    Step tile;
+    bool tile_open = false;
+    std::vector<int> tile_nd;    // physical nd bits of the open tile
+    auto close_tile = [&]() {
+        if (!tile_open) return;
+        // local set: nd bits, filled with the lowest local bits for contiguous segments
+        std::vector<int> set = tile_nd;
+        for (int b = 0; (int)set.size() < T && b < nloc; b++)
+            if (std::find(set.begin(), set.end(), b) == set.end()) set.push_back(b);
+        std::sort(set.begin(), set.end());
+        tile.tile_bits = set;
+        tile.bytes = 32.0 * local_amps;
+        s.pass_bytes += tile.bytes;
+        s.n_passes++;
+        s.steps.push_back(std::move(tile));
+        tile = Step();
+        tile_open = false;
+        tile_nd.clear();
+    };
+
+    for (size_t i = 0; i < ops.size(); i++) {
+        const Gate &g = ops[i];
+        if (g.kind == Kind::Swap) {
+            std::swap(phys[g.targets[0]], phys[g.targets[1]]);
+            continue;
+        }
+        s.n_fused++;
+        s.alg_bytes += alg_bytes(g, n);
+        // ---- bring non-diagonal targets local (multi-GPU)
+        std::vector<int> nd = nd_targets(g);
+        for (int q : nd) {
+            if (phys[q] < nloc) continue;
+            close_tile();
+            // victim: local logical qubit, not a target of g, farthest next nd use
+            int victim = -1;
+            size_t best = 0;
+            for (int l = 0; l < n; l++) {
+                if (phys[l] >= nloc) continue;
+                if (std::find(nd.begin(), nd.end(), l) != nd.end()) continue;
+                size_t nu = next_use(l, i);
+                // prefer high physical bits on ties (contiguous halves)
+                if (victim < 0 || nu > best || (nu == best && phys[l] > phys[victim])) {
+                    victim = l;
+                    best = nu;
+                }
+            }
+            if (victim < 0) fail(SV_E_ARG, "no local qubit available for a global swap");
+            Step ex;
+            ex.kind = StepKind::Exchange;
+            ex.gbit = phys[q];
+            ex.lbit = phys[victim];
+            ex.bytes = 2.0 * 16.0 * local_amps / 2.0;     // half the shard out and in (NVLink)
+            s.steps.push_back(ex);
+            std::swap(phys[q], phys[victim]);
+        }
+        Gate pg = to_physical(g, phys);
+        if (!tiles) {
+            Step st;
+            switch (g.kind) {
+                case Kind::Dense:
+                case Kind::Controlled:
+                    st.kind = StepKind::Dense;
+                    st.k = (int)pg.targets.size();
+                    for (int t = 0; t < st.k; t++) st.tpos[t] = pg.targets[t];
+                    st.ctrl_bits = pg.controls;
+                    st.cvals = pg.cvals;
+                    break;
+                case Kind::Diagonal:
+                    st.kind = StepKind::Diagonal;
+                    st.dbits = pg.targets;
+                    break;
+                case Kind::RecipRY:
+                    st.kind = StepKind::RecipRY;
+                    st.anc = pg.targets[0];
+                    st.clock_bits = pg.controls;
+                    st.delta = pg.delta;
+                    st.snap = pg.snap;
+                    st.is_signed = pg.is_signed;
+                    break;
+                default: break;
+            }
+            st.tile_ops.push_back(pg);   // keeps the data for upload
+            double by = alg_bytes(g, nloc);
+            for (int c : pg.controls)
+                if (g.kind == Kind::Controlled && c >= nloc) by *= 2.0;   // global control: all-or-nothing per rank
+            st.bytes = by;
+            s.pass_bytes += by;
+            s.n_passes++;
+            s.steps.push_back(std::move(st));
+            continue;
+        }
+        // ---- tile grouping
+        std::vector<int> pnd;
+        for (int q : nd) pnd.push_back(phys[q]);
+        std::vector<int> u = tile_nd;
+        for (int b : pnd)
+            if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
+        if (tile_open && (int)u.size() > T) {
+            close_tile();
+            u = pnd;
+        }
+        if (!tile_open) {
+            tile = Step();
+            tile.kind = StepKind::Tile;
+            tile_open = true;
+        }
+        tile_nd = u;
+        tile.tile_ops.push_back(std::move(pg));
+    }
+    close_tile();
+    s.phys_out = phys;
+    return s;
+}
+
+std::string dump_schedule(const Schedule &s) {
+    std::ostringstream os;
+    auto bits = [&](const std::vector<int> &v) {
+        std::ostringstream b;
+        for (size_t i = 0; i < v.size(); i++) b << (i ? "," : "") << v[i];
+        return b.str();
+    };
+    for (const Step &st : s.steps) {
+        switch (st.kind) {
+            case StepKind::InitZero: os << "INIT_ZERO\n"; break;
+            case StepKind::InitProduct:
+                os << "INIT_PRODUCT factors=" << st.factors.size() << "\n";
+                break;
+            case StepKind::Dense:
+                os << (st.ctrl_bits.empty() ? "DENSE" : "CONTROLLED") << " k=" << st.k << " t="
+                   << bits(std::vector<int>(st.tpos, st.tpos + st.k)) << " c=" << bits(st.ctrl_bits) << "\n";
+                break;
+            case StepKind::Diagonal: os << "DIAGONAL q=" << bits(st.dbits) << "\n"; break;
+            case StepKind::RecipRY: os << "RECIP_RY anc=" << st.anc << " clock=" << bits(st.clock_bits) << "\n"; break;
+            case StepKind::Exchange: os << "EXCHANGE global=" << st.gbit << " local=" << st.lbit << "\n"; break;
+            case StepKind::Tile: {
+                os << "TILE bits=" << bits(st.tile_bits) << " ops=" << st.tile_ops.size() << "\n";
+                for (const Gate &g : st.tile_ops) {
+                    const char *nm = g.kind == Kind::Dense ? "dense" : g.kind == Kind::Controlled ? "controlled"
+                                     : g.kind == Kind::Diagonal ? "diagonal" : "recip_ry";
+                    os << "  " << nm << " t=" << bits(g.targets) << " c=" << bits(g.controls) << "\n";
+                }
+                break;
+            }
+        }
+    }
+    return os.str();
+}
+
+}  // namespace hhlsv

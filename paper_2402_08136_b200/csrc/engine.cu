@@ -1,0 +1,667 @@
+// Device state, resident programs and readout.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "engine.h"
+
+namespace hhlsv {
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) fail(SV_E_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(SV_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void nccl_check(int rc, const char *what) {
+    if (rc) fail(SV_E_NCCL, std::string(what) + ": " + nccl_last_error());
+}
+
+// ------------------------------------------------------------------ state ----
+sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        fail(SV_E_CUDA, "no CUDA device: this library has no CPU fallback");
+    }
+    int world = 1, rank = 0, device = -1;
+    if (dist) {
+        world = dist->world;
+        rank = dist->rank;
+        device = dist->device;
+        if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world)
+            fail(SV_E_ARG, "sv_dist: world must be a power of two and 0 <= rank < world");
+        if (world > 1 && !dist->nccl_id) fail(SV_E_ARG, "sv_dist: nccl_id required for world > 1");
+    }
+    int g = 0;
+    while ((1 << g) < world) g++;
+    if (n < 1 || n - g < 1 || n > 62) fail(SV_E_ARG, "n_qubits out of range");
+    if (device >= 0) cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    else cuda_check(cudaGetDevice(&device), "cudaGetDevice");
+    std::unique_ptr<sv_state> sv(new sv_state());
+    sv->n = n;
+    sv->g = g;
+    sv->nloc = n - g;
+    sv->world = world;
+    sv->rank = rank;
+    sv->device = device;
+    sv->stream = stream;
+    sv->phys.resize(n);
+    std::iota(sv->phys.begin(), sv->phys.end(), 0);
+    const size_t bytes = sizeof(double2) << sv->nloc;
+    size_t freeb = 0, totb = 0;
+    cuda_check(cudaMemGetInfo(&freeb, &totb), "cudaMemGetInfo");
+    if (bytes > freeb) fail(SV_E_OOM, "state does not fit in device memory");
+    cuda_check(cudaMalloc(&sv->psi, bytes), "cudaMalloc(state)");
+    sv->red_len = dev::kRedBlocks;
+    cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * sv->red_len), "cudaMalloc(red)");
+    cuda_check(cudaMalloc(&sv->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
+    if (world > 1) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
+    state_reset(sv.get());
+    return sv.release();
+}
+
+void state_destroy(sv_state *sv) {
+    if (!sv) return;
+    cudaStreamSynchronize(sv->stream);
+    cudaFree(sv->psi);
+    cudaFree(sv->d_red);
+    cudaFree(sv->d_scalar);
+    cudaFree(sv->d_io);
+    cudaFree(sv->d_xsend);
+    cudaFree(sv->d_xrecv);
+    nccl_destroy(sv->comm);
+    delete sv;
+}
+
+void state_reset(sv_state *sv) {
+    std::iota(sv->phys.begin(), sv->phys.end(), 0);
+    cuda_check(dev::launch_zero_init(sv->psi, sv->local_amps(), sv->rank == 0, sv->stream), "init zero");
+}
+
+static void ensure_io(sv_state *sv, size_t n2) {
+    if (sv->io_len >= n2) return;
+    cudaFree(sv->d_io);
+    sv->d_io = nullptr;
+    sv->io_len = 0;
+    cuda_check(cudaMalloc(&sv->d_io, sizeof(double2) * n2), "cudaMalloc(io)");
+    sv->io_len = n2;
+}
+
+static void ensure_red(sv_state *sv, size_t n) {
+    if (sv->red_len >= n) return;
+    cudaFree(sv->d_red);
+    sv->d_red = nullptr;
+    cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * n), "cudaMalloc(red)");
+    sv->red_len = n;
+}
+
+// --------------------------------------------------------------- exchange ----
+// Swap physical global bit gbit with local bit lbit: send the half of the shard whose
+// lbit differs from this rank's gbit value to the partner rank, receive its half into
+// the same positions. Chunked: no half-state receive buffer.
+static void exchange(sv_state *sv, int gbit, int lbit) {
+    const int gb = gbit - sv->nloc;
+    const int partner = sv->rank ^ (1 << gb);
+    const int beta = (sv->rank >> gb) & 1;
+    const int val = 1 - beta;
+    const uint64_t half = sv->local_amps() >> 1;
+    const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);   // 1 GiB
+    if (sv->x_len < chunk) {
+        cudaFree(sv->d_xsend);
+        cudaFree(sv->d_xrecv);
+        sv->d_xsend = sv->d_xrecv = nullptr;
+        cuda_check(cudaMalloc(&sv->d_xsend, sizeof(double2) * chunk), "cudaMalloc(xsend)");
+        cuda_check(cudaMalloc(&sv->d_xrecv, sizeof(double2) * chunk), "cudaMalloc(xrecv)");
+        sv->x_len = chunk;
+    }
+    const bool top = lbit == sv->nloc - 1;
+    for (uint64_t off = 0; off < half; off += chunk) {
+        const uint64_t cnt = std::min(chunk, half - off);
+        const double2 *sendp;
+        if (top) {
+            sendp = sv->psi + (uint64_t)val * half + off;
+        } else {
+            cuda_check(dev::launch_pack(sv->psi, sv->d_xsend, lbit, val, off, cnt, sv->stream), "pack");
+            sendp = sv->d_xsend;
+        }
+        nccl_check(nccl_sendrecv(sv->comm, (const double *)sendp, (double *)sv->d_xrecv, 2 * cnt, partner,
+                                 sv->stream),
+                   "exchange sendrecv");
+        if (top)
+            cuda_check(cudaMemcpyAsync(sv->psi + (uint64_t)val * half + off, sv->d_xrecv, sizeof(double2) * cnt,
+                                       cudaMemcpyDeviceToDevice, sv->stream),
+                       "exchange copy");
+        else
+            cuda_check(dev::launch_unpack(sv->psi, sv->d_xrecv, lbit, val, off, cnt, sv->stream), "unpack");
+    }
+}
+
+// ---------------------------------------------------------------- program ----
+static int index_in(const std::vector<int> &v, int x) {
+    auto it = std::find(v.begin(), v.end(), x);
+    return it == v.end() ? -1 : (int)(it - v.begin());
+}
+
+static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec) {
+    // group factors (physical bits) into <= 4 chunks of <= 12 bits, each a tensor-product table
+    std::vector<const ProductFactor *> fs;
+    for (auto &f : st.factors) fs.push_back(&f);
+    std::sort(fs.begin(), fs.end(), [](const ProductFactor *a, const ProductFactor *b) {
+        return *std::min_element(a->qubits.begin(), a->qubits.end()) <
+               *std::min_element(b->qubits.begin(), b->qubits.end());
+    });
+    std::vector<std::vector<int>> cb;
+    std::vector<std::vector<cplx>> ct;
+    uint64_t covered = 0;
+    for (const ProductFactor *f : fs) {
+        if (cb.empty() || cb.back().size() + f->qubits.size() > 12) {
+            cb.emplace_back();
+            ct.push_back({cplx(1.0, 0.0)});
+        }
+        auto &bits = cb.back();
+        auto &tab = ct.back();
+        const size_t lo = tab.size();
+        std::vector<cplx> nt(lo * f->vec.size());
+        for (size_t x = 0; x < nt.size(); x++) nt[x] = tab[x % lo] * f->vec[x / lo];
+        tab.swap(nt);
+        for (int q : f->qubits) {
+            bits.push_back(q);
+            covered |= 1ull << q;
+        }
+    }
+    if (cb.size() > 4) fail(SV_E_ARG, "product initialisation needs more than 4 chunks");
+    dev::ProductArgs &a = rec.prod;
+    a.psi = sv->psi;
+    a.n_amps = sv->local_amps();
+    a.rank_base = (uint64_t)sv->rank << sv->nloc;
+    const uint64_t all = sv->n >= 64 ? ~0ull : ((1ull << sv->n) - 1ull);
+    a.zero_mask = all & ~covered;
+    a.nchunks = (int)cb.size();
+    for (size_t c = 0; c < cb.size(); c++) {
+        a.cn[c] = (int)cb[c].size();
+        bool contig = true;
+        for (size_t j = 0; j < cb[c].size(); j++) {
+            a.cbits[c][j] = cb[c][j];
+            if (cb[c][j] != cb[c][0] + (int)j) contig = false;
+        }
+        a.ccontig[c] = contig;
+        double2 *d = nullptr;
+        cuda_check(cudaMalloc(&d, sizeof(double2) * ct[c].size()), "cudaMalloc(product table)");
+        cuda_check(cudaMemcpy(d, ct[c].data(), sizeof(double2) * ct[c].size(), cudaMemcpyHostToDevice),
+                   "upload product table");
+        p->d_tabs.push_back(d);
+        p->h2d_bytes += sizeof(double2) * ct[c].size();
+        a.tab[c] = d;
+    }
+}
+
+sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,
+                           const CompileOptions &co, uint64_t n_logical) {
+    std::unique_ptr<sv_program> p(new sv_program());
+    p->sv = sv;
+    p->n_logical = n_logical;
+    p->resets = init != nullptr;
+    if (p->resets) {
+        p->phys_in.resize(sv->n);
+        std::iota(p->phys_in.begin(), p->phys_in.end(), 0);
+    } else {
+        p->phys_in = sv->phys;
+    }
+    CompileOptions c2 = co;
+    if (c2.tile_qubits > 14) c2.tile_qubits = 14;
+    p->sched = compile(ops, init, sv->n, sv->nloc, p->phys_in, c2);
+    const int nloc = sv->nloc;
+    const uint64_t rank_base = (uint64_t)sv->rank << nloc;
+    auto rank_bit = [&](int phys_bit) -> int { return (int)((rank_base >> phys_bit) & 1ull); };
+
+    std::vector<double2> blob;
+    std::vector<dev::TileOp> tops;
+    auto push_data = [&](const std::vector<cplx> &d) {
+        size_t off = blob.size();
+        for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
+        return off;
+    };
+    struct Pending { size_t rec; size_t op0; };
+    std::vector<Pending> tiles;
+    std::vector<size_t> blob_fix;     // recs whose pointer must be rebased (streaming data)
+
+    for (const Step &st : p->sched.steps) {
+        LaunchRec rec;
+        rec.kind = st.kind;
+        rec.bytes = st.bytes;
+        switch (st.kind) {
+            case StepKind::InitZero: break;
+            case StepKind::InitProduct: build_product(sv, p.get(), st, rec); break;
+            case StepKind::Exchange:
+                rec.gbit = st.gbit;
+                rec.lbit = st.lbit;
+                break;
+            case StepKind::Dense: {
+                const Gate &g = st.tile_ops[0];
+                dev::DenseArgs &a = rec.dense;
+                a.psi = sv->psi;
+                a.k = st.k;
+                std::vector<int> ins;
+                for (int t = 0; t < st.k; t++) {
+                    a.tpos[t] = st.tpos[t];
+                    ins.push_back(st.tpos[t]);
+                }
+                for (size_t j = 0; j < g.controls.size(); j++) {
+                    const int b = g.controls[j];
+                    const int want = (int)((g.cvals >> j) & 1ull);
+                    if (b >= nloc) {
+                        if (rank_bit(b) != want) rec.skip = true;
+                    } else {
+                        ins.push_back(b);
+                        if (want) a.cset |= 1ull << b;
+                    }
+                }
+                std::sort(ins.begin(), ins.end());
+                if ((int)ins.size() > dev::kMaxIns) fail(SV_E_ARG, "too many controls");
+                a.nins = (int)ins.size();
+                for (size_t i = 0; i < ins.size(); i++) a.ins[i] = ins[i];
+                a.n_groups = 1ull << (nloc - (int)ins.size());
+                a.U = reinterpret_cast<const double2 *>(push_data(g.data));
+                blob_fix.push_back(p->recs.size());
+                break;
+            }
+            case StepKind::Diagonal: {
+                const Gate &g = st.tile_ops[0];
+                dev::DiagArgs &a = rec.diag;
+                a.psi = sv->psi;
+                a.n_amps = sv->local_amps();
+                a.nl = 0;
+                a.gidx = 0;
+                for (size_t j = 0; j < g.targets.size(); j++) {
+                    const int b = g.targets[j];
+                    if (b >= nloc) {
+                        a.gidx |= (uint32_t)rank_bit(b) << j;
+                    } else {
+                        a.pos[a.nl] = b;
+                        a.tbit[a.nl] = (int)j;
+                        a.nl++;
+                    }
+                }
+                a.table_len = (int)g.data.size();
+                a.table = reinterpret_cast<const double2 *>(push_data(g.data));
+                blob_fix.push_back(p->recs.size());
+                break;
+            }
+            case StepKind::RecipRY: {
+                const Gate &g = st.tile_ops[0];
+                dev::RecipArgs &a = rec.recip;
+                a.psi = sv->psi;
+                a.n_pairs = sv->local_amps() >> 1;
+                a.anc = g.targets[0];
+                a.n_c = (int)g.controls.size();
+                a.dL = g.delta * std::ldexp(1.0, a.n_c - (g.is_signed ? 1 : 0));
+                a.snap = g.snap;
+                a.is_signed = g.is_signed;
+                a.nlc = 0;
+                a.mglob = 0;
+                for (int j = 0; j < a.n_c; j++) {
+                    const int b = g.controls[j];
+                    if (b >= nloc) {
+                        a.mglob |= (uint64_t)rank_bit(b) << j;
+                    } else {
+                        a.lpos[a.nlc] = b;
+                        a.lbit[a.nlc] = j;
+                        a.nlc++;
+                    }
+                }
+                a.contiguous = a.nlc > 0;
+                for (int j = 0; j < a.nlc; j++)
+                    if (a.lpos[j] != a.lpos[0] + j || a.lbit[j] != a.lbit[0] + j) a.contiguous = 0;
+                if (a.contiguous) {
+                    a.lo = a.lpos[0];
+                    a.sh = a.lbit[0];
+                    a.lmask = (a.nlc >= 64) ? ~0ull : ((1ull << a.nlc) - 1ull);
+                }
+                break;
+            }
+            case StepKind::Tile: {
+                dev::TileArgs &a = rec.tile;
+                a.psi = sv->psi;
+                a.T = (int)st.tile_bits.size();
+                for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
+                a.n_tiles = 1ull << (nloc - a.T);
+                a.rank_base = rank_base;
+                a.maxk = 0;
+                const size_t op0 = tops.size();
+                for (const Gate &g : st.tile_ops) {
+                    dev::TileOp t{};
+                    if (g.kind == Kind::Dense || g.kind == Kind::Controlled) {
+                        t.kind = 0;
+                        t.k = (int)g.targets.size();
+                        a.maxk = std::max(a.maxk, t.k);
+                        std::vector<int> ins;
+                        for (int i = 0; i < t.k; i++) {
+                            t.tpos[i] = index_in(st.tile_bits, g.targets[i]);
+                            if (t.tpos[i] < 0) fail(SV_E_ARG, "internal: tile target not local");
+                            ins.push_back(t.tpos[i]);
+                        }
+                        for (size_t j = 0; j < g.controls.size(); j++) {
+                            const int b = g.controls[j];
+                            const int want = (int)((g.cvals >> j) & 1ull);
+                            const int lp = index_in(st.tile_bits, b);
+                            if (lp >= 0) {
+                                ins.push_back(lp);
+                                if (want) t.lcset |= 1u << lp;
+                            } else {
+                                t.gcmask |= 1ull << b;
+                                if (want) t.gcval |= 1ull << b;
+                            }
+                        }
+                        std::sort(ins.begin(), ins.end());
+                        if (ins.size() > 16) fail(SV_E_ARG, "too many tile-local controls");
+                        t.nins = (int)ins.size();
+                        for (size_t i = 0; i < ins.size(); i++) t.ins[i] = ins[i];
+                        t.data_off = push_data(g.data);
+                    } else if (g.kind == Kind::Diagonal) {
+                        t.kind = 1;
+                        for (size_t j = 0; j < g.targets.size(); j++) {
+                            const int b = g.targets[j];
+                            const int lp = index_in(st.tile_bits, b);
+                            if (lp >= 0) {
+                                t.dl_pos[t.ndl] = lp;
+                                t.dl_tbit[t.ndl] = (int)j;
+                                t.ndl++;
+                            } else {
+                                t.dg_bit[t.ndg] = b;
+                                t.dg_tbit[t.ndg] = (int)j;
+                                t.ndg++;
+                            }
+                        }
+                        t.data_off = push_data(g.data);
+                    } else {
+                        t.kind = 2;
+                        t.anc = index_in(st.tile_bits, g.targets[0]);
+                        if (t.anc < 0) fail(SV_E_ARG, "internal: tile ancilla not local");
+                        t.n_c = (int)g.controls.size();
+                        t.is_signed = g.is_signed;
+                        t.dL = g.delta * std::ldexp(1.0, t.n_c - (g.is_signed ? 1 : 0));
+                        t.snap = g.snap;
+                        for (int j = 0; j < t.n_c; j++) {
+                            const int b = g.controls[j];
+                            const int lp = index_in(st.tile_bits, b);
+                            if (lp >= 0) {
+                                t.lc_pos[t.nlc] = lp;
+                                t.lc_bit[t.nlc] = j;
+                                t.nlc++;
+                            } else {
+                                t.gc_bit[t.ngc] = b;
+                                t.gc_rbit[t.ngc] = j;
+                                t.ngc++;
+                            }
+                        }
+                    }
+                    tops.push_back(t);
+                }
+                a.nops = (int)(tops.size() - op0);
+                tiles.push_back({p->recs.size(), op0});
+                break;
+            }
+        }
+        p->recs.push_back(rec);
+    }
+    // upload blob and tile ops, then rebase pointers
+    if (!blob.empty()) {
+        cuda_check(cudaMalloc(&p->d_blob, sizeof(double2) * blob.size()), "cudaMalloc(blob)");
+        cuda_check(cudaMemcpy(p->d_blob, blob.data(), sizeof(double2) * blob.size(), cudaMemcpyHostToDevice),
+                   "upload blob");
+    }
+    if (!tops.empty()) {
+        cuda_check(cudaMalloc(&p->d_ops, sizeof(dev::TileOp) * tops.size()), "cudaMalloc(tile ops)");
+        cuda_check(cudaMemcpy(p->d_ops, tops.data(), sizeof(dev::TileOp) * tops.size(), cudaMemcpyHostToDevice),
+                   "upload tile ops");
+    }
+    p->h2d_bytes += sizeof(double2) * blob.size() + sizeof(dev::TileOp) * tops.size();
+    for (size_t r : blob_fix) {
+        LaunchRec &rec = p->recs[r];
+        if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
+        if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
+    }
+    for (auto &t : tiles) {
+        p->recs[t.rec].tile.ops = p->d_ops + t.op0;
+        p->recs[t.rec].tile.blob = p->d_blob;
+    }
+    return p.release();
+}
+
+static int rec_launches(const sv_state *sv, const LaunchRec &r) {
+    if (r.skip) return 0;
+    if (r.kind != StepKind::Exchange) return 1;
+    const uint64_t half = sv->local_amps() >> 1;
+    const uint64_t chunks = (half + (1ull << 26) - 1) >> 26;
+    return r.lbit == sv->nloc - 1 ? 0 : (int)(2 * chunks);   // pack + unpack kernels
+}
+
+}  // namespace hhlsv
+
+uint64_t sv_program::launches() const {
+    uint64_t n = 0;
+    for (auto &r : recs) n += hhlsv::rec_launches(sv, r);
+    return n;
+}
+
+namespace hhlsv {
+
+void program_run(sv_state *sv, sv_program *p) {
+    if (p->sv != sv) fail(SV_E_ARG, "program belongs to another state");
+    if (!p->resets && sv->phys != p->phys_in) fail(SV_E_ARG, "qubit map changed since the program was created");
+    if (p->timing && p->ev.size() != 2 * p->recs.size()) {
+        for (auto e : p->ev) cudaEventDestroy(e);
+        p->ev.assign(2 * p->recs.size(), nullptr);
+        for (auto &e : p->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    }
+    for (size_t ri = 0; ri < p->recs.size(); ri++) {
+        const LaunchRec &r = p->recs[ri];
+        if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri], sv->stream), "event");
+        if (r.skip) {
+            if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
+            continue;
+        }
+        switch (r.kind) {
+            case StepKind::InitZero: cuda_check(dev::launch_zero_init(sv->psi, sv->local_amps(), sv->rank == 0, sv->stream), "init"); break;
+            case StepKind::InitProduct: cuda_check(dev::launch_product(r.prod, sv->stream), "product init"); break;
+            case StepKind::Dense: cuda_check(dev::launch_dense(r.dense, sv->stream), "dense"); break;
+            case StepKind::Diagonal: cuda_check(dev::launch_diag(r.diag, sv->stream), "diagonal"); break;
+            case StepKind::RecipRY: cuda_check(dev::launch_recip(r.recip, sv->stream), "recip_ry"); break;
+            case StepKind::Tile: cuda_check(dev::launch_tile(r.tile, sv->stream), "tile"); break;
+            case StepKind::Exchange: exchange(sv, r.gbit, r.lbit); break;
+        }
+        if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
+    }
+    sv->phys = p->sched.phys_out;
+}
+
+void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out) {
+    if (!p->timing || p->ev.size() != 2 * p->recs.size()) fail(SV_E_ARG, "timing not enabled or program not run");
+    cuda_check(cudaStreamSynchronize(p->sv->stream), "timings sync");
+    const size_t n = std::min(cap, p->recs.size());
+    for (size_t i = 0; i < n; i++) {
+        float t = 0.0f;
+        cuda_check(cudaEventElapsedTime(&t, p->ev[2 * i], p->ev[2 * i + 1]), "elapsed");
+        if (ms) ms[i] = t;
+        if (kind) kind[i] = (int)p->recs[i].kind;
+        if (bytes) bytes[i] = p->recs[i].bytes;
+        if (launches) launches[i] = rec_launches(p->sv, p->recs[i]);
+    }
+    if (n_out) *n_out = p->recs.size();
+}
+
+void program_destroy(sv_program *p) {
+    if (!p) return;
+    if (p->sv) cudaStreamSynchronize(p->sv->stream);
+    cudaFree(p->d_blob);
+    cudaFree(p->d_ops);
+    for (auto *d : p->d_tabs) cudaFree(d);
+    for (auto e : p->ev) cudaEventDestroy(e);
+    delete p;
+}
+
+// ---------------------------------------------------------------- readout ----
+static void allreduce_if_sharded(sv_state *sv, double *dbuf, size_t count) {
+    if (sv->world > 1) nccl_check(nccl_allreduce_sum(sv->comm, dbuf, count, sv->stream), "allreduce");
+}
+
+double state_norm2(sv_state *sv) {
+    cuda_check(dev::launch_norm2(sv->psi, sv->local_amps(), sv->d_red, sv->d_scalar, sv->stream), "norm2");
+    allreduce_if_sharded(sv, sv->d_scalar, 1);
+    double h = 0.0;
+    cuda_check(cudaMemcpyAsync(&h, sv->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, sv->stream), "norm2 d2h");
+    cuda_check(cudaStreamSynchronize(sv->stream), "norm2 sync");
+    return h;
+}
+
+void state_probabilities(sv_state *sv, const int *qubits, int nq, double *out) {
+    if (nq < 0 || nq > 26 || (nq > 0 && !qubits) || !out) fail(SV_E_ARG, "probabilities: bad qubit list");
+    std::vector<int> q(qubits, qubits + nq);
+    for (int i = 0; i < nq; i++) {
+        if (q[i] < 0 || q[i] >= sv->n) fail(SV_E_ARG, "probabilities: qubit out of range");
+        for (int j = 0; j < i; j++)
+            if (q[i] == q[j]) fail(SV_E_ARG, "probabilities: duplicated qubit");
+    }
+    std::vector<int> S, jpos;
+    uint64_t gv = 0;
+    for (int j = 0; j < nq; j++) {
+        const int b = sv->phys[q[j]];
+        if (b < sv->nloc) {
+            S.push_back(b);
+            jpos.push_back(j);
+        } else if ((sv->rank >> (b - sv->nloc)) & 1) {
+            gv |= 1ull << j;
+        }
+    }
+    const int ql = (int)S.size();
+    const size_t C = (size_t)dev::marginal_chunks(sv->nloc, ql);
+    ensure_red(sv, ((size_t)1 << ql) * C + ((size_t)1 << ql));
+    double *ws = sv->d_red;
+    double *dout = sv->d_red + ((size_t)1 << ql) * C;
+    cuda_check(dev::launch_marginal(sv->psi, sv->nloc, S.data(), ql, ws, dout, sv->stream), "marginal");
+    std::vector<double> loc((size_t)1 << ql);
+    cuda_check(cudaMemcpyAsync(loc.data(), dout, sizeof(double) * loc.size(), cudaMemcpyDeviceToHost, sv->stream),
+               "marginal d2h");
+    cuda_check(cudaStreamSynchronize(sv->stream), "marginal sync");
+    const size_t nout = (size_t)1 << nq;
+    std::fill(out, out + nout, 0.0);
+    for (size_t v = 0; v < loc.size(); v++) {
+        uint64_t o = gv;
+        for (int i = 0; i < ql; i++)
+            if ((v >> i) & 1) o |= 1ull << jpos[i];
+        out[o] = loc[v];
+    }
+    if (sv->world > 1) {
+        ensure_red(sv, nout);
+        cuda_check(cudaMemcpyAsync(sv->d_red, out, sizeof(double) * nout, cudaMemcpyHostToDevice, sv->stream), "h2d");
+        allreduce_if_sharded(sv, sv->d_red, nout);
+        cuda_check(cudaMemcpyAsync(out, sv->d_red, sizeof(double) * nout, cudaMemcpyDeviceToHost, sv->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(sv->stream), "probabilities sync");
+    }
+}
+
+static void fill_phys(const sv_state *sv, int *dst) {
+    for (int q = 0; q < sv->n; q++) dst[q] = sv->phys[q];
+}
+
+void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out) {
+    const uint64_t N = 1ull << sv->n;
+    if (first > N || count > N - first) fail(SV_E_RANGE, "read: range outside the state");
+    if (count && !out) fail(SV_E_ARG, "read: null output");
+    const uint64_t chunk = 1ull << 22;
+    ensure_io(sv, std::min(count, chunk));
+    for (uint64_t off = 0; off < count; off += chunk) {
+        const uint64_t c = std::min(chunk, count - off);
+        dev::GatherArgs a{};
+        a.psi = sv->psi;
+        a.out = sv->d_io;
+        a.count = c;
+        a.first = first + off;
+        a.n = sv->n;
+        a.nloc = sv->nloc;
+        a.rank = (uint64_t)sv->rank;
+        fill_phys(sv, a.phys);
+        cuda_check(dev::launch_gather(a, sv->stream), "gather");
+        allreduce_if_sharded(sv, (double *)sv->d_io, 2 * c);
+        cuda_check(cudaMemcpyAsync(out + 2 * off, sv->d_io, sizeof(double2) * c, cudaMemcpyDeviceToHost, sv->stream),
+                   "read d2h");
+    }
+    cuda_check(cudaStreamSynchronize(sv->stream), "read sync");
+}
+
+void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in) {
+    const uint64_t N = 1ull << sv->n;
+    if (first > N || count > N - first) fail(SV_E_RANGE, "write: range outside the state");
+    if (count && !in) fail(SV_E_ARG, "write: null input");
+    const uint64_t chunk = 1ull << 22;
+    ensure_io(sv, std::min(count, chunk));
+    for (uint64_t off = 0; off < count; off += chunk) {
+        const uint64_t c = std::min(chunk, count - off);
+        cuda_check(cudaMemcpyAsync(sv->d_io, in + 2 * off, sizeof(double2) * c, cudaMemcpyHostToDevice, sv->stream),
+                   "write h2d");
+        dev::ScatterArgs a{};
+        a.psi = sv->psi;
+        a.in = sv->d_io;
+        a.count = c;
+        a.first = first + off;
+        a.n = sv->n;
+        a.nloc = sv->nloc;
+        a.rank = (uint64_t)sv->rank;
+        fill_phys(sv, a.phys);
+        cuda_check(dev::launch_scatter(a, sv->stream), "scatter");
+    }
+    cuda_check(cudaStreamSynchronize(sv->stream), "write sync");
+}
+
+void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, double *amps, uint64_t *idx,
+                      uint64_t n_out, double *prob) {
+    if (nfixed < 0 || (nfixed > 0 && (!fq || !fv)) || !amps) fail(SV_E_ARG, "postselect: bad arguments");
+    uint64_t fixed = 0, fmask = 0;
+    for (int i = 0; i < nfixed; i++) {
+        if (fq[i] < 0 || fq[i] >= sv->n || (fmask >> fq[i]) & 1ull) fail(SV_E_ARG, "postselect: bad qubit");
+        if (fv[i] != 0 && fv[i] != 1) fail(SV_E_ARG, "postselect: values must be 0/1");
+        fmask |= 1ull << fq[i];
+        if (fv[i]) fixed |= 1ull << fq[i];
+    }
+    dev::GatherArgs a{};
+    int nfree = 0;
+    for (int q = 0; q < sv->n; q++)
+        if (!((fmask >> q) & 1ull)) a.free_q[nfree++] = q;
+    if (nfree > 26 || n_out != (1ull << nfree)) fail(SV_E_ARG, "postselect: n_out must be 2^(n - n_fixed) <= 2^26");
+    ensure_io(sv, n_out);
+    a.psi = sv->psi;
+    a.out = sv->d_io;
+    a.count = n_out;
+    a.first = 0;
+    a.n = sv->n;
+    a.nloc = sv->nloc;
+    a.rank = (uint64_t)sv->rank;
+    fill_phys(sv, a.phys);
+    a.nfree = nfree == 0 ? -1 : nfree;   // -1: only the fixed index
+    if (nfree == 0) {
+        a.nfree = 1;                     // deposit of 0 -> fixed (free_q[0] unused for x=0)
+        a.free_q[0] = 0;
+    }
+    a.fixed = fixed;
+    cuda_check(dev::launch_gather(a, sv->stream), "postselect gather");
+    allreduce_if_sharded(sv, (double *)sv->d_io, 2 * n_out);
+    cuda_check(cudaMemcpyAsync(amps, sv->d_io, sizeof(double2) * n_out, cudaMemcpyDeviceToHost, sv->stream),
+               "postselect d2h");
+    cuda_check(cudaStreamSynchronize(sv->stream), "postselect sync");
+    if (idx)
+        for (uint64_t e = 0; e < n_out; e++) {
+            uint64_t L = fixed;
+            for (int i = 0; i < nfree; i++)
+                if ((e >> i) & 1ull) L |= 1ull << a.free_q[i];
+            idx[e] = L;
+        }
+    if (prob) {
+        double s = 0.0;
+        for (uint64_t e = 0; e < 2 * n_out; e++) s += amps[e] * amps[e];
+        *prob = s;
+    }
+}
+
+}  // namespace hhlsv

@@ -1,0 +1,80 @@
+// Device state and resident programs (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "comm.h"
+#include "kernels.cuh"
+#include "sv_internal.h"
+
+struct sv_state {
+    int n = 0;              // total qubits
+    int g = 0;              // global (rank) qubits = log2(world)
+    int nloc = 0;           // local qubits
+    int world = 1, rank = 0, device = 0;
+    cudaStream_t stream = nullptr;
+    double2 *psi = nullptr; // 2^nloc local amplitudes, physical order
+    std::vector<int> phys;  // logical qubit -> physical bit
+    // workspace
+    double *d_red = nullptr;        // reduction partials
+    size_t red_len = 0;
+    double *d_scalar = nullptr;     // 8 doubles
+    double2 *d_io = nullptr;        // staging for gathers/exchanges
+    size_t io_len = 0;              // in double2
+    double2 *d_xsend = nullptr, *d_xrecv = nullptr;  // exchange buffers
+    size_t x_len = 0;
+    hhlsv::Comm comm;
+    uint64_t local_amps() const { return 1ull << nloc; }
+};
+
+namespace hhlsv {
+
+struct LaunchRec {
+    StepKind kind;
+    bool skip = false;                // controlled op whose global controls do not match this rank
+    dev::DenseArgs dense{};
+    dev::DiagArgs diag{};
+    dev::RecipArgs recip{};
+    dev::ProductArgs prod{};
+    dev::TileArgs tile{};
+    int gbit = 0, lbit = 0;           // exchange
+    double bytes = 0;
+};
+
+}  // namespace hhlsv
+
+struct sv_program {
+    sv_state *sv = nullptr;
+    hhlsv::Schedule sched;
+    std::vector<int> phys_in;
+    bool resets = false;              // starts with an initialisation step
+    double2 *d_blob = nullptr;
+    hhlsv::dev::TileOp *d_ops = nullptr;
+    std::vector<hhlsv::LaunchRec> recs;
+    uint64_t n_logical = 0;
+    std::vector<double2 *> d_tabs;    // product-init tables (owned)
+    double h2d_bytes = 0;             // uploaded at creation
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;      // 2 per rec when timing
+    uint64_t launches() const;
+};
+
+namespace hhlsv {
+void cuda_check(cudaError_t e, const char *what);
+sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream);
+void state_destroy(sv_state *sv);
+void state_reset(sv_state *sv);
+sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,
+                           const CompileOptions &co, uint64_t n_logical);
+void program_run(sv_state *sv, sv_program *p);
+void program_destroy(sv_program *p);
+void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out);
+void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out);
+void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in);
+double state_norm2(sv_state *sv);
+void state_probabilities(sv_state *sv, const int *qubits, int nq, double *out);
+void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, double *amps, uint64_t *idx,
+                      uint64_t n_out, double *prob);
+}  // namespace hhlsv

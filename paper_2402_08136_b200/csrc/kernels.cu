@@ -1,0 +1,608 @@
+// sm_100a kernels of the HHL state-vector hot path.
+//
+// Every kernel streams the interleaved complex128 state in HBM with 16-byte (double2)
+// accesses, 64-bit index arithmetic, grid-stride loops sized in multiples of the 148 SMs,
+// and fp64 FMA arithmetic (the paper's precision is fp64 complex; R16).
+// Reductions are fixed-order trees (warp shuffle -> block -> grid), never fp64 atomics,
+// so two runs are bit-identical.
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace hhlsv {
+namespace dev {
+
+constexpr int kThreads = 256;
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ uint64_t insz(uint64_t x, int p) {
+    const uint64_t lo = x & ((1ull << p) - 1ull);
+    return ((x >> p) << (p + 1)) | lo;
+}
+
+__device__ __forceinline__ void cfma(double2 &acc, const double2 a, const double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+
+__device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// Reciprocal rotation sine, SURVEY §8(a) a7 / DESIGN.md R6 (identical IEEE operations to the
+// oracle's definition so that the snapping/clipping decisions agree bit for bit).
+__device__ __forceinline__ double recip_s(uint64_t m, int n_c, double dL, int is_signed, double snap) {
+    if (m == 0) return 0.0;
+    double sign = 1.0;
+    uint64_t mp = m;
+    if (is_signed && m >= (1ull << (n_c - 1))) {
+        mp = (1ull << n_c) - m;
+        sign = -1.0;
+    }
+    const double r = __ddiv_rn(dL, (double)mp);
+    const double s = fabs(r - 1.0) <= snap ? 1.0 : (r < 1.0 ? r : 0.0);
+    return sign * s;
+}
+
+static int grid_for(uint64_t work, int per_block) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    const uint64_t cap = (uint64_t)kSMs * 8;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+// ============================================================ a4/a5 dense ====
+// One thread per group of 2^K amplitudes (G groups per thread for small K to keep
+// >= 8 independent 16-byte loads in flight). The matrix sits in shared memory and is
+// read as a warp-wide broadcast.
+template <int K, int G>
+__global__ void __launch_bounds__(kThreads) k_dense(const DenseArgs a) {
+    constexpr int D = 1 << K;
+    __shared__ double2 sU[D * D];
+    __shared__ uint64_t soff[D];
+    for (int i = threadIdx.x; i < D * D; i += blockDim.x) sU[i] = a.U[i];
+    if (threadIdx.x < D) {
+        uint64_t o = 0;
+        for (int i = 0; i < K; i++)
+            if ((threadIdx.x >> i) & 1) o |= 1ull << a.tpos[i];
+        soff[threadIdx.x] = o;
+    }
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * G;
+    for (uint64_t g0 = (uint64_t)blockIdx.x * blockDim.x * G + threadIdx.x; g0 < a.n_groups; g0 += stride) {
+        uint64_t base[G];
+        double2 v[G][D];
+#pragma unroll
+        for (int gg = 0; gg < G; gg++) {
+            uint64_t g = g0 + (uint64_t)gg * blockDim.x;
+            if (g >= a.n_groups) g = g0;          // duplicate work on the tail, stores are idempotent
+            uint64_t b = g;
+            for (int i = 0; i < a.nins; i++) b = insz(b, a.ins[i]);
+            base[gg] = b | a.cset;
+#pragma unroll
+            for (int c = 0; c < D; c++) v[gg][c] = a.psi[base[gg] | soff[c]];
+        }
+#pragma unroll
+        for (int gg = 0; gg < G; gg++) {
+            // r is not unrolled for K >= 3 so the compiler cannot hoist the whole matrix
+            // out of the grid-stride loop into registers.
+#pragma unroll(K >= 3 ? 1 : D)
+            for (int r = 0; r < D; r++) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int c = 0; c < D; c++) cfma(acc, sU[r * D + c], v[gg][c]);
+                a.psi[base[gg] | soff[r]] = acc;
+            }
+        }
+    }
+}
+
+cudaError_t launch_dense(const DenseArgs &a, cudaStream_t s) {
+    if (a.n_groups == 0) return cudaSuccess;
+    switch (a.k) {
+        case 1: k_dense<1, 4><<<grid_for(a.n_groups, kThreads * 4), kThreads, 0, s>>>(a); break;
+        case 2: k_dense<2, 2><<<grid_for(a.n_groups, kThreads * 2), kThreads, 0, s>>>(a); break;
+        case 3: k_dense<3, 1><<<grid_for(a.n_groups, kThreads), kThreads, 0, s>>>(a); break;
+        case 4: k_dense<4, 1><<<grid_for(a.n_groups, kThreads), kThreads, 0, s>>>(a); break;
+        case 5: k_dense<5, 1><<<grid_for(a.n_groups, kThreads), kThreads, 0, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// ========================================================= a6 diagonal ====
+__global__ void __launch_bounds__(kThreads) k_diag(const DiagArgs a) {
+    extern __shared__ double2 stab[];
+    for (int i = threadIdx.x; i < a.table_len; i += blockDim.x) stab[i] = a.table[i];
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 2;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * 2 + threadIdx.x; i0 < a.n_amps; i0 += stride) {
+        uint64_t ii[2] = {i0, i0 + blockDim.x};
+        double2 v[2];
+#pragma unroll
+        for (int q = 0; q < 2; q++)
+            if (ii[q] < a.n_amps) v[q] = a.psi[ii[q]];
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (ii[q] >= a.n_amps) continue;
+            uint32_t idx = a.gidx;
+            for (int j = 0; j < a.nl; j++) idx |= (uint32_t)((ii[q] >> a.pos[j]) & 1ull) << a.tbit[j];
+            a.psi[ii[q]] = cmul(stab[idx], v[q]);
+        }
+    }
+}
+
+cudaError_t launch_diag(const DiagArgs &a, cudaStream_t s) {
+    const size_t smem = sizeof(double2) * a.table_len;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_diag<<<grid_for(a.n_amps, kThreads * 2), kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ======================================================= a7 recip RY ====
+__global__ void __launch_bounds__(kThreads) k_recip(const RecipArgs a) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t abit = 1ull << a.anc;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.n_pairs; p += stride) {
+        const uint64_t i0 = insz(p, a.anc);
+        const double2 x0 = a.psi[i0], x1 = a.psi[i0 | abit];
+        uint64_t m = a.mglob;
+        if (a.contiguous) {
+            m |= ((i0 >> a.lo) & a.lmask) << a.sh;
+        } else {
+            for (int j = 0; j < a.nlc; j++) m |= ((i0 >> a.lpos[j]) & 1ull) << a.lbit[j];
+        }
+        const double sv = recip_s(m, a.n_c, a.dL, a.is_signed, a.snap);
+        const double cv = sqrt(fma(-sv, sv, 1.0));
+        a.psi[i0] = make_double2(cv * x0.x - sv * x1.x, cv * x0.y - sv * x1.y);
+        a.psi[i0 | abit] = make_double2(sv * x0.x + cv * x1.x, sv * x0.y + cv * x1.y);
+    }
+}
+
+cudaError_t launch_recip(const RecipArgs &a, cudaStream_t s) {
+    k_recip<<<grid_for(a.n_pairs, kThreads), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ===================================================== a3 product init ====
+__global__ void __launch_bounds__(kThreads) k_product(const ProductArgs a) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_amps; i += stride) {
+        const uint64_t gi = a.rank_base | i;
+        double2 amp = make_double2(0.0, 0.0);
+        if (!(gi & a.zero_mask)) {
+            amp = make_double2(1.0, 0.0);
+            for (int c = 0; c < a.nchunks; c++) {
+                uint32_t idx = 0;
+                if (a.ccontig[c]) {
+                    idx = (uint32_t)((gi >> a.cbits[c][0]) & ((1ull << a.cn[c]) - 1ull));
+                } else {
+                    for (int j = 0; j < a.cn[c]; j++) idx |= (uint32_t)((gi >> a.cbits[c][j]) & 1ull) << j;
+                }
+                amp = c == 0 ? __ldg(&a.tab[c][idx]) : cmul(amp, __ldg(&a.tab[c][idx]));
+            }
+        }
+        a.psi[i] = amp;
+    }
+}
+
+cudaError_t launch_product(const ProductArgs &a, cudaStream_t s) {
+    k_product<<<grid_for(a.n_amps, kThreads), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void k_zero(double2 *psi, uint64_t n, int set_first) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        psi[i] = make_double2((set_first && i == 0) ? 1.0 : 0.0, 0.0);
+}
+
+cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream_t s) {
+    k_zero<<<grid_for(n, kThreads), kThreads, 0, s>>>(psi, n, set_first);
+    return cudaGetLastError();
+}
+
+// ======================================================= f1 tile pass ====
+// One CTA stages the 2^T amplitudes spanned by the tile bits in shared memory (XOR
+// swizzled against bank conflicts), applies every op of the pass, and writes back:
+// ONE HBM read + write for the whole op list.
+__device__ __forceinline__ uint32_t swz(uint32_t u) {
+    return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u);
+}
+
+template <int K>
+__device__ __forceinline__ void tile_dense(double2 *st, const double2 *sU, const TileOp &op, int T) {
+    constexpr int D = 1 << K;
+    int tp[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) tp[i] = op.tpos[i];
+    const int nins = op.nins;
+    const uint32_t groups = 1u << (T - nins);
+    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
+        uint32_t b = g;
+        for (int i = 0; i < nins; i++) {
+            const int p = op.ins[i];
+            b = ((b >> p) << (p + 1)) | (b & ((1u << p) - 1u));
+        }
+        b |= op.lcset;
+        double2 v[D];
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < K; i++)
+                if ((c >> i) & 1) o |= 1u << tp[i];
+            v[c] = st[swz(b | o)];
+        }
+#pragma unroll(K >= 3 ? 1 : D)
+        for (int r = 0; r < D; r++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < D; c++) cfma(acc, sU[r * D + c], v[c]);
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < K; i++)
+                if ((r >> i) & 1) o |= 1u << tp[i];
+            st[swz(b | o)] = acc;
+        }
+    }
+}
+
+template <int MAXK>
+__global__ void __launch_bounds__(kThreads, MAXK >= 5 ? 1 : 2) k_tile(const TileArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int T = a.T;
+    const uint32_t NT = 1u << T;
+    double2 *st = reinterpret_cast<double2 *>(smem_raw);
+    double2 *sU = st + NT;
+    const int SA = (T + 1) / 2, SB = T - SA;
+    uint64_t *depA = reinterpret_cast<uint64_t *>(sU + (a.maxk > 0 ? (1 << (2 * a.maxk)) : 0));
+    uint64_t *depB = depA + (1 << SA);
+    for (int u = threadIdx.x; u < (1 << SA); u += blockDim.x) {
+        uint64_t d = 0;
+        for (int i = 0; i < SA; i++)
+            if ((u >> i) & 1) d |= 1ull << a.tbits[i];
+        depA[u] = d;
+    }
+    for (int u = threadIdx.x; u < (1 << SB); u += blockDim.x) {
+        uint64_t d = 0;
+        for (int i = 0; i < SB; i++)
+            if ((u >> i) & 1) d |= 1ull << a.tbits[SA + i];
+        depB[u] = d;
+    }
+    const uint32_t maskA = (1u << SA) - 1u;
+    __syncthreads();
+
+    for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        uint64_t base = tile;
+        for (int i = 0; i < T; i++) base = insz(base, a.tbits[i]);
+        const uint64_t gbase = a.rank_base | base;
+        // ---- load (8 independent 16-byte loads per thread in flight per batch)
+        for (uint32_t j = 0; j < NT; j += blockDim.x * 8) {
+            double2 r[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint32_t u = j + q * blockDim.x + threadIdx.x;
+                if (u < NT) r[q] = a.psi[base | depA[u & maskA] | depB[u >> SA]];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint32_t u = j + q * blockDim.x + threadIdx.x;
+                if (u < NT) st[swz(u)] = r[q];
+            }
+        }
+        __syncthreads();
+        // ---- ops
+        for (int oi = 0; oi < a.nops; oi++) {
+            const TileOp &op = a.ops[oi];
+            if ((gbase & op.gcmask) != op.gcval) continue;        // CTA-uniform
+            if (op.kind == 0) {
+                const int D = 1 << op.k;
+                const double2 *U = a.blob + op.data_off;
+                for (int i = threadIdx.x; i < D * D; i += blockDim.x) sU[i] = U[i];
+                __syncthreads();
+                switch (op.k) {
+                    case 1: tile_dense<1>(st, sU, op, T); break;
+                    case 2: if (MAXK >= 2) tile_dense<(MAXK >= 2 ? 2 : 1)>(st, sU, op, T); break;
+                    case 3: if (MAXK >= 3) tile_dense<(MAXK >= 3 ? 3 : 1)>(st, sU, op, T); break;
+                    case 4: if (MAXK >= 4) tile_dense<(MAXK >= 4 ? 4 : 1)>(st, sU, op, T); break;
+                    case 5: if (MAXK >= 5) tile_dense<(MAXK >= 5 ? 5 : 1)>(st, sU, op, T); break;
+                }
+            } else if (op.kind == 1) {
+                uint32_t gidx = 0;
+                for (int j = 0; j < op.ndg; j++) gidx |= (uint32_t)((gbase >> op.dg_bit[j]) & 1ull) << op.dg_tbit[j];
+                const double2 *tab = a.blob + op.data_off;
+                for (uint32_t u = threadIdx.x; u < NT; u += blockDim.x) {
+                    uint32_t idx = gidx;
+                    for (int j = 0; j < op.ndl; j++) idx |= ((u >> op.dl_pos[j]) & 1u) << op.dl_tbit[j];
+                    const uint32_t su = swz(u);
+                    st[su] = cmul(__ldg(&tab[idx]), st[su]);
+                }
+            } else {
+                uint64_t mg = 0;
+                for (int j = 0; j < op.ngc; j++) mg |= ((gbase >> op.gc_bit[j]) & 1ull) << op.gc_rbit[j];
+                const int anc = op.anc;
+                for (uint32_t p = threadIdx.x; p < (NT >> 1); p += blockDim.x) {
+                    const uint32_t u0 = ((p >> anc) << (anc + 1)) | (p & ((1u << anc) - 1u));
+                    const uint32_t u1 = u0 | (1u << anc);
+                    uint64_t m = mg;
+                    for (int j = 0; j < op.nlc; j++) m |= (uint64_t)((u0 >> op.lc_pos[j]) & 1u) << op.lc_bit[j];
+                    const double sv = recip_s(m, op.n_c, op.dL, op.is_signed, op.snap);
+                    const double cv = sqrt(fma(-sv, sv, 1.0));
+                    const uint32_t s0 = swz(u0), s1 = swz(u1);
+                    const double2 x0 = st[s0], x1 = st[s1];
+                    st[s0] = make_double2(cv * x0.x - sv * x1.x, cv * x0.y - sv * x1.y);
+                    st[s1] = make_double2(sv * x0.x + cv * x1.x, sv * x0.y + cv * x1.y);
+                }
+            }
+            __syncthreads();
+        }
+        // ---- store
+        for (uint32_t j = 0; j < NT; j += blockDim.x * 8) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint32_t u = j + q * blockDim.x + threadIdx.x;
+                if (u < NT) a.psi[base | depA[u & maskA] | depB[u >> SA]] = st[swz(u)];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t tile_smem_bytes(int T, int maxk) {
+    const int SA = (T + 1) / 2, SB = T - SA;
+    return sizeof(double2) * ((size_t)1 << T) + (maxk > 0 ? sizeof(double2) * ((size_t)1 << (2 * maxk)) : 0) +
+           sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
+}
+
+template <int MAXK>
+static cudaError_t launch_tile_k(const TileArgs &a, cudaStream_t s) {
+    const size_t smem = tile_smem_bytes(a.T, a.maxk);
+    static int per_sm_cache[16] = {0};
+    cudaError_t e = cudaFuncSetAttribute(k_tile<MAXK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<MAXK>, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    (void)per_sm_cache;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)kSMs * per_sm;
+    if (grid > a.n_tiles) grid = a.n_tiles;
+    k_tile<MAXK><<<(unsigned)grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile(const TileArgs &a, cudaStream_t s) {
+    switch (a.maxk) {
+        case 0:
+        case 1:
+        case 2: return launch_tile_k<2>(a, s);
+        case 3: return launch_tile_k<3>(a, s);
+        case 4: return launch_tile_k<4>(a, s);
+        default: return launch_tile_k<5>(a, s);
+    }
+}
+
+// ======================================================= a8 reductions ====
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order block reduction of one value per thread (result valid in thread 0).
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double ws[32];
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) ws[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < (int)(blockDim.x >> 5)) ? ws[l] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kThreads) k_norm2_partial(const double2 *psi, uint64_t n, uint64_t chunk,
+                                                            double *partial) {
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    uint64_t hi = lo + chunk;
+    if (hi > n) hi = n;
+    double acc = 0.0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 v = psi[i];
+        acc = fma(v.x, v.x, acc);
+        acc = fma(v.y, v.y, acc);
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(1024) k_sum_final(const double *partial, int np, double *out) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) out[0] = acc;
+}
+
+cudaError_t launch_norm2(const double2 *psi, uint64_t n, double *partial, double *out, cudaStream_t s) {
+    const uint64_t chunk = (n + kRedBlocks - 1) / kRedBlocks;
+    k_norm2_partial<<<kRedBlocks, kThreads, 0, s>>>(psi, n, chunk, partial);
+    k_sum_final<<<1, 1024, 0, s>>>(partial, kRedBlocks, out);
+    return cudaGetLastError();
+}
+
+int marginal_chunks(int nloc, int q) {
+    // enough warps for the whole GPU, segments of >= 256 elements
+    const int R = nloc - q;            // log2 elements per bin
+    int c = 0;
+    while ((q + c) < 12 + 5 && (R - c) > 8) c++;   // 2^(q+c) >= ~4k warps
+    return 1 << c;
+}
+
+struct MargArgs {
+    const double2 *psi;
+    int nloc, q, logC;
+    uint64_t Smask, Omask;
+    int S[32];
+    uint64_t step_dep;                 // deposit of 32 into O bits
+    int O[64];
+    int nO;
+};
+
+__device__ __forceinline__ uint64_t deposit_list(uint64_t x, const int *bits, int nb) {
+    uint64_t d = 0;
+    for (int i = 0; i < nb && x; i++, x >>= 1)
+        if (x & 1ull) d |= 1ull << bits[i];
+    return d;
+}
+
+__global__ void __launch_bounds__(kThreads) k_marginal(const MargArgs a, double *ws) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = 1ull << (a.q + a.logC);
+    if (warp >= nwarps) return;
+    const uint64_t v = warp >> a.logC, c = warp & ((1ull << a.logC) - 1ull);
+    const int lr = a.nloc - a.q;                      // log2 elements per bin
+    const uint64_t seg = 1ull << (lr - a.logC);
+    const uint64_t r0 = c * seg + lane;
+    double acc = 0.0;
+    if (r0 < (c + 1) * seg) {
+        const uint64_t sdep = deposit_list(v, a.S, a.q);
+        uint64_t cur = deposit_list(r0, a.O, a.nO);
+        const uint64_t cnt = seg >= 32 ? seg / 32 : 1;
+        for (uint64_t j = 0; j < cnt; j++) {
+            const double2 x = a.psi[sdep | cur];
+            acc = fma(x.x, x.x, acc);
+            acc = fma(x.y, x.y, acc);
+            cur = ((cur | ~a.Omask) + a.step_dep) & a.Omask;
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) ws[warp] = acc;
+}
+
+__global__ void k_marginal_final(const double *ws, int logC, uint64_t nbins, double *out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nbins; v += stride) {
+        double acc = 0.0;
+        for (uint64_t c = 0; c < (1ull << logC); c++) acc += ws[(v << logC) + c];
+        out[v] = acc;
+    }
+}
+
+cudaError_t launch_marginal(const double2 *psi, int nloc, const int *S, int q, double *ws, double *out,
+                            cudaStream_t s) {
+    MargArgs a{};
+    a.psi = psi;
+    a.nloc = nloc;
+    a.q = q;
+    const int C = marginal_chunks(nloc, q);
+    int logC = 0;
+    while ((1 << logC) < C) logC++;
+    a.logC = logC;
+    for (int i = 0; i < q; i++) {
+        a.S[i] = S[i];
+        a.Smask |= 1ull << S[i];
+    }
+    a.nO = 0;
+    for (int b = 0; b < nloc; b++)
+        if (!((a.Smask >> b) & 1ull)) {
+            a.O[a.nO++] = b;
+            a.Omask |= 1ull << b;
+        }
+    // deposit of 32 into the O bits (used as the per-iteration stride of a lane)
+    uint64_t d = 0;
+    {
+        uint64_t x = 32;
+        for (int i = 0; i < a.nO && x; i++, x >>= 1)
+            if (x & 1ull) d |= 1ull << a.O[i];
+    }
+    a.step_dep = d;
+    const uint64_t nwarps = 1ull << (q + logC);
+    const uint64_t blocks = (nwarps * 32 + kThreads - 1) / kThreads;
+    k_marginal<<<(unsigned)blocks, kThreads, 0, s>>>(a, ws);
+    const uint64_t nbins = 1ull << q;
+    k_marginal_final<<<grid_for(nbins, kThreads), kThreads, 0, s>>>(ws, logC, nbins, out);
+    return cudaGetLastError();
+}
+
+// ======================================================= gather / scatter ====
+__global__ void k_gather(const GatherArgs a) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.count; e += stride) {
+        uint64_t L;
+        if (a.nfree == 0) {
+            L = a.first + e;
+        } else {
+            L = a.fixed;
+            uint64_t x = a.first + e;
+            for (int i = 0; i < a.nfree; i++)
+                if ((x >> i) & 1ull) L |= 1ull << a.free_q[i];
+        }
+        uint64_t P = 0;
+        for (int q = 0; q < a.n; q++)
+            if ((L >> q) & 1ull) P |= 1ull << a.phys[q];
+        double2 v = make_double2(0.0, 0.0);
+        if ((P >> a.nloc) == a.rank) v = a.psi[P & ((1ull << a.nloc) - 1ull)];
+        a.out[e] = v;
+    }
+}
+
+cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    k_gather<<<grid_for(a.count, kThreads), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void k_scatter(const ScatterArgs a) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.count; e += stride) {
+        const uint64_t L = a.first + e;
+        uint64_t P = 0;
+        for (int q = 0; q < a.n; q++)
+            if ((L >> q) & 1ull) P |= 1ull << a.phys[q];
+        if ((P >> a.nloc) == a.rank) a.psi[P & ((1ull << a.nloc) - 1ull)] = a.in[e];
+    }
+}
+
+cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    k_scatter<<<grid_for(a.count, kThreads), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ====================================================== K7 pack / unpack ====
+__global__ void k_pack(const double2 *psi, double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        buf[j] = psi[insz(off + j, lbit) | ((uint64_t)val << lbit)];
+}
+__global__ void k_unpack(double2 *psi, const double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        psi[insz(off + j, lbit) | ((uint64_t)val << lbit)] = buf[j];
+}
+
+cudaError_t launch_pack(const double2 *psi, double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
+                        cudaStream_t s) {
+    k_pack<<<grid_for(cnt, kThreads), kThreads, 0, s>>>(psi, buf, lbit, val, off, cnt);
+    return cudaGetLastError();
+}
+cudaError_t launch_unpack(double2 *psi, const double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
+                          cudaStream_t s) {
+    k_unpack<<<grid_for(cnt, kThreads), kThreads, 0, s>>>(psi, buf, lbit, val, off, cnt);
+    return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace hhlsv

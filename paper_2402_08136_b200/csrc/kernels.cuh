@@ -1,0 +1,152 @@
+// Kernel parameter blocks and launchers for the sm_100a state-vector kernels.
+// All amplitude arrays are interleaved complex128 (double2), PHYSICAL local order.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hhlsv {
+namespace dev {
+
+constexpr int kMaxIns = 26;      // zero-insertion bits (targets + local controls)
+constexpr int kMaxDiag = 12;
+constexpr int kMaxClock = 62;
+constexpr int kMaxTileOps = 4096;
+
+struct DenseArgs {               // a4/a5: dense or controlled fused gate, one streaming pass
+    double2 *psi;
+    uint64_t n_groups;           // 2^(nloc - k - #local controls)
+    int nins;
+    int ins[kMaxIns];            // sorted bits where zeros are inserted (targets + local controls)
+    uint64_t cset;               // OR-mask of local control bits required to be 1
+    int k;
+    int tpos[5];                 // target bits, tpos[0] = LSB of the matrix index
+    const double2 *U;            // 2^k x 2^k row-major, device
+};
+
+struct DiagArgs {                // a6: diagonal fused gate (phase table over <= 12 qubits)
+    double2 *psi;
+    uint64_t n_amps;
+    int nl;                      // local table qubits
+    int pos[kMaxDiag];           // physical local bit of local table qubit j
+    int tbit[kMaxDiag];          // table-index bit it feeds
+    uint32_t gidx;               // table-index bits from global qubits (rank)
+    const double2 *table;
+    int table_len;
+};
+
+struct RecipArgs {               // a7: eigenvalue-inversion RY, multiplexed by the clock register
+    double2 *psi;
+    uint64_t n_pairs;            // 2^(nloc-1)
+    int anc;                     // ancilla physical (local) bit
+    int nlc;                     // local clock bits
+    int lpos[kMaxClock];         // physical bit of local clock qubit
+    int lbit[kMaxClock];         // register bit it feeds
+    uint64_t mglob;              // register bits from global clock qubits
+    int n_c;
+    double dL;                   // delta * 2^(n_c - signed) (exact)
+    double snap;
+    int is_signed;
+    int contiguous;              // local clock bits are physical lo..lo+nlc-1 feeding register bits sh..
+    int lo, sh;
+    uint64_t lmask;
+};
+
+struct ProductArgs {             // a3: product-state initialisation (prep + H layer folded)
+    double2 *psi;
+    uint64_t n_amps;
+    uint64_t rank_base;          // rank << nloc (global index of local 0)
+    uint64_t zero_mask;          // global-index bits that must be 0 (uncovered qubits)
+    int nchunks;
+    int cbits[4][16];            // physical (global-index) bits of chunk c, table bit j
+    int cn[4];
+    int ccontig[4];              // chunk bits contiguous: lo = cbits[c][0]
+    const double2 *tab[4];       // chunk tables (2^cn entries)
+};
+
+// Tile pass op (TOP_DENSE covers dense and controlled).
+struct TileOp {
+    int kind;                    // 0 dense/controlled, 1 diagonal, 2 recip
+    int k;                       // dense: targets
+    int tpos[5];                 // dense: tile-local target positions
+    int nins;
+    int ins[16];                 // dense: sorted tile-local positions (targets + local controls)
+    uint32_t lcset;              // dense: tile-local control bits required to be 1
+    uint64_t gcmask, gcval;      // controls on non-tile bits (global index): op skipped unless match
+    // diagonal
+    int ndl;
+    int dl_pos[kMaxDiag], dl_tbit[kMaxDiag];
+    int ndg;
+    int dg_bit[kMaxDiag], dg_tbit[kMaxDiag];   // global-index bit -> table bit
+    // recip
+    int anc;                     // tile-local position of the ancilla
+    int nlc;
+    int lc_pos[32], lc_bit[32];
+    int ngc;
+    int gc_bit[kMaxClock], gc_rbit[kMaxClock]; // global-index bit -> register bit
+    int n_c, is_signed;
+    double dL, snap;
+    uint64_t data_off;           // matrix/table offset in the program blob (double2 units)
+};
+
+struct TileArgs {
+    double2 *psi;
+    uint64_t n_tiles;            // 2^(nloc - T)
+    int T;
+    int tbits[16];               // sorted physical local bits of the tile
+    int nops;
+    const TileOp *ops;           // device array
+    const double2 *blob;         // program data blob
+    uint64_t rank_base;
+    int maxk;                    // largest dense k in the op list (sizes the matrix buffer)
+};
+
+// ---- launchers (stream-ordered, no sync) ----
+cudaError_t launch_dense(const DenseArgs &a, cudaStream_t s);
+cudaError_t launch_diag(const DiagArgs &a, cudaStream_t s);
+cudaError_t launch_recip(const RecipArgs &a, cudaStream_t s);
+cudaError_t launch_product(const ProductArgs &a, cudaStream_t s);
+cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream_t s);
+cudaError_t launch_tile(const TileArgs &a, cudaStream_t s);
+size_t tile_smem_bytes(int T, int maxk);
+
+// Deterministic reductions. partial has >= kRedBlocks doubles; result written to out (device).
+constexpr int kRedBlocks = 1184;   // 148 SMs x 8
+cudaError_t launch_norm2(const double2 *psi, uint64_t n, double *partial, double *out, cudaStream_t s);
+// Marginal over physical bits S (q = |S| <= 26, bit j of v <- S[j]); others O = remaining local bits.
+// Writes 2^q doubles to out (device). ws must hold 2^q * C doubles (C returned by marginal_chunks).
+int marginal_chunks(int nloc, int q);
+cudaError_t launch_marginal(const double2 *psi, int nloc, const int *S, int q, double *ws, double *out,
+                            cudaStream_t s);
+// Gather amplitudes by LOGICAL index: for e < count, logical index L = fixed | deposit(first+e into free bits)
+// (free = NULL: L = first + e). Physical global index via phys[]; elements not owned by rank -> 0.
+struct GatherArgs {
+    const double2 *psi;
+    double2 *out;
+    uint64_t count;
+    uint64_t first;
+    int n;
+    int nloc;
+    uint64_t rank;
+    int phys[64];
+    int nfree;                   // 0 -> contiguous logical range
+    int free_q[64];              // free logical qubits ascending (postselect)
+    uint64_t fixed;              // logical bits of fixed qubits
+};
+cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s);
+struct ScatterArgs {             // inverse of gather (sv_write): only owned elements are written
+    double2 *psi;
+    const double2 *in;
+    uint64_t count, first;
+    int n, nloc;
+    uint64_t rank;
+    int phys[64];
+};
+cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
+// Exchange helpers: pack/unpack the half of the local state whose bit lbit == val, elements [off, off+cnt).
+cudaError_t launch_pack(const double2 *psi, double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
+                        cudaStream_t s);
+cudaError_t launch_unpack(double2 *psi, const double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
+                          cudaStream_t s);
+
+}  // namespace dev
+}  // namespace hhlsv

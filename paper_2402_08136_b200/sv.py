@@ -1,0 +1,406 @@
+"""Thin ctypes binding of include/sv.h (argument marshalling only).
+
+Every function here forwards to the same-named C entry point of libhhlsv.so; all
+state-vector work happens in the library's CUDA kernels. There is no CPU fallback:
+if the library is missing, or no CUDA device is present, calls raise SVError.
+PyTorch is used only to hand the library the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhhlsv.so")
+
+SV_DENSE, SV_CONTROLLED, SV_DIAGONAL, SV_RECIP_RY, SV_SWAP = range(5)
+_KINDS = {"dense": SV_DENSE, "controlled": SV_CONTROLLED, "diagonal": SV_DIAGONAL, "recip_ry": SV_RECIP_RY,
+          "swap": SV_SWAP}
+STATUS = ["SV_OK", "SV_E_ARG", "SV_E_RANGE", "SV_E_NOTUNITARY", "SV_E_NOTHERMITIAN", "SV_E_CLOCK",
+          "SV_E_ZEROPROB", "SV_E_OOM", "SV_E_CUDA", "SV_E_NCCL"]
+
+
+class SVError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS[code] if 0 <= code < len(STATUS) else code}: {msg}")
+        self.code = code
+        self.status = STATUS[code] if 0 <= code < len(STATUS) else str(code)
+
+
+class sv_dist(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int), ("rank", ctypes.c_int), ("device", ctypes.c_int),
+                ("nccl_id", ctypes.c_char_p)]
+
+
+class sv_gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("n_targets", ctypes.c_int), ("targets", ctypes.POINTER(ctypes.c_int)),
+                ("n_controls", ctypes.c_int), ("controls", ctypes.POINTER(ctypes.c_int)),
+                ("control_values", ctypes.c_uint64), ("data", ctypes.POINTER(ctypes.c_double)),
+                ("recip_delta", ctypes.c_double), ("recip_signed", ctypes.c_int), ("recip_snap", ctypes.c_double)]
+
+
+class sv_fuse_options(ctypes.Structure):
+    _fields_ = [("fusion_kmax", ctypes.c_int), ("diag_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int)]
+
+
+class sv_plan_report(ctypes.Structure):
+    _fields_ = [("n_logical", ctypes.c_uint64), ("n_fused", ctypes.c_uint64), ("n_passes", ctypes.c_uint64),
+                ("alg_bytes", ctypes.c_double), ("pass_bytes", ctypes.c_double)]
+
+
+class hhl_options(ctypes.Structure):
+    _fields_ = [("clock_qubits", ctypes.c_int), ("fusion_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
+                ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int)]
+
+
+class hhl_report(ctypes.Structure):
+    _fields_ = [("p_success", ctypes.c_double), ("norm2", ctypes.c_double), ("lambda_min", ctypes.c_double),
+                ("lambda_max", ctypes.c_double), ("kappa", ctypes.c_double), ("delta", ctypes.c_double),
+                ("t_evol", ctypes.c_double), ("n_data", ctypes.c_int), ("n_clock", ctypes.c_int),
+                ("n_total", ctypes.c_int), ("n_logical", ctypes.c_uint64), ("n_fused", ctypes.c_uint64),
+                ("n_passes", ctypes.c_uint64), ("alg_bytes", ctypes.c_double), ("pass_bytes", ctypes.c_double),
+                ("t_frontend_s", ctypes.c_double), ("t_sim_s", ctypes.c_double), ("h2d_bytes", ctypes.c_double),
+                ("d2h_bytes", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_destroy", "sv_reset", "sv_info",
+           "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
+           "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
+           "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
+           "sv_norm2", "sv_postselect_slice", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve"]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libhhlsv.so (raises if it is missing: the product has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise SVError(8, f"{path} not built (run python -m paper_2402_08136_b200.build)")
+    L = ctypes.CDLL(path)
+    P, c_int, c_u64, c_dbl, vp = ctypes.POINTER, ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+    L.sv_last_error.restype = ctypes.c_char_p
+    L.sv_version.restype = ctypes.c_char_p
+    sig = {
+        "sv_nccl_unique_id": [ctypes.c_char_p],
+        "sv_create": [c_int, P(sv_dist), vp, P(vp)],
+        "sv_destroy": [vp], "sv_reset": [vp],
+        "sv_info": [vp, P(c_int), P(c_u64), P(vp)],
+        "sv_qubit_map": [vp, P(c_int)],
+        "sv_sync": [vp],
+        "sv_read": [vp, c_u64, c_u64, P(c_dbl)],
+        "sv_write": [vp, c_u64, c_u64, P(c_dbl)],
+        "sv_apply_fused": [vp, P(sv_gate), ctypes.c_size_t],
+        "sv_apply_circuit": [vp, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), P(sv_plan_report)],
+        "sv_program_create": [vp, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), P(vp), P(sv_plan_report)],
+        "sv_program_run": [vp, vp], "sv_program_destroy": [vp],
+        "sv_program_dump": [vp, ctypes.c_char_p, ctypes.c_size_t],
+        "sv_program_set_timing": [vp, c_int],
+        "sv_program_timings": [vp, P(ctypes.c_float), P(c_int), P(c_dbl), P(c_int), ctypes.c_size_t,
+                               P(ctypes.c_size_t)],
+        "sv_program_stats": [vp, P(c_u64), P(c_u64)],
+        "sv_schedule_dump": [c_int, c_int, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), ctypes.c_char_p,
+                             ctypes.c_size_t, P(sv_plan_report)],
+        "sv_probabilities": [vp, P(c_int), c_int, P(c_dbl)],
+        "sv_norm2": [vp, P(c_dbl)],
+        "sv_postselect_slice": [vp, P(c_int), P(c_int), c_int, P(c_dbl), P(c_u64), c_u64, P(c_dbl)],
+        "hhl_plan_size": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(c_int), P(c_int), P(c_int)],
+        "hhl_build_program": [vp, P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(vp), P(hhl_report)],
+        "hhl_readout": [vp, P(hhl_report), c_int, c_dbl, P(c_dbl), P(c_dbl)],
+        "hhl_solve": [P(c_dbl), P(c_dbl), c_int, c_int, P(hhl_options), P(sv_dist), vp, P(c_dbl), P(hhl_report)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise SVError(rc, load().sv_last_error().decode())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(lst):
+    return (ctypes.c_int * max(1, len(lst)))(*[int(x) for x in lst])
+
+
+def _current_stream():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:
+        pass
+    return ctypes.c_void_p(0)
+
+
+class _GateArray:
+    """Marshal a list of gate dicts (workloads/synthetic.py format) into sv_gate[] (keeps buffers alive)."""
+
+    def __init__(self, gates):
+        self.keep = []
+        self.arr = (sv_gate * max(1, len(gates)))()
+        for i, g in enumerate(gates):
+            s = self.arr[i]
+            s.kind = _KINDS[g["kind"]]
+            t = _ip(g["targets"])
+            s.n_targets = len(g["targets"])
+            s.targets = t
+            c = list(g.get("controls", []))
+            ca = _ip(c)
+            s.n_controls = len(c)
+            s.controls = ca
+            s.control_values = int(g.get("cvals", (1 << len(c)) - 1 if c else 0))
+            self.keep += [t, ca]
+            if "data" in g and g["data"] is not None:
+                d = np.ascontiguousarray(np.asarray(g["data"], dtype=np.complex128)).view(np.float64)
+                self.keep.append(d)
+                s.data = _dp(d)
+            s.recip_delta = float(g.get("delta", 0.0))
+            s.recip_signed = int(g.get("signed", 1))
+            s.recip_snap = float(g.get("snap", 0.0))
+        self.n = len(gates)
+
+
+def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0):
+    return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().sv_nccl_unique_id(buf))
+    return buf.raw
+
+
+class State:
+    """A (sharded) n-qubit state vector on the GPU (sv_create / sv_destroy)."""
+
+    def __init__(self, n_qubits: int, world: int = 1, rank: int = 0, device: int = -1, nccl_id: bytes | None = None,
+                 stream=None):
+        L = load()
+        self._h = ctypes.c_void_p()
+        self._dist = None
+        if world > 1 or device >= 0:
+            self._idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+            self._dist = sv_dist(world, rank, device, ctypes.cast(self._idbuf, ctypes.c_char_p) if self._idbuf else None)
+        self.stream = stream if stream is not None else _current_stream()
+        _check(L.sv_create(int(n_qubits), ctypes.byref(self._dist) if self._dist else None, self.stream,
+                           ctypes.byref(self._h)))
+        self.n = int(n_qubits)
+        self.world, self.rank = world, rank
+
+    @property
+    def handle(self):
+        return self._h
+
+    def destroy(self):
+        if self._h:
+            _check(load().sv_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def reset(self):
+        _check(load().sv_reset(self._h))
+
+    def info(self):
+        n, la, p = ctypes.c_int(), ctypes.c_uint64(), ctypes.c_void_p()
+        _check(load().sv_info(self._h, ctypes.byref(n), ctypes.byref(la), ctypes.byref(p)))
+        return n.value, la.value, p.value
+
+    def qubit_map(self):
+        m = (ctypes.c_int * self.n)()
+        _check(load().sv_qubit_map(self._h, m))
+        return list(m)
+
+    def sync(self):
+        _check(load().sv_sync(self._h))
+
+    def read(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        count = (1 << self.n) - first if count is None else count
+        out = np.empty(count, dtype=np.complex128)
+        _check(load().sv_read(self._h, first, count, _dp(out.view(np.float64))))
+        return out
+
+    def write(self, amps, first: int = 0):
+        a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128))
+        _check(load().sv_write(self._h, first, a.size, _dp(a.view(np.float64))))
+
+    def apply_fused(self, gates):
+        ga = _GateArray(gates)
+        _check(load().sv_apply_fused(self._h, ga.arr, ga.n))
+
+    def apply_circuit(self, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0) -> dict:
+        ga = _GateArray(gates)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+        rep = sv_plan_report()
+        _check(load().sv_apply_circuit(self._h, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(rep)))
+        return {f: getattr(rep, f) for f, _ in rep._fields_}
+
+    def probabilities(self, qubits) -> np.ndarray:
+        out = np.empty(1 << len(qubits))
+        _check(load().sv_probabilities(self._h, _ip(qubits), len(qubits), _dp(out)))
+        return out
+
+    def norm2(self) -> float:
+        v = ctypes.c_double()
+        _check(load().sv_norm2(self._h, ctypes.byref(v)))
+        return v.value
+
+    def postselect_slice(self, fixed_q, fixed_v):
+        nfree = self.n - len(fixed_q)
+        amps = np.empty(1 << nfree, dtype=np.complex128)
+        idx = np.empty(1 << nfree, dtype=np.uint64)
+        p = ctypes.c_double()
+        _check(load().sv_postselect_slice(self._h, _ip(fixed_q), _ip(fixed_v), len(fixed_q),
+                                          _dp(amps.view(np.float64)),
+                                          idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), amps.size,
+                                          ctypes.byref(p)))
+        return amps, idx, p.value
+
+
+class Program:
+    """A fused, scheduled circuit resident on the device (sv_program_*)."""
+
+    def __init__(self, state: State, handle, report: dict):
+        self.state = state
+        self._h = handle
+        self.report = report
+
+    @classmethod
+    def create(cls, state: State, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0):
+        ga = _GateArray(gates)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+        h = ctypes.c_void_p()
+        rep = sv_plan_report()
+        _check(load().sv_program_create(state.handle, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(h),
+                                        ctypes.byref(rep)))
+        return cls(state, h, {f: getattr(rep, f) for f, _ in rep._fields_})
+
+    def run(self):
+        _check(load().sv_program_run(self.state.handle, self._h))
+
+    def dump(self) -> str:
+        buf = ctypes.create_string_buffer(1 << 20)
+        _check(load().sv_program_dump(self._h, buf, len(buf)))
+        return buf.value.decode()
+
+    def set_timing(self, enable: bool = True):
+        _check(load().sv_program_set_timing(self._h, int(enable)))
+
+    def timings(self):
+        """Per-step (ms, kind, bytes, launches) of the last run (needs set_timing(True) before it)."""
+        n = ctypes.c_size_t()
+        _check(load().sv_program_timings(self._h, None, None, None, None, 0, ctypes.byref(n)))
+        cap = n.value
+        ms = (ctypes.c_float * max(1, cap))()
+        kd = (ctypes.c_int * max(1, cap))()
+        by = (ctypes.c_double * max(1, cap))()
+        la = (ctypes.c_int * max(1, cap))()
+        _check(load().sv_program_timings(self._h, ms, kd, by, la, cap, ctypes.byref(n)))
+        return [(ms[i], kd[i], by[i], la[i]) for i in range(cap)]
+
+    def stats(self):
+        la, h2d = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(load().sv_program_stats(self._h, ctypes.byref(la), ctypes.byref(h2d)))
+        return {"launches": la.value, "h2d_bytes": h2d.value}
+
+    def destroy(self):
+        if self._h:
+            _check(load().sv_program_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+STEP_KINDS = ["init_zero", "init_product", "dense", "diagonal", "recip_ry", "tile", "exchange"]
+
+
+def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax=0, tile_qubits=0):
+    """Host-only: fuse + schedule a logical gate list (no GPU needed). Returns (text, report)."""
+    ga = _GateArray(gates)
+    o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+    buf = ctypes.create_string_buffer(1 << 22)
+    rep = sv_plan_report()
+    _check(load().sv_schedule_dump(int(n_qubits), int(world), ga.arr, ga.n, ctypes.byref(o), buf, len(buf),
+                                   ctypes.byref(rep)))
+    return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
+
+
+def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0):
+    return hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap), int(init_fold))
+
+
+def hhl_plan_size(A, b, **kw):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    o = _opts(**kw)
+    nd, nc, nt = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(load().hhl_plan_size(_dp(A), _dp(b), b.size, ctypes.byref(o), ctypes.byref(nd), ctypes.byref(nc),
+                                ctypes.byref(nt)))
+    return nd.value, nc.value, nt.value
+
+
+class HHLProgram(Program):
+    """hhl_build_program: the HHL circuit for (A, b) as a resident program on `state`."""
+
+    @classmethod
+    def build(cls, state: State, A, b, **kw):
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        o = _opts(**kw)
+        h = ctypes.c_void_p()
+        rep = hhl_report()
+        _check(load().hhl_build_program(state.handle, _dp(A), _dp(b), b.size, ctypes.byref(o), ctypes.byref(h),
+                                        ctypes.byref(rep)))
+        p = cls(state, h, rep.as_dict())
+        p._rep = rep
+        p.N = b.size
+        p.b_norm = float(np.linalg.norm(b))
+        return p
+
+    def readout(self):
+        x = np.empty(self.N)
+        ps = ctypes.c_double()
+        _check(load().hhl_readout(self.state.handle, ctypes.byref(self._rep), self.N, self.b_norm, _dp(x),
+                                  ctypes.byref(ps)))
+        return x, ps.value
+
+
+def hhl_solve(A, b, clock_qubits=0, world=1, rank=0, device=-1, nccl_id=None, stream=None, **kw):
+    """Solve A x = b with the simulated HHL circuit on the GPU(s). A, b, x are host arrays."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    o = _opts(clock_qubits=clock_qubits, **kw)
+    x = np.empty(b.size)
+    rep = hhl_report()
+    dist = None
+    idbuf = None
+    if world > 1 or device >= 0:
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        dist = sv_dist(world, rank, device, ctypes.cast(idbuf, ctypes.c_char_p) if idbuf else None)
+    _check(load().hhl_solve(_dp(A), _dp(b), b.size, int(clock_qubits), ctypes.byref(o),
+                            ctypes.byref(dist) if dist else None, stream if stream is not None else _current_stream(),
+                            _dp(x), ctypes.byref(rep)))
+    return x, rep.as_dict()

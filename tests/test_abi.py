@@ -1,0 +1,146 @@
+"""Host-side checks of the C-ABI library (-m "not gpu"): it loads, exports every symbol
+include/sv.h declares, refuses to compute without a GPU (no CPU fallback), and its host
+front end / scheduler logic (hhl_plan_size, sv_schedule_dump) behaves."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2402_08136_b200 as pkg
+from oracle import hhl as ohhl
+from workloads import configs, matpower, synthetic
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2402_08136_b200 import build
+    build.build()
+    return pkg.load()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "sv.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:sv_status|const char \*)\s*(\w+)\s*\(", src, flags=re.M)))
+
+
+def test_exports_every_header_symbol(lib):
+    names = header_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(pkg.EXPORTS)
+
+
+def test_library_is_sm100a_only(lib):
+    assert b"sm_100a" in lib.sv_version()
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pkg.SVError) as e:
+        pkg.State(5)
+    assert e.value.status == "SV_E_CUDA"
+    A, b, nc = configs.get("C1")
+    with pytest.raises(pkg.SVError) as e:
+        pkg.hhl_solve(A, b, clock_qubits=nc)
+    assert e.value.status == "SV_E_CUDA"
+
+
+def test_plan_size_matches_table1(lib):
+    """Host front end resources (Table 1): 14-bus 13 = (4, 8), 30-bus 16 = (5, 10)."""
+    A, b = matpower.case14()
+    assert pkg.hhl_plan_size(A, b) == (4, 8, 13)
+    A, b = matpower.case30()
+    assert pkg.hhl_plan_size(A, b) == (5, 10, 16)
+    for name in ("C1", "C2", "C3", "S30", "S33"):
+        A, b, nc = configs.get(name)
+        assert pkg.hhl_plan_size(A, b, clock_qubits=nc)[2] == configs.n_qubits(name)
+
+
+def test_plan_errors(lib):
+    A, b = matpower.case5()
+    with pytest.raises(pkg.SVError) as e:
+        pkg.hhl_plan_size(A, b, clock_qubits=5)          # delta = 0
+    assert e.value.status == "SV_E_CLOCK"
+    with pytest.raises(pkg.SVError) as e:
+        pkg.hhl_plan_size(A, np.zeros(4))
+    assert e.value.status == "SV_E_ARG"
+    with pytest.raises(pkg.SVError) as e:
+        pkg.hhl_plan_size(np.array([[1.0, 2.0], [0.0, 1.0]]), np.ones(2))
+    assert e.value.status == "SV_E_NOTHERMITIAN"
+
+
+def test_gate_validation(lib):
+    bad = [{"kind": "dense", "targets": [0], "data": np.array([[1, 1], [0, 1]], complex)}]
+    with pytest.raises(pkg.SVError) as e:
+        pkg.schedule_dump(3, bad)
+    assert e.value.status == "SV_E_NOTUNITARY"
+    with pytest.raises(pkg.SVError) as e:
+        pkg.schedule_dump(3, [{"kind": "dense", "targets": [0, 0], "data": np.eye(4)}])
+    assert e.value.status == "SV_E_ARG"
+    with pytest.raises(pkg.SVError) as e:
+        pkg.schedule_dump(3, [{"kind": "dense", "targets": [3], "data": np.eye(2)}])
+    assert e.value.status == "SV_E_ARG"
+    with pytest.raises(pkg.SVError):
+        pkg.schedule_dump(7, [{"kind": "dense", "targets": list(range(6)), "data": np.eye(64)}])
+
+
+def _sched(n, gates, **kw):
+    txt, rep = pkg.schedule_dump(n, gates, **kw)
+    return txt.splitlines(), rep
+
+
+def test_fusion_counts_s30(lib):
+    """Sequential greedy k<=4 fusion of the S30 circuit (after the folded prep + H layer):
+    168 fused ops ('S30 -> 168'), and the tile scheduler needs <= 8 passes."""
+    A, b, nc = configs.get("S30")
+    p = ohhl.plan(A, b, nc)
+    g = ohhl.build(p)[1 + nc:]
+    _, rep = _sched(p.n, g, fusion_kmax=4, tile_qubits=-1)
+    assert rep["n_fused"] == 168 and rep["n_passes"] == 168
+    _, rep2 = _sched(p.n, g, fusion_kmax=4, tile_qubits=12)
+    assert rep2["n_fused"] == 168 and rep2["n_passes"] <= 8
+    assert rep2["alg_bytes"] == rep["alg_bytes"]
+
+
+def test_swaps_are_relabels(lib):
+    """IQFT/QFT swaps never become data movement; a lone swap only changes the final map."""
+    lines, rep = _sched(4, [{"kind": "swap", "targets": [0, 3]}], tile_qubits=-1)
+    assert rep["n_passes"] == 0
+    assert lines[-1] == "FINAL_MAP 3 1 2 0"
+
+
+def test_exchange_scheduler_pairs_global_targets(lib):
+    """world=4 (2 global bits): every dense op on a global bit gets exactly one EXCHANGE before it,
+    and controls / diagonals on global bits never do."""
+    n = 8
+    H = np.array([[1, 1], [1, -1]], complex) / np.sqrt(2)
+    X = np.array([[0, 1], [1, 0]], complex)
+    gates = [{"kind": "controlled", "targets": [0], "controls": [7], "cvals": 1, "data": X},
+             {"kind": "diagonal", "targets": [6, 7], "data": np.exp(1j * np.arange(4))},
+             {"kind": "dense", "targets": [7], "data": H}]
+    lines, rep = _sched(n, gates, world=4, fusion_kmax=0, tile_qubits=-1)
+    kinds = [ln.split()[0] for ln in lines]
+    assert kinds[:2] == ["CONTROLLED", "DIAGONAL"]
+    assert kinds[2] == "EXCHANGE" and kinds[3] == "DENSE"
+    ex = lines[2].split()
+    assert ex[1] == "global=7" and int(ex[2].split("=")[1]) < 6
+
+
+def test_random_circuit_schedule_covers_all_ops(lib):
+    gates = synthetic.random_circuit(10, 60, seed=3, kmax=3)
+    for T in (-1, 6, 10):
+        for w in (1, 2, 4):
+            lines, rep = _sched(10, gates, world=w, fusion_kmax=3, tile_qubits=T)
+            n_ops = sum(1 for ln in lines if ln.startswith("  ") or ln.split()[0] in
+                        ("DENSE", "CONTROLLED", "DIAGONAL", "RECIP_RY"))
+            assert n_ops == rep["n_fused"]

@@ -275,3 +275,14 @@ def test_accuracy_improves_with_clock_register():
         errs.append(np.linalg.norm(x / np.linalg.norm(x) - xt))
     assert errs[0] > errs[1] > errs[2]
     assert errs[-1] < 5e-3
+
+
+def test_alpha_geometric_equals_fft():
+    """The geometric-series QPE amplitude (used at n_c > 16) equals the FFT of the phase vector."""
+    for phi in (0.123456789, 0.25, 0.49999, 1 / 3):
+        for nc in (4, 10, 14):
+            a = cf.alpha_geometric(phi, nc)
+            b = np.fft.fft(cf.phase_vector(phi, nc)) / (1 << nc)
+            assert np.abs(a - b).max() < 1e-12          # FFT sums 2^nc rounded terms
+            p2 = cf.alpha_abs2(phi, nc)
+            assert np.abs(p2 - np.abs(b) ** 2).max() < 5e-12
