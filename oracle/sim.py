@@ -3,7 +3,8 @@
 Applies a logical gate list (workloads/synthetic.py dict format) one gate at a
 time in fp64, exactly as each gate's plain definition states (SURVEY §8(c):
 psi = G_L ... G_2 G_1 |0...0>). Named gate kinds are expanded here to their
-textbook dense matrices; 'diagonal' is diag(data); 'swap' is the 4×4 SWAP
+textbook dense matrices; 'diagonal' multiplies each amplitude by its table entry
+(sv_oracle.c orc_apply_diagonal); 'swap' is the 4×4 SWAP
 permutation. No fusion, no blocking, no reordering.
 """
 from __future__ import annotations
@@ -39,6 +40,8 @@ def lib():
                                            ctypes.c_int, P(ctypes.c_int), ctypes.c_uint64, P(ctypes.c_double)]
         L.orc_apply_recip_ry.argtypes = [ctypes.c_int, P(ctypes.c_double), ctypes.c_int, ctypes.c_int,
                                          P(ctypes.c_int), ctypes.c_double, ctypes.c_int, ctypes.c_double]
+        L.orc_apply_diagonal.argtypes = [ctypes.c_int, P(ctypes.c_double), ctypes.c_int, P(ctypes.c_int),
+                                         P(ctypes.c_double)]
         L.orc_recip_s.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double]
         L.orc_recip_s.restype = ctypes.c_double
         L.orc_marginal.argtypes = [ctypes.c_int, P(ctypes.c_double), ctypes.c_int, P(ctypes.c_int),
@@ -85,7 +88,12 @@ def apply_gate(psi: np.ndarray, n: int, g: dict) -> None:
     assert psi.dtype == np.complex128 and psi.flags.c_contiguous and psi.size == 1 << n
     L = lib()
     fp = _dp(psi.view(np.float64))
-    if g["kind"] == "recip_ry":
+    if g["kind"] == "diagonal":
+        d = np.ascontiguousarray(g["data"], dtype=np.complex128)
+        t = list(g["targets"])
+        assert d.size == 1 << len(t)
+        rc = L.orc_apply_diagonal(n, fp, len(t), _ip(t), _dp(d.view(np.float64)))
+    elif g["kind"] == "recip_ry":
         clock = list(g["controls"])
         rc = L.orc_apply_recip_ry(n, fp, int(g["targets"][0]), len(clock), _ip(clock), float(g["delta"]),
                                   int(g.get("signed", 1)), float(g.get("snap", 0.0)))

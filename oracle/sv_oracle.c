@@ -68,6 +68,23 @@ int orc_apply_controlled(int n, double *psi_il, int k, const int *targets, int n
     return 0;
 }
 
+/* Diagonal gate: psi_i <- d[bits(i, qubits)] psi_i (bit j of the table index = qubits[j]).
+ * Plain definition of a diagonal unitary (the CP ladders of the (I)QFT are diagonal). */
+int orc_apply_diagonal(int n, double *psi_il, int k, const int *qubits, const double *d_il) {
+    if (k < 1 || k > 30 || n < k) return -1;
+    cplx *psi = (cplx *)psi_il;
+    const cplx *d = (const cplx *)d_il;
+    const uint64_t N = 1ull << n;
+#pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < (int64_t)N; ii++) {
+        uint64_t v = 0;
+        for (int j = 0; j < k; j++)
+            if (((uint64_t)ii >> qubits[j]) & 1ull) v |= 1ull << j;
+        psi[ii] *= d[v];
+    }
+    return 0;
+}
+
 /* Eigenvalue-inversion rotation (the uniformly-controlled RY of Fig. 5,
  * PAPER.md:212-217, built "following the settings in [qlsarepo]").
  * For clock value m = sum_j bit(clock[j]) 2^j (LSB first) and half-range

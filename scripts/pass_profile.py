@@ -1,0 +1,39 @@
+"""Per-step CUDA-event timing of one HHL program (developer tool, GPU only).
+
+    python scripts/pass_profile.py [--config S30] [--kmax 4] [--tile 12] [--reps 2]
+Prints each scheduled step (kind, ops, ms, GB/s of its HBM bytes) and the total.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2402_08136_b200 as pkg  # noqa: E402
+from workloads import configs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="S30")
+ap.add_argument("--kmax", type=int, nargs="+", default=[4])
+ap.add_argument("--tile", type=int, nargs="+", default=[12])
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--verbose", action="store_true")
+a = ap.parse_args()
+A, b, nc = configs.get(a.config)
+st = pkg.State(configs.n_qubits(a.config))
+for k in a.kmax:
+    for T in a.tile:
+        prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=k, tile_qubits=T)
+        prog.set_timing(True)
+        for _ in range(a.reps):
+            prog.run()
+            t = prog.timings()
+        dump = prog.dump().splitlines()
+        heads = [ln for ln in dump if not ln.startswith("  ")]
+        total = sum(x[0] for x in t)
+        print(f"== {a.config} kmax={k} tile={T}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
+              f"total {total:.1f} ms")
+        if a.verbose or True:
+            for (ms, kind, by, la), h in zip(t, heads):
+                print(f"   {ms:9.3f} ms  {by / ms / 1e6 if ms > 0 else 0:8.1f} GB/s  {h[:100]}")
+        prog.destroy()
