@@ -297,7 +297,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     const double t0 = now_s();
     HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
-    std::vector<Gate> gates = hhl_build(p);
+    std::vector<Gate> gates = hhl_build(p, opt ? opt->qpe_mode : 0);
     const bool fold = !opt || opt->init_fold >= 0;
     std::vector<ProductFactor> factors;
     size_t nf = fold ? fold_product_prefix(gates, p.n, factors) : 0;

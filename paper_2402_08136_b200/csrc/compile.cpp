@@ -55,7 +55,9 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
         s.n_passes++;
     }
     const int T = std::min(o.tile_qubits, nloc);
-    const bool tiles = o.tile_qubits > 0;
+    const bool tiles = o.tile_qubits > 0 && nloc >= o.reg_bits + 3;
+    const int wmin = std::min(o.wmin, T - o.reg_bits);
+    const int R = o.reg_bits;
 
     // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.
     std::vector<std::vector<size_t>> uses(n);
@@ -78,6 +80,27 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
             if (std::find(set.begin(), set.end(), b) == set.end()) set.push_back(b);
         std::sort(set.begin(), set.end());
         tile.tile_bits = set;
+        // register phases: greedy, each phase's ops have their nd targets inside R (|R| <= reg_bits)
+        std::vector<int> cur;
+        for (size_t oi = 0; oi < tile.tile_ops.size(); oi++) {
+            std::vector<int> u = cur;
+            for (int b : nd_targets(tile.tile_ops[oi]))
+                if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
+            if (oi == 0 || (int)u.size() > R) {
+                if (oi > 0) tile.phase_R.push_back(cur);
+                tile.phase_start.push_back(oi);
+                u.clear();
+                for (int b : nd_targets(tile.tile_ops[oi])) u.push_back(b);
+            }
+            cur = u;
+        }
+        tile.phase_R.push_back(cur);
+        tile.phase_start.push_back(tile.tile_ops.size());
+        for (auto &rr : tile.phase_R) {       // fill with the highest tile bits (lanes keep the low ones)
+            for (int i = (int)set.size() - 1; (int)rr.size() < R && i >= 0; i--)
+                if (std::find(rr.begin(), rr.end(), set[i]) == rr.end()) rr.push_back(set[i]);
+            std::sort(rr.begin(), rr.end());
+        }
         tile.bytes = 32.0 * local_amps;
         s.pass_bytes += tile.bytes;
         s.n_passes++;
@@ -123,7 +146,9 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
             std::swap(phys[q], phys[victim]);
         }
         Gate pg = to_physical(g, phys);
-        if (!tiles) {
+        const bool too_wide = (g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R;
+        if (!tiles || too_wide) {
+            close_tile();
             Step st;
             switch (g.kind) {
                 case Kind::Dense:
@@ -164,7 +189,12 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
         std::vector<int> u = tile_nd;
         for (int b : pnd)
             if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
-        if (tile_open && (int)u.size() > T) {
+        auto fits = [&](const std::vector<int> &v) {
+            int high = 0;
+            for (int b : v) high += b >= wmin;
+            return (int)v.size() <= T && high <= T - wmin;
+        };
+        if (tile_open && !fits(u)) {
             close_tile();
             u = pnd;
         }

@@ -217,7 +217,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     auto rank_bit = [&](int phys_bit) -> int { return (int)((rank_base >> phys_bit) & 1ull); };
 
     std::vector<double2> blob;
-    std::vector<dev::TileOp> tops;
+    std::vector<dev::RegOp> rops;
+    std::vector<dev::RegPhase> phases;
     auto push_data = [&](const std::vector<cplx> &d) {
         size_t off = blob.size();
         for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
@@ -328,79 +329,97 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
                 a.n_tiles = 1ull << (nloc - a.T);
                 a.rank_base = rank_base;
-                a.maxk = 0;
-                const size_t op0 = tops.size();
-                for (const Gate &g : st.tile_ops) {
-                    dev::TileOp t{};
-                    if (g.kind == Kind::Dense || g.kind == Kind::Controlled) {
-                        t.kind = 0;
-                        t.k = (int)g.targets.size();
-                        a.maxk = std::max(a.maxk, t.k);
-                        std::vector<int> ins;
-                        for (int i = 0; i < t.k; i++) {
-                            t.tpos[i] = index_in(st.tile_bits, g.targets[i]);
-                            if (t.tpos[i] < 0) fail(SV_E_ARG, "internal: tile target not local");
-                            ins.push_back(t.tpos[i]);
-                        }
-                        for (size_t j = 0; j < g.controls.size(); j++) {
-                            const int b = g.controls[j];
-                            const int want = (int)((g.cvals >> j) & 1ull);
-                            const int lp = index_in(st.tile_bits, b);
-                            if (lp >= 0) {
-                                ins.push_back(lp);
-                                if (want) t.lcset |= 1u << lp;
-                            } else {
-                                t.gcmask |= 1ull << b;
-                                if (want) t.gcval |= 1ull << b;
+                const size_t ph0 = phases.size();
+                for (size_t pi = 0; pi + 1 < st.phase_start.size(); pi++) {
+                    dev::RegPhase ph{};
+                    const std::vector<int> &Rp = st.phase_R[pi];   // physical bits, ascending
+                    std::vector<int> Rt;                            // tile positions
+                    for (int b : Rp) Rt.push_back(index_in(st.tile_bits, b));
+                    for (int i = 0; i < dev::kRegBits; i++) ph.R[i] = Rt[i];
+                    int nt = 0;
+                    for (int tp = 0; tp < a.T; tp++)
+                        if (std::find(Rt.begin(), Rt.end(), tp) == Rt.end()) ph.tpos[nt++] = tp;
+                    ph.op0 = (int)rops.size();
+                    for (size_t oi = st.phase_start[pi]; oi < st.phase_start[pi + 1]; oi++) {
+                        const Gate &g = st.tile_ops[oi];
+                        dev::RegOp r{};
+                        auto regbit = [&](int phys_bit) { return index_in(Rp, phys_bit); };
+                        auto route = [&](int b, int out, int *rb, int *ro, int &nr, int *tpos, int *to, int &ntt,
+                                         int *gb, int *go, int &ng) {
+                            const int tp = index_in(st.tile_bits, b);
+                            const int rg = regbit(b);
+                            if (rg >= 0) { rb[nr] = rg; ro[nr] = out; nr++; }
+                            else if (tp >= 0) { tpos[ntt] = tp; to[ntt] = out; ntt++; }
+                            else { gb[ng] = b; go[ng] = out; ng++; }
+                        };
+                        if (g.kind == Kind::Dense || g.kind == Kind::Controlled) {
+                            r.kind = 0;
+                            const int k = (int)g.targets.size();
+                            std::vector<int> rb(k);
+                            for (int i = 0; i < k; i++) {
+                                rb[i] = regbit(g.targets[i]);
+                                if (rb[i] < 0) fail(SV_E_ARG, "internal: phase target not in registers");
+                                r.mask |= 1 << rb[i];
                             }
-                        }
-                        std::sort(ins.begin(), ins.end());
-                        if (ins.size() > 16) fail(SV_E_ARG, "too many tile-local controls");
-                        t.nins = (int)ins.size();
-                        for (size_t i = 0; i < ins.size(); i++) t.ins[i] = ins[i];
-                        t.data_off = push_data(g.data);
-                    } else if (g.kind == Kind::Diagonal) {
-                        t.kind = 1;
-                        for (size_t j = 0; j < g.targets.size(); j++) {
-                            const int b = g.targets[j];
-                            const int lp = index_in(st.tile_bits, b);
-                            if (lp >= 0) {
-                                t.dl_pos[t.ndl] = lp;
-                                t.dl_tbit[t.ndl] = (int)j;
-                                t.ndl++;
-                            } else {
-                                t.dg_bit[t.ndg] = b;
-                                t.dg_tbit[t.ndg] = (int)j;
-                                t.ndg++;
+                            // kernel matrix bit order = ascending register bits
+                            std::vector<int> order(rb);
+                            std::sort(order.begin(), order.end());
+                            std::vector<int> src(k);   // kernel bit b <- original matrix bit src[b]
+                            for (int bb = 0; bb < k; bb++)
+                                src[bb] = (int)(std::find(rb.begin(), rb.end(), order[bb]) - rb.begin());
+                            const size_t D = (size_t)1 << k;
+                            auto orig = [&](size_t x) {
+                                size_t o = 0;
+                                for (int bb = 0; bb < k; bb++)
+                                    if ((x >> bb) & 1) o |= (size_t)1 << src[bb];
+                                return o;
+                            };
+                            std::vector<cplx> Mp(D * D);
+                            for (size_t x = 0; x < D; x++)
+                                for (size_t y = 0; y < D; y++) Mp[x * D + y] = g.data[orig(x) * D + orig(y)];
+                            for (size_t j = 0; j < g.controls.size(); j++) {
+                                const int b = g.controls[j];
+                                const int want = (int)((g.cvals >> j) & 1ull);
+                                const int tp = index_in(st.tile_bits, b);
+                                const int rg = regbit(b);
+                                if (rg >= 0) {
+                                    r.rcm |= 1 << rg;
+                                    if (want) r.rcv |= 1 << rg;
+                                } else if (tp >= 0) {
+                                    r.tcm |= 1u << tp;
+                                    if (want) r.tcv |= 1u << tp;
+                                } else {
+                                    r.gcm |= 1ull << b;
+                                    if (want) r.gcv |= 1ull << b;
+                                }
                             }
+                            r.data_off = push_data(Mp);
+                        } else if (g.kind == Kind::Diagonal) {
+                            r.kind = 1;
+                            for (size_t j = 0; j < g.targets.size(); j++)
+                                route(g.targets[j], (int)j, r.r_bit, r.r_out, r.nr, r.t_pos, r.t_out, r.nt, r.g_bit,
+                                      r.g_out, r.ng);
+                            r.data_off = push_data(g.data);
+                        } else {
+                            r.kind = 2;
+                            const int ab = regbit(g.targets[0]);
+                            if (ab < 0) fail(SV_E_ARG, "internal: ancilla not in registers");
+                            r.mask = 1 << ab;
+                            r.n_c = (int)g.controls.size();
+                            r.is_signed = g.is_signed;
+                            r.dL = g.delta * std::ldexp(1.0, r.n_c - (g.is_signed ? 1 : 0));
+                            r.snap = g.snap;
+                            for (int j = 0; j < r.n_c; j++)
+                                route(g.controls[j], j, r.r_bit, r.r_out, r.nr, r.t_pos, r.t_out, r.nt, r.g_bit,
+                                      r.g_out, r.ng);
                         }
-                        t.data_off = push_data(g.data);
-                    } else {
-                        t.kind = 2;
-                        t.anc = index_in(st.tile_bits, g.targets[0]);
-                        if (t.anc < 0) fail(SV_E_ARG, "internal: tile ancilla not local");
-                        t.n_c = (int)g.controls.size();
-                        t.is_signed = g.is_signed;
-                        t.dL = g.delta * std::ldexp(1.0, t.n_c - (g.is_signed ? 1 : 0));
-                        t.snap = g.snap;
-                        for (int j = 0; j < t.n_c; j++) {
-                            const int b = g.controls[j];
-                            const int lp = index_in(st.tile_bits, b);
-                            if (lp >= 0) {
-                                t.lc_pos[t.nlc] = lp;
-                                t.lc_bit[t.nlc] = j;
-                                t.nlc++;
-                            } else {
-                                t.gc_bit[t.ngc] = b;
-                                t.gc_rbit[t.ngc] = j;
-                                t.ngc++;
-                            }
-                        }
+                        rops.push_back(r);
                     }
-                    tops.push_back(t);
+                    ph.op1 = (int)rops.size();
+                    phases.push_back(ph);
                 }
-                a.nops = (int)(tops.size() - op0);
-                tiles.push_back({p->recs.size(), op0});
+                a.nphase = (int)(phases.size() - ph0);
+                tiles.push_back({p->recs.size(), ph0});
                 break;
             }
         }
@@ -412,19 +431,27 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         cuda_check(cudaMemcpy(p->d_blob, blob.data(), sizeof(double2) * blob.size(), cudaMemcpyHostToDevice),
                    "upload blob");
     }
-    if (!tops.empty()) {
-        cuda_check(cudaMalloc(&p->d_ops, sizeof(dev::TileOp) * tops.size()), "cudaMalloc(tile ops)");
-        cuda_check(cudaMemcpy(p->d_ops, tops.data(), sizeof(dev::TileOp) * tops.size(), cudaMemcpyHostToDevice),
+    if (!rops.empty()) {
+        cuda_check(cudaMalloc(&p->d_ops, sizeof(dev::RegOp) * rops.size()), "cudaMalloc(tile ops)");
+        cuda_check(cudaMemcpy(p->d_ops, rops.data(), sizeof(dev::RegOp) * rops.size(), cudaMemcpyHostToDevice),
                    "upload tile ops");
     }
-    p->h2d_bytes += sizeof(double2) * blob.size() + sizeof(dev::TileOp) * tops.size();
+    if (!phases.empty()) {
+        cuda_check(cudaMalloc(&p->d_phases, sizeof(dev::RegPhase) * phases.size()), "cudaMalloc(phases)");
+        cuda_check(cudaMemcpy(p->d_phases, phases.data(), sizeof(dev::RegPhase) * phases.size(),
+                              cudaMemcpyHostToDevice),
+                   "upload phases");
+    }
+    p->h2d_bytes += sizeof(double2) * blob.size() + sizeof(dev::RegOp) * rops.size() +
+                    sizeof(dev::RegPhase) * phases.size();
     for (size_t r : blob_fix) {
         LaunchRec &rec = p->recs[r];
         if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
     }
     for (auto &t : tiles) {
-        p->recs[t.rec].tile.ops = p->d_ops + t.op0;
+        p->recs[t.rec].tile.phases = p->d_phases + t.op0;
+        p->recs[t.rec].tile.ops = p->d_ops;
         p->recs[t.rec].tile.blob = p->d_blob;
     }
     return p.release();
@@ -497,6 +524,7 @@ void program_destroy(sv_program *p) {
     if (p->sv) cudaStreamSynchronize(p->sv->stream);
     cudaFree(p->d_blob);
     cudaFree(p->d_ops);
+    cudaFree(p->d_phases);
     for (auto *d : p->d_tabs) cudaFree(d);
     for (auto e : p->ev) cudaEventDestroy(e);
     delete p;

@@ -51,7 +51,8 @@ struct sv_program {
     std::vector<int> phys_in;
     bool resets = false;              // starts with an initialisation step
     double2 *d_blob = nullptr;
-    hhlsv::dev::TileOp *d_ops = nullptr;
+    hhlsv::dev::RegOp *d_ops = nullptr;
+    hhlsv::dev::RegPhase *d_phases = nullptr;
     std::vector<hhlsv::LaunchRec> recs;
     uint64_t n_logical = 0;
     std::vector<double2 *> d_tabs;    // product-init tables (owned)

@@ -253,7 +253,51 @@ static void append_qft(std::vector<Gate> &out, const std::vector<int> &q, bool i
 
 // Fig. 5 circuit: U_b; H^{(x)n_c}; c-U_j (j ascending); IQFT; RECIP_RY;
 // QFT; c-U_j^dagger (j descending); H^{(x)n_c}. U_j = V diag(exp(2 pi i frac(2^j phi_s))) V^T.
-std::vector<Gate> hhl_build(const HHLPlanHost &p) {
+// Eigenbasis form of the controlled-evolution chain:
+//   prod_j c-U_j = (V (x) I) D (V^T (x) I),  D[s, m] = exp(2 pi i sum_j m_j frac(2^j phi_s)),
+// emitted as V^T on the system register, then one diagonal table per chunk of clock bits
+// (system qubits + <= 12 - n_b clock qubits), then V. conj = the inverse chain.
+static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const std::vector<int> &sys,
+                               const std::vector<int> &clk, bool inverse) {
+    const int N = p.N, nb = p.n_b, nc = p.n_c;
+    auto dense_V = [&](bool transpose) {
+        Gate v;
+        v.kind = Kind::Dense;
+        v.targets = sys;
+        v.data.assign((size_t)N * N, 0.0);
+        for (int r = 0; r < N; r++)
+            for (int c = 0; c < N; c++)
+                v.data[(size_t)r * N + c] = transpose ? p.V[c + (size_t)N * r] : p.V[r + (size_t)N * c];
+        return v;
+    };
+    const int chunk = std::max(1, 12 - nb);
+    std::vector<Gate> diags;
+    for (int j0 = 0; j0 < nc; j0 += chunk) {
+        const int cj = std::min(chunk, nc - j0);
+        Gate d;
+        d.kind = Kind::Diagonal;
+        d.targets = sys;
+        for (int j = 0; j < cj; j++) d.targets.push_back(clk[j0 + j]);
+        d.data.resize((size_t)N << cj);
+        for (size_t mc = 0; mc < ((size_t)1 << cj); mc++)
+            for (int s = 0; s < N; s++) {
+                double acc = 0.0;
+                for (int j = 0; j < cj; j++)
+                    if ((mc >> j) & 1) {
+                        double x = std::ldexp(p.phi[s], j0 + j);
+                        acc += x - std::floor(x);
+                    }
+                acc -= std::floor(acc);
+                d.data[s + (mc << nb)] = std::polar(1.0, (inverse ? -2.0 : 2.0) * M_PI * acc);
+            }
+        diags.push_back(std::move(d));
+    }
+    g.push_back(dense_V(true));            // V^T
+    for (auto &d : diags) g.push_back(std::move(d));
+    g.push_back(dense_V(false));           // V
+}
+
+std::vector<Gate> hhl_build(const HHLPlanHost &p, int qpe_mode) {
     const int N = p.N, nb = p.n_b, nc = p.n_c;
     std::vector<int> sys(nb), clk(nc);
     std::iota(sys.begin(), sys.end(), 0);
@@ -281,6 +325,28 @@ std::vector<Gate> hhl_build(const HHLPlanHost &p) {
         h.targets = {clk[j]};
         h.data = hadamard();
         g.push_back(h);
+    }
+    if (qpe_mode == 1) {
+        append_eigen_chain(g, p, sys, clk, false);
+        append_qft(g, clk, true);
+        Gate r;
+        r.kind = Kind::RecipRY;
+        r.targets = {anc};
+        r.controls = clk;
+        r.delta = p.delta;
+        r.is_signed = 1;
+        r.snap = p.snap;
+        g.push_back(r);
+        append_qft(g, clk, false);
+        append_eigen_chain(g, p, sys, clk, true);
+        for (int j = 0; j < nc; j++) {
+            Gate h;
+            h.kind = Kind::Dense;
+            h.targets = {clk[j]};
+            h.data = hadamard();
+            g.push_back(h);
+        }
+        return g;
     }
     std::vector<std::vector<cplx>> U(nc);
     for (int j = 0; j < nc; j++) {
@@ -340,6 +406,9 @@ std::vector<Gate> hhl_build(const HHLPlanHost &p) {
     return g;
 }
 
+static std::vector<cplx> embed_dense(const std::vector<cplx> &m, const std::vector<int> &q,
+                                     const std::vector<int> &u);
+
 // ------------------------------------------------------------ product fold ----
 size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors) {
     std::vector<char> touched(n, 0);
@@ -350,7 +419,23 @@ size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<Pr
         if (g.kind != Kind::Dense) break;
         bool fresh = true;
         for (int q : g.targets) fresh &= !touched[q];
-        if (!fresh) break;
+        if (!fresh) {
+            // a dense gate acting inside ONE existing factor: multiply it into that factor
+            ProductFactor *host = nullptr;
+            for (auto &f : factors) {
+                bool inside = true;
+                for (int q : g.targets) inside &= std::find(f.qubits.begin(), f.qubits.end(), q) != f.qubits.end();
+                if (inside) host = &f;
+            }
+            if (!host) break;
+            const size_t d = host->vec.size();
+            auto E = embed_dense(g.data, g.targets, host->qubits);
+            std::vector<cplx> nv(d, 0.0);
+            for (size_t r = 0; r < d; r++)
+                for (size_t c = 0; c < d; c++) nv[r] += E[r * d + c] * host->vec[c];
+            host->vec.swap(nv);
+            continue;
+        }
         ProductFactor f;
         f.qubits = g.targets;
         const size_t d = (size_t)1 << g.targets.size();

@@ -209,68 +209,151 @@ cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream
 }
 
 // ======================================================= f1 tile pass ====
-// One CTA stages the 2^T amplitudes spanned by the tile bits in shared memory (XOR
-// swizzled against bank conflicts), applies every op of the pass, and writes back:
-// ONE HBM read + write for the whole op list.
+// Tile pass v2 (see kernels.cuh): persistent CTAs, cp.async double buffering of whole
+// tiles (2^T x 16 B, XOR swizzled), and register-resident op phases: within a phase each
+// thread holds the 16 amplitudes spanned by the phase's 4 register bits and applies every op
+// of the phase without touching shared memory. ONE HBM read + write for the whole op list.
 __device__ __forceinline__ uint32_t swz(uint32_t u) {
     return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u);
 }
 
-template <int K>
-__device__ __forceinline__ void tile_dense(double2 *st, const double2 *sU, const TileOp &op, int T) {
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// deposit the bits of c into the set bits of M (constexpr; register-slot arithmetic)
+__host__ __device__ constexpr int dep_mask(int c, int M) {
+    int out = 0, bit = 0;
+    for (int i = 0; i < 4; i++)
+        if ((M >> i) & 1) {
+            if ((c >> bit) & 1) out |= 1 << i;
+            bit++;
+        }
+    return out;
+}
+__host__ __device__ constexpr int popc4(int M) { return (M & 1) + ((M >> 1) & 1) + ((M >> 2) & 1) + ((M >> 3) & 1); }
+
+// Dense / controlled op whose targets are the register bits of mask M (matrix bit order =
+// ascending register bits, re-ordered on the host). rcm/rcv: register-bit controls.
+template <int M>
+__device__ __forceinline__ void reg_dense(double2 (&v)[kRegAmps], const double2 *__restrict__ U, int rcm, int rcv) {
+    constexpr int K = popc4(M);
     constexpr int D = 1 << K;
-    int tp[K];
+    if (K <= 2) {
+        double2 u[D * D];
 #pragma unroll
-    for (int i = 0; i < K; i++) tp[i] = op.tpos[i];
-    const int nins = op.nins;
-    const uint32_t groups = 1u << (T - nins);
-    for (uint32_t g = threadIdx.x; g < groups; g += blockDim.x) {
-        uint32_t b = g;
-        for (int i = 0; i < nins; i++) {
-            const int p = op.ins[i];
-            b = ((b >> p) << (p + 1)) | (b & ((1u << p) - 1u));
+        for (int i = 0; i < D * D; i++) u[i] = __ldg(&U[i]);
+#pragma unroll
+        for (int g = 0; g < kRegAmps; g++) {
+            if (g & M) continue;
+            if ((g & rcm) != rcv) continue;
+            double2 in[D];
+#pragma unroll
+            for (int c = 0; c < D; c++) in[c] = v[g | dep_mask(c, M)];
+#pragma unroll
+            for (int r = 0; r < D; r++) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int c = 0; c < D; c++) cfma(acc, u[r * D + c], in[c]);
+                v[g | dep_mask(r, M)] = acc;
+            }
         }
-        b |= op.lcset;
-        double2 v[D];
+    } else {
 #pragma unroll
-        for (int c = 0; c < D; c++) {
-            uint32_t o = 0;
+        for (int g = 0; g < kRegAmps; g++) {
+            if (g & M) continue;
+            if ((g & rcm) != rcv) continue;
+            double2 in[D];
 #pragma unroll
-            for (int i = 0; i < K; i++)
-                if ((c >> i) & 1) o |= 1u << tp[i];
-            v[c] = st[swz(b | o)];
-        }
-#pragma unroll(K >= 3 ? 1 : D)
-        for (int r = 0; r < D; r++) {
-            double2 acc = make_double2(0.0, 0.0);
+            for (int c = 0; c < D; c++) in[c] = v[g | dep_mask(c, M)];
 #pragma unroll
-            for (int c = 0; c < D; c++) cfma(acc, sU[r * D + c], v[c]);
-            uint32_t o = 0;
+            for (int r = 0; r < D; r++) {
+                double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int i = 0; i < K; i++)
-                if ((r >> i) & 1) o |= 1u << tp[i];
-            st[swz(b | o)] = acc;
+                for (int c = 0; c < D; c++) cfma(acc, __ldg(&U[r * D + c]), in[c]);
+                v[g | dep_mask(r, M)] = acc;
+            }
         }
     }
 }
 
-template <int MAXK>
-__global__ void __launch_bounds__(kThreads, MAXK >= 5 ? 1 : 2) k_tile(const TileArgs a) {
+template <int A>   // A = register bit of the ancilla
+__device__ __forceinline__ void reg_recip(double2 (&v)[kRegAmps], const RegOp &op, uint64_t mbase) {
+#pragma unroll
+    for (int j = 0; j < kRegAmps; j++) {
+        if ((j >> A) & 1) continue;
+        uint64_t m = mbase;
+        for (int i = 0; i < op.nr; i++) m |= (uint64_t)((j >> op.r_bit[i]) & 1) << op.r_out[i];
+        const double sv = recip_s(m, op.n_c, op.dL, op.is_signed, op.snap);
+        const double cv = sqrt(fma(-sv, sv, 1.0));
+        const double2 x0 = v[j], x1 = v[j | (1 << A)];
+        v[j] = make_double2(cv * x0.x - sv * x1.x, cv * x0.y - sv * x1.y);
+        v[j | (1 << A)] = make_double2(sv * x0.x + cv * x1.x, sv * x0.y + cv * x1.y);
+    }
+}
+
+__device__ __forceinline__ void apply_phase_ops(double2 (&v)[kRegAmps], const TileArgs &a, const RegPhase &ph,
+                                                uint32_t tb, uint64_t gbase) {
+    for (int oi = ph.op0; oi < ph.op1; oi++) {
+        const RegOp &op = a.ops[oi];
+        if ((gbase & op.gcm) != op.gcv) continue;                 // CTA-uniform
+        if (op.kind == 0) {
+            if ((tb & op.tcm) != op.tcv) continue;                // thread-uniform
+            const double2 *U = a.blob + op.data_off;
+            const int rcm = op.rcm, rcv = op.rcv;
+            switch (op.mask) {
+#define DCASE(M) case M: reg_dense<M>(v, U, rcm, rcv); break;
+                DCASE(1) DCASE(2) DCASE(3) DCASE(4) DCASE(5) DCASE(6) DCASE(7) DCASE(8)
+                DCASE(9) DCASE(10) DCASE(11) DCASE(12) DCASE(13) DCASE(14) DCASE(15)
+#undef DCASE
+                default: break;
+            }
+        } else {
+            uint64_t base = 0;
+            for (int i = 0; i < op.ng; i++) base |= ((gbase >> op.g_bit[i]) & 1ull) << op.g_out[i];
+            for (int i = 0; i < op.nt; i++) base |= (uint64_t)((tb >> op.t_pos[i]) & 1u) << op.t_out[i];
+            if (op.kind == 1) {
+                const double2 *tab = a.blob + op.data_off;
+#pragma unroll
+                for (int j = 0; j < kRegAmps; j++) {
+                    uint32_t idx = (uint32_t)base;
+                    for (int i = 0; i < op.nr; i++) idx |= (uint32_t)((j >> op.r_bit[i]) & 1) << op.r_out[i];
+                    v[j] = cmul(__ldg(&tab[idx]), v[j]);
+                }
+            } else {
+                switch (op.mask) {
+                    case 1: reg_recip<0>(v, op, base); break;
+                    case 2: reg_recip<1>(v, op, base); break;
+                    case 4: reg_recip<2>(v, op, base); break;
+                    case 8: reg_recip<3>(v, op, base); break;
+                    default: break;
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int T = a.T;
     const uint32_t NT = 1u << T;
-    double2 *st = reinterpret_cast<double2 *>(smem_raw);
-    double2 *sU = st + NT;
+    const int nthr = (int)blockDim.x;            // = NT / 16
+    double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);
+    double2 *buf1 = buf0 + NT;
     const int SA = (T + 1) / 2, SB = T - SA;
-    uint64_t *depA = reinterpret_cast<uint64_t *>(sU + (a.maxk > 0 ? (1 << (2 * a.maxk)) : 0));
+    uint64_t *depA = reinterpret_cast<uint64_t *>(buf1 + NT);
     uint64_t *depB = depA + (1 << SA);
-    for (int u = threadIdx.x; u < (1 << SA); u += blockDim.x) {
+    for (int u = threadIdx.x; u < (1 << SA); u += nthr) {
         uint64_t d = 0;
         for (int i = 0; i < SA; i++)
             if ((u >> i) & 1) d |= 1ull << a.tbits[i];
         depA[u] = d;
     }
-    for (int u = threadIdx.x; u < (1 << SB); u += blockDim.x) {
+    for (int u = threadIdx.x; u < (1 << SB); u += nthr) {
         uint64_t d = 0;
         for (int i = 0; i < SB; i++)
             if ((u >> i) & 1) d |= 1ull << a.tbits[SA + i];
@@ -279,114 +362,77 @@ __global__ void __launch_bounds__(kThreads, MAXK >= 5 ? 1 : 2) k_tile(const Tile
     const uint32_t maskA = (1u << SA) - 1u;
     __syncthreads();
 
-    for (uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-        uint64_t base = tile;
-        for (int i = 0; i < T; i++) base = insz(base, a.tbits[i]);
-        const uint64_t gbase = a.rank_base | base;
-        // ---- load (8 independent 16-byte loads per thread in flight per batch)
-        for (uint32_t j = 0; j < NT; j += blockDim.x * 8) {
-            double2 r[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const uint32_t u = j + q * blockDim.x + threadIdx.x;
-                if (u < NT) r[q] = a.psi[base | depA[u & maskA] | depB[u >> SA]];
-            }
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const uint32_t u = j + q * blockDim.x + threadIdx.x;
-                if (u < NT) st[swz(u)] = r[q];
-            }
-        }
+    auto tile_base = [&](uint64_t tile) {
+        uint64_t b = tile;
+        for (int i = 0; i < T; i++) b = insz(b, a.tbits[i]);
+        return b;
+    };
+    auto prefetch = [&](uint64_t tile, double2 *dst) {
+        const uint64_t base = tile_base(tile);
+        for (uint32_t u = threadIdx.x; u < NT; u += nthr)
+            cp_async16(&dst[swz(u)], &a.psi[base | depA[u & maskA] | depB[u >> SA]]);
+    };
+
+    uint64_t tile = blockIdx.x;
+    if (tile < a.n_tiles) prefetch(tile, buf0);
+    cp_async_commit();
+    for (int it = 0; tile < a.n_tiles; tile += gridDim.x, it++) {
+        double2 *cur = (it & 1) ? buf1 : buf0;
+        double2 *nxt = (it & 1) ? buf0 : buf1;
+        const uint64_t next = tile + gridDim.x;
+        if (next < a.n_tiles) prefetch(next, nxt);
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
-        // ---- ops
-        for (int oi = 0; oi < a.nops; oi++) {
-            const TileOp &op = a.ops[oi];
-            if ((gbase & op.gcmask) != op.gcval) continue;        // CTA-uniform
-            if (op.kind == 0) {
-                const int D = 1 << op.k;
-                const double2 *U = a.blob + op.data_off;
-                for (int i = threadIdx.x; i < D * D; i += blockDim.x) sU[i] = U[i];
-                __syncthreads();
-                switch (op.k) {
-                    case 1: tile_dense<1>(st, sU, op, T); break;
-                    case 2: if (MAXK >= 2) tile_dense<(MAXK >= 2 ? 2 : 1)>(st, sU, op, T); break;
-                    case 3: if (MAXK >= 3) tile_dense<(MAXK >= 3 ? 3 : 1)>(st, sU, op, T); break;
-                    case 4: if (MAXK >= 4) tile_dense<(MAXK >= 4 ? 4 : 1)>(st, sU, op, T); break;
-                    case 5: if (MAXK >= 5) tile_dense<(MAXK >= 5 ? 5 : 1)>(st, sU, op, T); break;
-                }
-            } else if (op.kind == 1) {
-                uint32_t gidx = 0;
-                for (int j = 0; j < op.ndg; j++) gidx |= (uint32_t)((gbase >> op.dg_bit[j]) & 1ull) << op.dg_tbit[j];
-                const double2 *tab = a.blob + op.data_off;
-                for (uint32_t u = threadIdx.x; u < NT; u += blockDim.x) {
-                    uint32_t idx = gidx;
-                    for (int j = 0; j < op.ndl; j++) idx |= ((u >> op.dl_pos[j]) & 1u) << op.dl_tbit[j];
-                    const uint32_t su = swz(u);
-                    st[su] = cmul(__ldg(&tab[idx]), st[su]);
-                }
-            } else {
-                uint64_t mg = 0;
-                for (int j = 0; j < op.ngc; j++) mg |= ((gbase >> op.gc_bit[j]) & 1ull) << op.gc_rbit[j];
-                const int anc = op.anc;
-                for (uint32_t p = threadIdx.x; p < (NT >> 1); p += blockDim.x) {
-                    const uint32_t u0 = ((p >> anc) << (anc + 1)) | (p & ((1u << anc) - 1u));
-                    const uint32_t u1 = u0 | (1u << anc);
-                    uint64_t m = mg;
-                    for (int j = 0; j < op.nlc; j++) m |= (uint64_t)((u0 >> op.lc_pos[j]) & 1u) << op.lc_bit[j];
-                    const double sv = recip_s(m, op.n_c, op.dL, op.is_signed, op.snap);
-                    const double cv = sqrt(fma(-sv, sv, 1.0));
-                    const uint32_t s0 = swz(u0), s1 = swz(u1);
-                    const double2 x0 = st[s0], x1 = st[s1];
-                    st[s0] = make_double2(cv * x0.x - sv * x1.x, cv * x0.y - sv * x1.y);
-                    st[s1] = make_double2(sv * x0.x + cv * x1.x, sv * x0.y + cv * x1.y);
-                }
+        const uint64_t base = tile_base(tile);
+        const uint64_t gbase = a.rank_base | base;
+        for (int p = 0; p < a.nphase; p++) {
+            const RegPhase &ph = a.phases[p];
+            uint32_t tb = 0;                          // tile-local index bits of this thread
+            for (int i = 0; i < T - kRegBits; i++) tb |= (uint32_t)((threadIdx.x >> i) & 1) << ph.tpos[i];
+            uint32_t rd[kRegAmps];
+#pragma unroll
+            for (int j = 0; j < kRegAmps; j++) {
+                uint32_t d = 0;
+#pragma unroll
+                for (int i = 0; i < kRegBits; i++)
+                    if ((j >> i) & 1) d |= 1u << ph.R[i];
+                rd[j] = d;
             }
+            double2 v[kRegAmps];
+#pragma unroll
+            for (int j = 0; j < kRegAmps; j++) v[j] = cur[swz(tb | rd[j])];
+            apply_phase_ops(v, a, ph, tb, gbase);
+#pragma unroll
+            for (int j = 0; j < kRegAmps; j++) cur[swz(tb | rd[j])] = v[j];
             __syncthreads();
         }
-        // ---- store
-        for (uint32_t j = 0; j < NT; j += blockDim.x * 8) {
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const uint32_t u = j + q * blockDim.x + threadIdx.x;
-                if (u < NT) a.psi[base | depA[u & maskA] | depB[u >> SA]] = st[swz(u)];
-            }
-        }
+        // write back (coalesced: consecutive threads -> consecutive low bits)
+#pragma unroll 4
+        for (uint32_t u = threadIdx.x; u < NT; u += nthr) a.psi[base | depA[u & maskA] | depB[u >> SA]] = cur[swz(u)];
         __syncthreads();
     }
+    cp_async_wait<0>();
 }
 
-size_t tile_smem_bytes(int T, int maxk) {
+size_t tile_smem_bytes(int T) {
     const int SA = (T + 1) / 2, SB = T - SA;
-    return sizeof(double2) * ((size_t)1 << T) + (maxk > 0 ? sizeof(double2) * ((size_t)1 << (2 * maxk)) : 0) +
-           sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
-}
-
-template <int MAXK>
-static cudaError_t launch_tile_k(const TileArgs &a, cudaStream_t s) {
-    const size_t smem = tile_smem_bytes(a.T, a.maxk);
-    static int per_sm_cache[16] = {0};
-    cudaError_t e = cudaFuncSetAttribute(k_tile<MAXK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<MAXK>, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    (void)per_sm_cache;
-    if (per_sm < 1) per_sm = 1;
-    uint64_t grid = (uint64_t)kSMs * per_sm;
-    if (grid > a.n_tiles) grid = a.n_tiles;
-    k_tile<MAXK><<<(unsigned)grid, kThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    return 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
 }
 
 cudaError_t launch_tile(const TileArgs &a, cudaStream_t s) {
-    switch (a.maxk) {
-        case 0:
-        case 1:
-        case 2: return launch_tile_k<2>(a, s);
-        case 3: return launch_tile_k<3>(a, s);
-        case 4: return launch_tile_k<4>(a, s);
-        default: return launch_tile_k<5>(a, s);
-    }
+    const size_t smem = tile_smem_bytes(a.T);
+    const int threads = 1 << (a.T - kRegBits);
+    cudaError_t e = cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)kSMs * per_sm;
+    if (grid > a.n_tiles) grid = a.n_tiles;
+    k_tile<<<(unsigned)grid, threads, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ======================================================= a8 reductions ====

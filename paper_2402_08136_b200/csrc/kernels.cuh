@@ -63,29 +63,32 @@ struct ProductArgs {             // a3: product-state initialisation (prep + H l
     const double2 *tab[4];       // chunk tables (2^cn entries)
 };
 
-// Tile pass op (TOP_DENSE covers dense and controlled).
-struct TileOp {
+// Tile pass v2: a CTA holds 2^T amplitudes of one tile in shared memory
+// (cp.async double-buffered, persistent CTAs); the pass's ops are grouped in register phases:
+// in phase p every thread holds the 16 amplitudes spanned by the 4 tile positions R[p] (the
+// "register bits") at its own thread-bit coordinates, and applies all the phase's ops in
+// registers. Phases exchange data through shared memory.
+constexpr int kRegBits = 4;
+constexpr int kRegAmps = 1 << kRegBits;
+
+struct RegOp {
     int kind;                    // 0 dense/controlled, 1 diagonal, 2 recip
-    int k;                       // dense: targets
-    int tpos[5];                 // dense: tile-local target positions
-    int nins;
-    int ins[16];                 // dense: sorted tile-local positions (targets + local controls)
-    uint32_t lcset;              // dense: tile-local control bits required to be 1
-    uint64_t gcmask, gcval;      // controls on non-tile bits (global index): op skipped unless match
-    // diagonal
-    int ndl;
-    int dl_pos[kMaxDiag], dl_tbit[kMaxDiag];
-    int ndg;
-    int dg_bit[kMaxDiag], dg_tbit[kMaxDiag];   // global-index bit -> table bit
-    // recip
-    int anc;                     // tile-local position of the ancilla
-    int nlc;
-    int lc_pos[32], lc_bit[32];
-    int ngc;
-    int gc_bit[kMaxClock], gc_rbit[kMaxClock]; // global-index bit -> register bit
+    int mask;                    // dense: register-bit mask of the targets; recip: 1 << (anc register bit)
+    int rcm, rcv;                // dense: register-bit controls (mask / required values)
+    uint32_t tcm, tcv;           // dense: controls on thread-held tile positions (tile-local masks)
+    uint64_t gcm, gcv;           // controls outside the tile (global index bits): op skipped unless match
+    int nr, r_bit[4], r_out[4];  // diag/recip: register bits -> output bit (table index / clock value)
+    int nt, t_pos[16], t_out[16];// diag/recip: tile positions held by threads -> output bit
+    int ng, g_bit[62], g_out[62];// diag/recip: global-index bits outside the tile -> output bit
     int n_c, is_signed;
     double dL, snap;
-    uint64_t data_off;           // matrix/table offset in the program blob (double2 units)
+    uint64_t data_off;           // matrix (register-bit order) / table offset in the blob (double2 units)
+};
+
+struct RegPhase {
+    int R[kRegBits];             // tile positions held in registers (ascending)
+    int tpos[16];                // the other T - 4 tile positions (ascending) = thread bits
+    int op0, op1;                // ops [op0, op1)
 };
 
 struct TileArgs {
@@ -93,11 +96,11 @@ struct TileArgs {
     uint64_t n_tiles;            // 2^(nloc - T)
     int T;
     int tbits[16];               // sorted physical local bits of the tile
-    int nops;
-    const TileOp *ops;           // device array
+    int nphase;
+    const RegPhase *phases;      // device
+    const RegOp *ops;            // device
     const double2 *blob;         // program data blob
     uint64_t rank_base;
-    int maxk;                    // largest dense k in the op list (sizes the matrix buffer)
 };
 
 // ---- launchers (stream-ordered, no sync) ----
@@ -107,7 +110,7 @@ cudaError_t launch_recip(const RecipArgs &a, cudaStream_t s);
 cudaError_t launch_product(const ProductArgs &a, cudaStream_t s);
 cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream_t s);
 cudaError_t launch_tile(const TileArgs &a, cudaStream_t s);
-size_t tile_smem_bytes(int T, int maxk);
+size_t tile_smem_bytes(int T);
 
 // Deterministic reductions. partial has >= kRedBlocks doubles; result written to out (device).
 constexpr int kRedBlocks = 1184;   // 148 SMs x 8

@@ -64,7 +64,7 @@ struct HHLPlanHost {
 };
 
 HHLPlanHost hhl_plan(const double *A, const double *b, int N, int clock_qubits, double snap);
-std::vector<Gate> hhl_build(const HHLPlanHost &p);
+std::vector<Gate> hhl_build(const HHLPlanHost &p, int qpe_mode = 0);
 void jacobi_eigh(int N, std::vector<double> A, std::vector<double> &lam, std::vector<double> &V);
 
 struct FuseOptions {
@@ -113,6 +113,10 @@ struct Step {
     // ---- Tile: sorted physical bits held in shared memory, plus the op list
     std::vector<int> tile_bits;
     std::vector<Gate> tile_ops;    // physical-bit gates (targets/controls are physical bits)
+    // register phases of a Tile step: phase p holds ops [phase_start[p], phase_start[p+1]) and
+    // keeps the physical bits phase_R[p] (kRegBits of them) in registers
+    std::vector<size_t> phase_start;
+    std::vector<std::vector<int>> phase_R;
     // ---- Exchange: swap physical global bit gbit with local bit lbit
     int gbit = 0, lbit = 0;
     // ---- InitProduct: factors on physical bits
@@ -124,6 +128,8 @@ struct Program;   // defined in engine.cu (device blob, launch records)
 
 struct CompileOptions {
     int tile_qubits = 12;      // <= 0 : no tiles (one streaming pass per op)
+    int wmin = 5;              // tiles always hold the lowest wmin physical bits (512 B segments)
+    int reg_bits = 4;          // qubits held in registers per thread in a tile phase (16 amplitudes)
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.

@@ -119,7 +119,8 @@ def test_basis_gate_stream_paper_fusion():
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3p", "C3"])
 @pytest.mark.parametrize("opts", [dict(), dict(tile_qubits=-1), dict(fusion_kmax=-1, tile_qubits=-1),
-                                  dict(fusion_kmax=2, tile_qubits=8), dict(init_fold=-1)])
+                                  dict(fusion_kmax=2, tile_qubits=8), dict(init_fold=-1), dict(qpe_mode=1),
+                                  dict(qpe_mode=1, tile_qubits=-1), dict(qpe_mode=1, fusion_kmax=1, tile_qubits=11)])
 def test_hhl_configs_full_state(name, opts):
     """C1-C3 (configs[0..2]) + C3p (Table 1 14-bus): every amplitude within 1e-10 of the oracle,
     identical post-selection index set, |dP| <= 1e-12, x within 1e-10."""
@@ -221,23 +222,48 @@ def _tol_frontend(p):
     return max(1e-10, 2 * np.pi * (1 << p.n_c) * 8 * np.finfo(float).eps * float(np.max(np.abs(p.phi))))
 
 
-@pytest.mark.slow
-def test_s30_full_size():
-    """configs[3] (30 qubits, 16 GiB state) in the launch configuration bench.py times: sampled
-    amplitudes vs the closed form, the whole post-selected slice and P_succ."""
+@pytest.fixture(scope="module")
+def s30_reference():
+    """Closed-form (oracle) values for S30: P_succ, x~ and sampled amplitudes (~1-2 min of CPU)."""
     A, b, nc = configs.get("S30")
     p = ohhl.plan(A, b, nc)
+    xt, P = cf.postselected(p)
+    g = synthetic.rng(30)
+    idx = np.unique(np.concatenate([g.integers(0, 1 << p.n, 12), [0, 5, (1 << p.n) - 1, 1 << (p.n - 1)]]))
+    return A, b, nc, p, xt, P, idx, cf.sampled_amplitudes(p, idx)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("opts", [dict(), dict(qpe_mode=1)])
+def test_s30_full_size(s30_reference, opts):
+    """configs[3] (30 qubits, 16 GiB state) in the launch configuration bench.py times (product
+    front end): sampled amplitudes vs the closed form, post-selected x and P_succ within the derived
+    front-end tolerance."""
+    A, b, nc, p, xt, P, idx, ref = s30_reference
     st = pkg.State(p.n)
-    prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc)
+    prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, **opts)
     prog.run()
     x, ps = prog.readout()
-    xt, P = cf.postselected(p)
     tol = _tol_frontend(p)
     assert abs(ps - P) < max(1e-12, tol)
     assert np.abs(x - p.b_norm * xt[: p.n_orig] / p.lam_min).max() < 10 * tol
-    g = synthetic.rng(30)
-    idx = np.unique(np.concatenate([g.integers(0, 1 << p.n, 24), [0, (1 << p.n) - 1, 1 << (p.n - 1)]]))
     got = np.array([st.read(int(i), 1)[0] for i in idx])
-    ref = cf.sampled_amplitudes(p, idx)
     assert np.abs(got - ref).max() < tol
     assert abs(st.norm2() - 1.0) < 1e-11
+
+
+@pytest.mark.slow
+def test_s30_engine_parity_oracle_gates(s30_reference):
+    """The engine at full size held to 1e-10: the ORACLE's own S30 gate list (oracle phases) run
+    through the product fusion + tile scheduler + kernels vs the oracle closed form."""
+    A, b, nc, p, xt, P, idx, ref = s30_reference
+    gates = ohhl.build(p)
+    st = pkg.State(p.n)
+    prog = pkg.Program.create(st, gates, fusion_kmax=2, tile_qubits=12)
+    prog.run()
+    got = np.array([st.read(int(i), 1)[0] for i in idx])
+    assert np.abs(got - ref).max() < 1e-10
+    base = 1 << (p.n - 1)
+    sl = st.read(base, 1 << p.n_b)
+    assert np.abs(sl - xt).max() < 1e-10
+    assert abs(float(np.sum(np.abs(sl) ** 2)) - P) < 1e-12
