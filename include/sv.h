@@ -134,6 +134,8 @@ typedef struct {
     int fusion_kmax;
     int diag_kmax;
     int tile_qubits;
+    int tile_jit;       /* 0: auto (NVRTC-specialised tile passes when the local state has >= 2^18 amplitudes),
+                           1: always, -1: never (generic interpreting tile kernel) */
 } sv_fuse_options;
 
 typedef struct {
@@ -203,6 +205,7 @@ typedef struct {
     int tile_qubits;    /* 0 -> library default ; -1 -> one pass per fused op */
     double recip_snap;  /* reciprocal snapping tolerance (qlsarepo: 1e-5); < 0 -> default 1e-5 */
     int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; -1: don't */
+    int tile_jit;       /* as sv_fuse_options.tile_jit */
     int qpe_mode;       /* 0: textbook circuit (c-U^(2^j) blocks, Fig. 5); 1: eigenbasis rewrite:
                            c-U_j = V diag(e^{2 pi i frac(2^j phi_s)}) V^T, so the controlled chain becomes
                            V^T, <= 12-qubit diagonal phase tables over (system, clock chunk), V — the same

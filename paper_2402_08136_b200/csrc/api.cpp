@@ -53,6 +53,7 @@ FuseOptions fuse_opts(const sv_fuse_options *o) {
 CompileOptions compile_opts(const sv_fuse_options *o) {
     CompileOptions c;
     if (o && o->tile_qubits != 0) c.tile_qubits = o->tile_qubits;
+    if (o) c.jit = o->tile_jit;
     return c;
 }
 
@@ -245,8 +246,30 @@ sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
         }
+        std::string jitlog;
+        if (opt && opt->tile_jit > 0) {      // host-only: generate + NVRTC-compile every tile pass
+            std::string why;
+            if (!jit_available(&why)) fail(SV_E_CUDA, "tile JIT unavailable: " + why);
+            std::vector<double2> blob;
+            std::vector<dev::RegOp> rops;
+            std::vector<dev::RegPhase> phases;
+            for (const Step &st : s.steps) {
+                if (st.kind != StepKind::Tile) continue;
+                dev::TileArgs a{};
+                a.T = (int)st.tile_bits.size();
+                for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
+                size_t ph0 = 0, opb = 0;
+                lower_tile_step(st, a, blob, rops, phases, ph0, opb);
+                std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
+                std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
+                std::string err;
+                auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops), err);
+                if (cubin.empty()) fail(SV_E_CUDA, err);
+                jitlog += "JIT_PASS cubin_bytes=" + std::to_string(cubin.size()) + "\n";
+            }
+        }
         if (buf && buf_len) {
-            std::string t = dump_schedule(s);
+            std::string t = dump_schedule(s) + jitlog;
             std::string perm = "FINAL_MAP";
             for (int q = 0; q < n_qubits; q++) perm += " " + std::to_string(s.phys_out[q]);
             t += perm + "\n";
@@ -308,6 +331,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     std::vector<Gate> fused = fuse(rest, fo);
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
+    if (opt) co.jit = opt->tile_jit;
     sv_program *prog = program_create(sv, fused, &factors, co, gates.size());
     if (rep) {
         std::memset(rep, 0, sizeof(*rep));

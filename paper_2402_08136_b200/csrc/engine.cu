@@ -197,6 +197,140 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
     }
 }
 
+// Host-side lowering of one Tile step into register phases + op descriptors (also used by the
+// host-only schedule check). Appends to blob/rops/phases; returns the first phase/op index.
+void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blob, std::vector<dev::RegOp> &rops,
+                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out) {
+    auto push_data = [&](const std::vector<cplx> &d) {
+        size_t off = blob.size();
+        for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
+        return off;
+    };
+    const size_t ph0 = phases.size();
+    const size_t opbase = rops.size();
+    for (size_t pi = 0; pi + 1 < st.phase_start.size(); pi++) {
+        dev::RegPhase ph{};
+        const std::vector<int> &Rp = st.phase_R[pi];   // physical bits, ascending
+        std::vector<int> Rt;                            // tile positions
+        for (int b : Rp) Rt.push_back(index_in(st.tile_bits, b));
+        for (int i = 0; i < dev::kRegBits; i++) ph.R[i] = Rt[i];
+        int nt = 0;
+        for (int tp = 0; tp < a.T; tp++)
+            if (std::find(Rt.begin(), Rt.end(), tp) == Rt.end()) ph.tpos[nt++] = tp;
+        ph.op0 = (int)(rops.size() - opbase);
+        for (size_t oi = st.phase_start[pi]; oi < st.phase_start[pi + 1]; oi++) {
+            const Gate &g = st.tile_ops[oi];
+            dev::RegOp r{};
+            auto regbit = [&](int phys_bit) { return index_in(Rp, phys_bit); };
+            // route the bits of an index (table index / clock value): register slots ->
+            // ridx[], thread-held tile positions and out-of-tile bits -> bit runs
+            std::vector<std::pair<int, int>> tpairs, gpairs;
+            auto route = [&](int b, int out) {
+                const int tp = index_in(st.tile_bits, b);
+                const int rg = regbit(b);
+                if (rg >= 0) {
+                    for (int j = 0; j < dev::kRegAmps; j++)
+                        if ((j >> rg) & 1) r.ridx[j] |= 1u << out;
+                } else if (tp >= 0) {
+                    tpairs.push_back({tp, out});
+                } else {
+                    gpairs.push_back({b, out});
+                }
+            };
+            auto to_runs = [&](std::vector<std::pair<int, int>> v, uint8_t *src, uint8_t *len,
+                               uint8_t *dst, int cap) {
+                std::sort(v.begin(), v.end());
+                int n = 0;
+                for (size_t i = 0; i < v.size(); i++) {
+                    if (n > 0 && v[i].first == src[n - 1] + len[n - 1] &&
+                        v[i].second == dst[n - 1] + len[n - 1]) {
+                        len[n - 1]++;
+                        continue;
+                    }
+                    if (n == cap) fail(SV_E_ARG, "internal: too many bit runs in a tile op");
+                    src[n] = (uint8_t)v[i].first;
+                    dst[n] = (uint8_t)v[i].second;
+                    len[n] = 1;
+                    n++;
+                }
+                return n;
+            };
+            if (g.kind == Kind::Dense || g.kind == Kind::Controlled) {
+                r.kind = 0;
+                const int k = (int)g.targets.size();
+                std::vector<int> rb(k);
+                for (int i = 0; i < k; i++) {
+                    rb[i] = regbit(g.targets[i]);
+                    if (rb[i] < 0) fail(SV_E_ARG, "internal: phase target not in registers");
+                    r.mask |= 1 << rb[i];
+                }
+                // kernel matrix bit order = ascending register bits
+                std::vector<int> order(rb);
+                std::sort(order.begin(), order.end());
+                std::vector<int> src(k);   // kernel bit b <- original matrix bit src[b]
+                for (int bb = 0; bb < k; bb++)
+                    src[bb] = (int)(std::find(rb.begin(), rb.end(), order[bb]) - rb.begin());
+                const size_t D = (size_t)1 << k;
+                auto orig = [&](size_t x) {
+                    size_t o = 0;
+                    for (int bb = 0; bb < k; bb++)
+                        if ((x >> bb) & 1) o |= (size_t)1 << src[bb];
+                    return o;
+                };
+                std::vector<cplx> Mp(D * D);
+                for (size_t x = 0; x < D; x++)
+                    for (size_t y = 0; y < D; y++) Mp[x * D + y] = g.data[orig(x) * D + orig(y)];
+                for (size_t j = 0; j < g.controls.size(); j++) {
+                    const int b = g.controls[j];
+                    const int want = (int)((g.cvals >> j) & 1ull);
+                    const int tp = index_in(st.tile_bits, b);
+                    const int rg = regbit(b);
+                    if (rg >= 0) {
+                        r.rcm |= 1 << rg;
+                        if (want) r.rcv |= 1 << rg;
+                    } else if (tp >= 0) {
+                        r.tcm |= 1u << tp;
+                        if (want) r.tcv |= 1u << tp;
+                    } else {
+                        r.gcm |= 1ull << b;
+                        if (want) r.gcv |= 1ull << b;
+                    }
+                }
+                bool real = true;
+                for (auto &z : Mp) real &= z.imag() == 0.0;
+                r.is_signed = real ? 1 : 0;          // dense: real-matrix flag
+                r.data_off = push_data(Mp);
+            } else if (g.kind == Kind::Diagonal) {
+                r.kind = 1;
+                for (size_t j = 0; j < g.targets.size(); j++) route(g.targets[j], (int)j);
+                r.data_off = push_data(g.data);
+            } else {
+                r.kind = 2;
+                const int ab = regbit(g.targets[0]);
+                if (ab < 0) fail(SV_E_ARG, "internal: ancilla not in registers");
+                r.mask = 1 << ab;
+                r.n_c = (int)g.controls.size();
+                if (r.n_c > 62) fail(SV_E_ARG, "clock register too wide");
+                r.is_signed = g.is_signed;
+                r.dL = g.delta * std::ldexp(1.0, r.n_c - (g.is_signed ? 1 : 0));
+                r.snap = g.snap;
+                for (int j = 0; j < r.n_c; j++) route(g.controls[j], j);
+                r.data_off = push_data({cplx(r.dL, r.snap)});
+                for (auto &pr : gpairs)
+                    if (pr.second >= 63) fail(SV_E_ARG, "clock register too wide for a tile");
+            }
+            r.ntr = to_runs(tpairs, r.t_src, r.t_len, r.t_dst, 12);
+            r.ngr = to_runs(gpairs, r.g_src, r.g_len, r.g_dst, 48);
+            rops.push_back(r);
+        }
+        ph.op1 = (int)(rops.size() - opbase);
+        phases.push_back(ph);
+    }
+    a.nops = (int)(rops.size() - opbase);
+    ph0_out = ph0;
+    opbase_out = opbase;
+}
+
 sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,
                            const CompileOptions &co, uint64_t n_logical) {
     std::unique_ptr<sv_program> p(new sv_program());
@@ -210,7 +344,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         p->phys_in = sv->phys;
     }
     CompileOptions c2 = co;
-    if (c2.tile_qubits > 14) c2.tile_qubits = 14;
+    if (c2.tile_qubits > 12) c2.tile_qubits = 12;
+    const bool use_jit = co.jit > 0 || (co.jit == 0 && sv->nloc >= 18);
     p->sched = compile(ops, init, sv->n, sv->nloc, p->phys_in, c2);
     const int nloc = sv->nloc;
     const uint64_t rank_base = (uint64_t)sv->rank << nloc;
@@ -224,7 +359,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
         return off;
     };
-    struct Pending { size_t rec; size_t op0; };
+    struct Pending { size_t rec; size_t op0; size_t opbase; };
     std::vector<Pending> tiles;
     std::vector<size_t> blob_fix;     // recs whose pointer must be rebased (streaming data)
 
@@ -329,97 +464,19 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
                 a.n_tiles = 1ull << (nloc - a.T);
                 a.rank_base = rank_base;
-                const size_t ph0 = phases.size();
-                for (size_t pi = 0; pi + 1 < st.phase_start.size(); pi++) {
-                    dev::RegPhase ph{};
-                    const std::vector<int> &Rp = st.phase_R[pi];   // physical bits, ascending
-                    std::vector<int> Rt;                            // tile positions
-                    for (int b : Rp) Rt.push_back(index_in(st.tile_bits, b));
-                    for (int i = 0; i < dev::kRegBits; i++) ph.R[i] = Rt[i];
-                    int nt = 0;
-                    for (int tp = 0; tp < a.T; tp++)
-                        if (std::find(Rt.begin(), Rt.end(), tp) == Rt.end()) ph.tpos[nt++] = tp;
-                    ph.op0 = (int)rops.size();
-                    for (size_t oi = st.phase_start[pi]; oi < st.phase_start[pi + 1]; oi++) {
-                        const Gate &g = st.tile_ops[oi];
-                        dev::RegOp r{};
-                        auto regbit = [&](int phys_bit) { return index_in(Rp, phys_bit); };
-                        auto route = [&](int b, int out, int *rb, int *ro, int &nr, int *tpos, int *to, int &ntt,
-                                         int *gb, int *go, int &ng) {
-                            const int tp = index_in(st.tile_bits, b);
-                            const int rg = regbit(b);
-                            if (rg >= 0) { rb[nr] = rg; ro[nr] = out; nr++; }
-                            else if (tp >= 0) { tpos[ntt] = tp; to[ntt] = out; ntt++; }
-                            else { gb[ng] = b; go[ng] = out; ng++; }
-                        };
-                        if (g.kind == Kind::Dense || g.kind == Kind::Controlled) {
-                            r.kind = 0;
-                            const int k = (int)g.targets.size();
-                            std::vector<int> rb(k);
-                            for (int i = 0; i < k; i++) {
-                                rb[i] = regbit(g.targets[i]);
-                                if (rb[i] < 0) fail(SV_E_ARG, "internal: phase target not in registers");
-                                r.mask |= 1 << rb[i];
-                            }
-                            // kernel matrix bit order = ascending register bits
-                            std::vector<int> order(rb);
-                            std::sort(order.begin(), order.end());
-                            std::vector<int> src(k);   // kernel bit b <- original matrix bit src[b]
-                            for (int bb = 0; bb < k; bb++)
-                                src[bb] = (int)(std::find(rb.begin(), rb.end(), order[bb]) - rb.begin());
-                            const size_t D = (size_t)1 << k;
-                            auto orig = [&](size_t x) {
-                                size_t o = 0;
-                                for (int bb = 0; bb < k; bb++)
-                                    if ((x >> bb) & 1) o |= (size_t)1 << src[bb];
-                                return o;
-                            };
-                            std::vector<cplx> Mp(D * D);
-                            for (size_t x = 0; x < D; x++)
-                                for (size_t y = 0; y < D; y++) Mp[x * D + y] = g.data[orig(x) * D + orig(y)];
-                            for (size_t j = 0; j < g.controls.size(); j++) {
-                                const int b = g.controls[j];
-                                const int want = (int)((g.cvals >> j) & 1ull);
-                                const int tp = index_in(st.tile_bits, b);
-                                const int rg = regbit(b);
-                                if (rg >= 0) {
-                                    r.rcm |= 1 << rg;
-                                    if (want) r.rcv |= 1 << rg;
-                                } else if (tp >= 0) {
-                                    r.tcm |= 1u << tp;
-                                    if (want) r.tcv |= 1u << tp;
-                                } else {
-                                    r.gcm |= 1ull << b;
-                                    if (want) r.gcv |= 1ull << b;
-                                }
-                            }
-                            r.data_off = push_data(Mp);
-                        } else if (g.kind == Kind::Diagonal) {
-                            r.kind = 1;
-                            for (size_t j = 0; j < g.targets.size(); j++)
-                                route(g.targets[j], (int)j, r.r_bit, r.r_out, r.nr, r.t_pos, r.t_out, r.nt, r.g_bit,
-                                      r.g_out, r.ng);
-                            r.data_off = push_data(g.data);
-                        } else {
-                            r.kind = 2;
-                            const int ab = regbit(g.targets[0]);
-                            if (ab < 0) fail(SV_E_ARG, "internal: ancilla not in registers");
-                            r.mask = 1 << ab;
-                            r.n_c = (int)g.controls.size();
-                            r.is_signed = g.is_signed;
-                            r.dL = g.delta * std::ldexp(1.0, r.n_c - (g.is_signed ? 1 : 0));
-                            r.snap = g.snap;
-                            for (int j = 0; j < r.n_c; j++)
-                                route(g.controls[j], j, r.r_bit, r.r_out, r.nr, r.t_pos, r.t_out, r.nt, r.g_bit,
-                                      r.g_out, r.ng);
-                        }
-                        rops.push_back(r);
-                    }
-                    ph.op1 = (int)rops.size();
-                    phases.push_back(ph);
+                size_t ph0 = 0, opbase = 0;
+                lower_tile_step(st, a, blob, rops, phases, ph0, opbase);
+                if (use_jit) {
+                    std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
+                    std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
+                    JitPass jp;
+                    jp.name = "hhlsv_tile";
+                    jp.src = gen_tile_kernel(jp.name, a, lph, lops);
+                    rec.jit = (int)p->jit.size();
+                    p->jit.push_back(std::move(jp));
                 }
                 a.nphase = (int)(phases.size() - ph0);
-                tiles.push_back({p->recs.size(), ph0});
+                tiles.push_back({p->recs.size(), ph0, opbase});
                 break;
             }
         }
@@ -449,9 +506,10 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
     }
+    if (!p->jit.empty()) jit_build(p->jit);
     for (auto &t : tiles) {
         p->recs[t.rec].tile.phases = p->d_phases + t.op0;
-        p->recs[t.rec].tile.ops = p->d_ops;
+        p->recs[t.rec].tile.ops = p->d_ops + t.opbase;
         p->recs[t.rec].tile.blob = p->d_blob;
     }
     return p.release();
@@ -496,7 +554,14 @@ void program_run(sv_state *sv, sv_program *p) {
             case StepKind::Dense: cuda_check(dev::launch_dense(r.dense, sv->stream), "dense"); break;
             case StepKind::Diagonal: cuda_check(dev::launch_diag(r.diag, sv->stream), "diagonal"); break;
             case StepKind::RecipRY: cuda_check(dev::launch_recip(r.recip, sv->stream), "recip_ry"); break;
-            case StepKind::Tile: cuda_check(dev::launch_tile(r.tile, sv->stream), "tile"); break;
+            case StepKind::Tile:
+                if (r.jit >= 0)
+                    cuda_check(jit_launch(p->jit[r.jit], r.tile.psi, r.tile.blob, r.tile.n_tiles, r.tile.rank_base,
+                                          r.tile.T, sv->stream),
+                               "tile (jit)");
+                else
+                    cuda_check(dev::launch_tile(r.tile, sv->stream), "tile");
+                break;
             case StepKind::Exchange: exchange(sv, r.gbit, r.lbit); break;
         }
         if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");

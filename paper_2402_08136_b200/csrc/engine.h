@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "jit.h"
 #include "kernels.cuh"
 #include "sv_internal.h"
 
@@ -40,6 +41,7 @@ struct LaunchRec {
     dev::ProductArgs prod{};
     dev::TileArgs tile{};
     int gbit = 0, lbit = 0;           // exchange
+    int jit = -1;                     // tile: index into sv_program::jit (specialised kernel) or -1
     double bytes = 0;
 };
 
@@ -57,6 +59,7 @@ struct sv_program {
     uint64_t n_logical = 0;
     std::vector<double2 *> d_tabs;    // product-init tables (owned)
     double h2d_bytes = 0;             // uploaded at creation
+    std::vector<hhlsv::JitPass> jit;  // specialised tile passes
     bool timing = false;
     std::vector<cudaEvent_t> ev;      // 2 per rec when timing
     uint64_t launches() const;
@@ -71,6 +74,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                            const CompileOptions &co, uint64_t n_logical);
 void program_run(sv_state *sv, sv_program *p);
 void program_destroy(sv_program *p);
+void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blob, std::vector<dev::RegOp> &rops,
+                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out);
 void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out);
 void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out);
 void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in);

@@ -1,0 +1,386 @@
+// Tile-pass specialisation with NVRTC (sm_100a) — DESIGN.md §Tile / §JIT.
+//
+// The generic k_tile kernel interprets each op descriptor for every tile; at 2^30
+// amplitudes that per-op dispatch (dependent shared loads, branches, bit loops) costs
+// ~1 ms per op, 4-5x its FP64 work. Every op of a pass is identical for all tiles, so at
+// program-creation time we emit one straight-line CUDA kernel per tile pass in which the
+// tile bits, register phases, register-slot indices, control masks, bit runs and blob
+// offsets are compile-time constants, compile it with NVRTC for sm_100a, and launch it
+// through the runtime's library API. Matrix/table VALUES stay in the program's device
+// blob, so the generated source depends only on the circuit's structure and is cached
+// (in-process, keyed by the exact source text).
+#include <dlfcn.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "engine.h"
+#include "jit.h"
+
+namespace hhlsv {
+
+// ------------------------------------------------------------------ NVRTC ----
+namespace {
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram *nvrtcProgram_t;
+struct Nvrtc {
+    void *h = nullptr;
+    nvrtcResult_t (*create)(nvrtcProgram_t *, const char *, const char *, int, const char *const *,
+                            const char *const *) = nullptr;
+    nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char *const *) = nullptr;
+    nvrtcResult_t (*cubinSize)(nvrtcProgram_t, size_t *) = nullptr;
+    nvrtcResult_t (*cubin)(nvrtcProgram_t, char *) = nullptr;
+    nvrtcResult_t (*logSize)(nvrtcProgram_t, size_t *) = nullptr;
+    nvrtcResult_t (*log)(nvrtcProgram_t, char *) = nullptr;
+    nvrtcResult_t (*destroy)(nvrtcProgram_t *) = nullptr;
+    const char *(*errStr)(nvrtcResult_t) = nullptr;
+    std::string why;
+    bool ok = false;
+};
+
+Nvrtc &nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *names[] = {getenv("HHLSV_NVRTC_LIB"), "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                               "libnvrtc.so"};
+        for (const char *nm : names) {
+            if (!nm) continue;
+            n.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+            if (n.h) break;
+        }
+        if (!n.h) {
+            n.why = "cannot dlopen libnvrtc.so.12 (set HHLSV_NVRTC_LIB)";
+            return;
+        }
+#define SYM(f, s)                                                   \
+    n.f = reinterpret_cast<decltype(n.f)>(dlsym(n.h, s));           \
+    if (!n.f) {                                                     \
+        n.why = "libnvrtc lacks " s;                                \
+        return;                                                     \
+    }
+        SYM(create, "nvrtcCreateProgram")
+        SYM(compile, "nvrtcCompileProgram")
+        SYM(cubinSize, "nvrtcGetCUBINSize")
+        SYM(cubin, "nvrtcGetCUBIN")
+        SYM(logSize, "nvrtcGetProgramLogSize")
+        SYM(log, "nvrtcGetProgramLog")
+        SYM(destroy, "nvrtcDestroyProgram")
+        SYM(errStr, "nvrtcGetErrorString")
+#undef SYM
+        n.ok = true;
+    });
+    return n;
+}
+
+const char *kPrelude = R"(
+typedef unsigned long long u64;
+typedef unsigned int u32;
+__device__ __forceinline__ u32 swz(u32 u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+__device__ __forceinline__ u64 insz(u64 x, int p) { return ((x >> p) << (p + 1)) | (x & ((1ull << p) - 1ull)); }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ double2 mk(double x, double y) { double2 r; r.x = x; r.y = y; return r; }
+__device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
+    return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double recip_s(u64 m, int n_c, double dL, int sg, double snap) {
+    if (m == 0) return 0.0;
+    double sign = 1.0;
+    u64 mp = m;
+    if (sg && m >= (1ull << (n_c - 1))) { mp = (1ull << n_c) - m; sign = -1.0; }
+    const double r = __ddiv_rn(dL, (double)mp);
+    const double s = fabs(r - 1.0) <= snap ? 1.0 : (r < 1.0 ? r : 0.0);
+    return sign * s;
+}
+)";
+
+int dep_slot(int c, int M) {   // deposit bits of c into the set bits of M (4-bit register masks)
+    int out = 0, bit = 0;
+    for (int i = 0; i < 4; i++)
+        if ((M >> i) & 1) {
+            if ((c >> bit) & 1) out |= 1 << i;
+            bit++;
+        }
+    return out;
+}
+
+std::string u64s(uint64_t x) {
+    std::ostringstream o;
+    o << x << "ull";
+    return o.str();
+}
+
+std::string runs_expr(const char *src, int n, const uint8_t *s, const uint8_t *l, const uint8_t *d) {
+    if (n == 0) return "0ull";
+    std::ostringstream o;
+    for (int i = 0; i < n; i++) {
+        if (i) o << " | ";
+        o << "((((u64)(" << src << ")) >> " << (int)s[i] << ") & " << u64s((l[i] >= 64) ? ~0ull : ((1ull << l[i]) - 1))
+          << ") << " << (int)d[i];
+    }
+    return o.str();
+}
+}  // namespace
+
+bool jit_available(std::string *why) {
+    Nvrtc &n = nvrtc();
+    if (why) *why = n.why;
+    return n.ok;
+}
+
+// ---------------------------------------------------------------- codegen ----
+std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
+                            const std::vector<dev::RegOp> &ops) {
+    const int T = a.T;
+    const int NTHR = 1 << (T - dev::kRegBits);
+    const int SA = (T + 1) / 2, SB = T - SA;
+    std::ostringstream k;
+    k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ") " << name
+      << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
+    k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
+    k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+    k << "  double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);\n  double2 *buf1 = buf0 + NT;\n";
+    k << "  u64 *depA = reinterpret_cast<u64 *>(buf1 + NT);\n  u64 *depB = depA + " << (1 << SA) << ";\n";
+    k << "  for (int u = threadIdx.x; u < " << (1 << SA) << "; u += " << NTHR << ") { u64 d = 0;";
+    for (int i = 0; i < SA; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[i] << ";";
+    k << " depA[u] = d; }\n";
+    k << "  for (int u = threadIdx.x; u < " << (1 << SB) << "; u += " << NTHR << ") { u64 d = 0;";
+    for (int i = 0; i < SB; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[SA + i] << ";";
+    k << " depB[u] = d; }\n";
+    k << "  auto tile_base = [](u64 t) { u64 b = t;";
+    for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
+    k << " return b; };\n";
+    k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
+      << "]; };\n";
+    k << "  __syncthreads();\n";
+    k << "  u64 tile = blockIdx.x;\n";
+    k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+      << ") cp_async16(&buf0[swz(u)], &psi[addr(b0, u)]); }\n";
+    k << "  cp_async_commit();\n";
+    k << "  for (int it = 0; tile < n_tiles; tile += gridDim.x, it++) {\n";
+    k << "    double2 *cur = (it & 1) ? buf1 : buf0;\n    double2 *nxt = (it & 1) ? buf0 : buf1;\n";
+    k << "    const u64 next = tile + gridDim.x;\n";
+    k << "    if (next < n_tiles) { const u64 b1 = tile_base(next); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+      << ") cp_async16(&nxt[swz(u)], &psi[addr(b1, u)]); }\n";
+    k << "    cp_async_commit();\n";
+    k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
+    k << "    cp_async_wait1();\n    __syncthreads();\n";
+    for (size_t p = 0; p < ph.size(); p++) {
+        const dev::RegPhase &P = ph[p];
+        k << "    { // phase " << p << "\n      const u32 tb = 0u";
+        for (int i = 0; i < T - dev::kRegBits; i++) k << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
+        k << ";\n";
+        int rd[16];
+        for (int j = 0; j < 16; j++) {
+            rd[j] = 0;
+            for (int i = 0; i < 4; i++)
+                if ((j >> i) & 1) rd[j] |= 1 << P.R[i];
+        }
+        for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+        for (int oi = P.op0; oi < P.op1; oi++) {
+            const dev::RegOp &op = ops[oi];
+            std::ostringstream cond;
+            if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
+            if (op.kind == 0 && op.tcm) {
+                if (op.gcm) cond << " && ";
+                cond << "((tb & " << op.tcm << "u) == " << op.tcv << "u)";
+            }
+            const std::string c = cond.str();
+            k << "      " << (c.empty() ? "{" : "if (" + c + ") {") << " // op " << oi << "\n";
+            if (op.kind == 0) {
+                const int M = op.mask;
+                int K = 0;
+                for (int i = 0; i < 4; i++) K += (M >> i) & 1;
+                const int D = 1 << K;
+                const bool real = op.is_signed != 0;
+                k << "        const double2 *U = blob + " << op.data_off << "ull;\n";
+                if (K <= 2)
+                    for (int i = 0; i < D * D; i++) k << "        const double2 u" << i << " = __ldg(U + " << i << ");\n";
+                for (int g = 0; g < 16; g++) {
+                    if (g & M) continue;
+                    if ((g & op.rcm) != op.rcv) continue;
+                    k << "        {";
+                    for (int cc = 0; cc < D; cc++) k << " const double2 i" << cc << " = v" << (g | dep_slot(cc, M)) << ";";
+                    k << "\n";
+                    if (K >= 3) {
+                        // wide op: rolled row loop (bounded code size / compile time); outputs via a small array
+                        k << "          double2 o[" << D << "];\n          #pragma unroll 1\n          for (int r = 0; r < " << D
+                          << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = U + r * " << D << ";";
+                        for (int cc = 0; cc < D; cc++) {
+                            if (real)
+                                k << " { const double w = __ldg(&Ur[" << cc << "].x); ax = fma(w, i" << cc << ".x, ax); ay = fma(w, i"
+                                  << cc << ".y, ay); }";
+                            else
+                                k << " { const double2 w = __ldg(Ur + " << cc << "); ax = fma(w.x, i" << cc << ".x, ax); ax = fma(-w.y, i"
+                                  << cc << ".y, ax); ay = fma(w.x, i" << cc << ".y, ay); ay = fma(w.y, i" << cc << ".x, ay); }";
+                        }
+                        k << " o[r] = mk(ax, ay); }\n";
+                        for (int r = 0; r < D; r++) k << "          v" << (g | dep_slot(r, M)) << " = o[" << r << "];\n";
+                        k << "        }\n";
+                        continue;
+                    }
+                    for (int r = 0; r < D; r++) {
+                        k << "          { double ax = 0.0, ay = 0.0;";
+                        for (int cc = 0; cc < D; cc++) {
+                            std::string u = "u" + std::to_string(r * D + cc);
+                            if (real) {
+                                k << " ax = fma(" << u << ".x, i" << cc << ".x, ax); ay = fma(" << u << ".x, i" << cc
+                                  << ".y, ay);";
+                            } else {
+                                k << " { const double2 w = " << u << "; ax = fma(w.x, i" << cc << ".x, ax); ax = fma(-w.y, i"
+                                  << cc << ".y, ax); ay = fma(w.x, i" << cc << ".y, ay); ay = fma(w.y, i" << cc
+                                  << ".x, ay); }";
+                            }
+                        }
+                        k << " v" << (g | dep_slot(r, M)) << " = mk(ax, ay); }\n";
+                    }
+                    k << "        }\n";
+                }
+            } else {
+                k << "        const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
+                  << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
+                if (op.kind == 1) {
+                    k << "        const double2 *D = blob + " << op.data_off << "ull;\n";
+                    for (int j = 0; j < 16; j++)
+                        k << "        const double2 d" << j << " = __ldg(D + (ib | " << op.ridx[j] << "u));\n";
+                    for (int j = 0; j < 16; j++) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
+                } else {
+                    int A = 0;
+                    while (!((op.mask >> A) & 1)) A++;
+                    k << "        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n";
+                    for (int j = 0; j < 16; j++) {
+                        if ((j >> A) & 1) continue;
+                        const int j1 = j | (1 << A);
+                        k << "        { const double s = recip_s(ib | " << op.ridx[j] << "u, " << op.n_c << ", pr.x, "
+                          << op.is_signed << ", pr.y); const double c = sqrt(fma(-s, s, 1.0)); const double2 x0 = v"
+                          << j << ", x1 = v" << j1 << "; v" << j << " = mk(c * x0.x - s * x1.x, c * x0.y - s * x1.y); v"
+                          << j1 << " = mk(s * x0.x + c * x1.x, s * x0.y + c * x1.y); }\n";
+                    }
+                }
+            }
+            k << "      }\n";
+        }
+        for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
+        k << "      __syncthreads();\n    }\n";
+    }
+    k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+    k << "    __syncthreads();\n  }\n  cp_async_wait0();\n}\n";
+    return k.str();
+}
+
+// ---------------------------------------------------------------- compile ----
+namespace {
+struct CacheEntry {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    std::string err;
+};
+std::mutex g_mu;
+std::map<std::string, std::shared_ptr<CacheEntry>> g_cache;
+
+std::vector<char> compile_cubin(const std::string &src, std::string &err) {
+    Nvrtc &n = nvrtc();
+    nvrtcProgram_t prog = nullptr;
+    const std::string full = std::string(kPrelude) + src;
+    if (n.create(&prog, full.c_str(), "hhlsv_tile.cu", 0, nullptr, nullptr)) {
+        err = "nvrtcCreateProgram failed";
+        return {};
+    }
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "--extra-device-vectorization"};
+    int rc = n.compile(prog, 4, opts);
+    if (rc) {
+        size_t ls = 0;
+        n.logSize(prog, &ls);
+        std::string log(ls, '\0');
+        n.log(prog, &log[0]);
+        err = std::string("NVRTC: ") + n.errStr(rc) + "\n" + log.substr(0, 2000);
+        n.destroy(&prog);
+        return {};
+    }
+    size_t cs = 0;
+    n.cubinSize(prog, &cs);
+    std::vector<char> cubin(cs);
+    n.cubin(prog, cubin.data());
+    n.destroy(&prog);
+    return cubin;
+}
+}  // namespace
+
+std::vector<char> jit_compile_only(const std::string &src, std::string &err) {
+    if (!nvrtc().ok) {
+        err = nvrtc().why;
+        return {};
+    }
+    return compile_cubin(src, err);
+}
+
+void jit_build(std::vector<JitPass> &passes) {
+    if (!nvrtc().ok) fail(SV_E_CUDA, "tile JIT unavailable: " + nvrtc().why);
+    // compile the passes not yet in the cache in parallel (NVRTC programs are independent)
+    std::vector<std::shared_ptr<CacheEntry>> ents(passes.size());
+    std::vector<size_t> todo;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        for (size_t i = 0; i < passes.size(); i++) {
+            auto it = g_cache.find(passes[i].src);
+            if (it != g_cache.end()) {
+                ents[i] = it->second;
+            } else {
+                ents[i] = std::make_shared<CacheEntry>();
+                g_cache[passes[i].src] = ents[i];
+                todo.push_back(i);
+            }
+        }
+    }
+    std::vector<std::vector<char>> cubins(passes.size());
+    std::vector<std::thread> th;
+    for (size_t i : todo)
+        th.emplace_back([&, i] { cubins[i] = compile_cubin(passes[i].src, ents[i]->err); });
+    for (auto &t : th) t.join();
+    for (size_t i : todo) {
+        if (cubins[i].empty()) continue;
+        cudaError_t e = cudaLibraryLoadData(&ents[i]->lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        if (e == cudaSuccess) e = cudaLibraryGetKernel(&ents[i]->kern, ents[i]->lib, passes[i].name.c_str());
+        if (e != cudaSuccess) ents[i]->err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+    }
+    for (size_t i = 0; i < passes.size(); i++) {
+        if (!ents[i]->kern) {
+            std::lock_guard<std::mutex> lk(g_mu);
+            g_cache.erase(passes[i].src);
+            fail(SV_E_CUDA, "tile JIT failed: " + ents[i]->err);
+        }
+        passes[i].kern = ents[i]->kern;
+    }
+}
+
+cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
+                       int T, cudaStream_t s) {
+    const int threads = 1 << (T - dev::kRegBits);
+    const int SA = (T + 1) / 2, SB = T - SA;
+    const size_t smem = 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
+    const void *f = reinterpret_cast<const void *>(p.kern);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)148 * per_sm;
+    if (grid > n_tiles) grid = n_tiles;
+    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base};
+    return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);
+}
+
+}  // namespace hhlsv

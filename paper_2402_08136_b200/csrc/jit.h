@@ -1,0 +1,26 @@
+// NVRTC specialisation of tile passes (see jit.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace hhlsv {
+
+struct JitPass {
+    std::string name;
+    std::string src;
+    cudaKernel_t kern = nullptr;
+};
+
+bool jit_available(std::string *why);
+std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
+                            const std::vector<dev::RegOp> &ops);
+void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
+std::vector<char> jit_compile_only(const std::string &src, std::string &err);
+cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
+                       int T, cudaStream_t s);
+
+}  // namespace hhlsv

@@ -209,10 +209,14 @@ cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream
 }
 
 // ======================================================= f1 tile pass ====
-// Tile pass v2 (see kernels.cuh): persistent CTAs, cp.async double buffering of whole
-// tiles (2^T x 16 B, XOR swizzled), and register-resident op phases: within a phase each
-// thread holds the 16 amplitudes spanned by the phase's 4 register bits and applies every op
-// of the phase without touching shared memory. ONE HBM read + write for the whole op list.
+// Tile pass v3 (see kernels.cuh): persistent CTAs, cp.async double buffering of whole
+// tiles (2^T x 16 B, XOR swizzled), op descriptors staged once per CTA in shared memory,
+// a per-tile cooperative prologue (control checks + tile part of every index), and
+// register-resident op phases: within a phase each thread holds the 16 amplitudes spanned by
+// the phase's 4 register bits and applies every op of the phase without touching shared
+// memory. ONE HBM read + write for the whole op list.
+static_assert(sizeof(RegOp) % 16 == 0, "RegOp must be 16-byte sized");
+
 __device__ __forceinline__ uint32_t swz(uint32_t u) {
     return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u);
 }
@@ -238,27 +242,39 @@ __host__ __device__ constexpr int dep_mask(int c, int M) {
 __host__ __device__ constexpr int popc4(int M) { return (M & 1) + ((M >> 1) & 1) + ((M >> 2) & 1) + ((M >> 3) & 1); }
 
 // Dense / controlled op whose targets are the register bits of mask M (matrix bit order =
-// ascending register bits, re-ordered on the host). rcm/rcv: register-bit controls.
-template <int M>
+// ascending register bits, re-ordered on the host). rcm/rcv: register-bit controls (HasC).
+// Real matrices (H, V, V^T, RY — flagged by the host) use half the FP64 work.
+template <int M, bool HasC, bool Real>
 __device__ __forceinline__ void reg_dense(double2 (&v)[kRegAmps], const double2 *__restrict__ U, int rcm, int rcv) {
     constexpr int K = popc4(M);
     constexpr int D = 1 << K;
-    if (K <= 2) {
+    if (K <= 1) {
         double2 u[D * D];
 #pragma unroll
         for (int i = 0; i < D * D; i++) u[i] = __ldg(&U[i]);
 #pragma unroll
         for (int g = 0; g < kRegAmps; g++) {
             if (g & M) continue;
-            if ((g & rcm) != rcv) continue;
+            if (HasC && (g & rcm) != rcv) continue;
             double2 in[D];
 #pragma unroll
             for (int c = 0; c < D; c++) in[c] = v[g | dep_mask(c, M)];
 #pragma unroll
             for (int r = 0; r < D; r++) {
-                double2 acc = make_double2(0.0, 0.0);
+                double2 acc;
+                if (Real) {
+                    acc.x = u[r * D] .x * in[0].x;
+                    acc.y = u[r * D].x * in[0].y;
 #pragma unroll
-                for (int c = 0; c < D; c++) cfma(acc, u[r * D + c], in[c]);
+                    for (int c = 1; c < D; c++) {
+                        acc.x = fma(u[r * D + c].x, in[c].x, acc.x);
+                        acc.y = fma(u[r * D + c].x, in[c].y, acc.y);
+                    }
+                } else {
+                    acc = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int c = 0; c < D; c++) cfma(acc, u[r * D + c], in[c]);
+                }
                 v[g | dep_mask(r, M)] = acc;
             }
         }
@@ -266,29 +282,51 @@ __device__ __forceinline__ void reg_dense(double2 (&v)[kRegAmps], const double2 
 #pragma unroll
         for (int g = 0; g < kRegAmps; g++) {
             if (g & M) continue;
-            if ((g & rcm) != rcv) continue;
+            if (HasC && (g & rcm) != rcv) continue;
             double2 in[D];
 #pragma unroll
             for (int c = 0; c < D; c++) in[c] = v[g | dep_mask(c, M)];
 #pragma unroll
             for (int r = 0; r < D; r++) {
                 double2 acc = make_double2(0.0, 0.0);
+                if (Real) {
 #pragma unroll
-                for (int c = 0; c < D; c++) cfma(acc, __ldg(&U[r * D + c]), in[c]);
+                    for (int c = 0; c < D; c++) {
+                        const double w = __ldg(&U[r * D + c].x);
+                        acc.x = fma(w, in[c].x, acc.x);
+                        acc.y = fma(w, in[c].y, acc.y);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < D; c++) cfma(acc, __ldg(&U[r * D + c]), in[c]);
+                }
                 v[g | dep_mask(r, M)] = acc;
             }
         }
     }
 }
 
+template <int M>
+__device__ __forceinline__ void reg_dense_dispatch(double2 (&v)[kRegAmps], const double2 *__restrict__ U, int rcm,
+                                                   int rcv, bool real) {
+    if (rcm) {
+        if (real) reg_dense<M, true, true>(v, U, rcm, rcv);
+        else reg_dense<M, true, false>(v, U, rcm, rcv);
+    } else {
+        if (real) reg_dense<M, false, true>(v, U, 0, 0);
+        else reg_dense<M, false, false>(v, U, 0, 0);
+    }
+}
+
 template <int A>   // A = register bit of the ancilla
 __device__ __forceinline__ void reg_recip(double2 (&v)[kRegAmps], const RegOp &op, uint64_t mbase) {
+    const int n_c = op.n_c, sg = op.is_signed;
+    const double dL = op.dL, snap = op.snap;
 #pragma unroll
     for (int j = 0; j < kRegAmps; j++) {
         if ((j >> A) & 1) continue;
-        uint64_t m = mbase;
-        for (int i = 0; i < op.nr; i++) m |= (uint64_t)((j >> op.r_bit[i]) & 1) << op.r_out[i];
-        const double sv = recip_s(m, op.n_c, op.dL, op.is_signed, op.snap);
+        const uint64_t m = mbase | op.ridx[j];
+        const double sv = recip_s(m, n_c, dL, sg, snap);
         const double cv = sqrt(fma(-sv, sv, 1.0));
         const double2 x0 = v[j], x1 = v[j | (1 << A)];
         v[j] = make_double2(cv * x0.x - sv * x1.x, cv * x0.y - sv * x1.y);
@@ -296,45 +334,11 @@ __device__ __forceinline__ void reg_recip(double2 (&v)[kRegAmps], const RegOp &o
     }
 }
 
-__device__ __forceinline__ void apply_phase_ops(double2 (&v)[kRegAmps], const TileArgs &a, const RegPhase &ph,
-                                                uint32_t tb, uint64_t gbase) {
-    for (int oi = ph.op0; oi < ph.op1; oi++) {
-        const RegOp &op = a.ops[oi];
-        if ((gbase & op.gcm) != op.gcv) continue;                 // CTA-uniform
-        if (op.kind == 0) {
-            if ((tb & op.tcm) != op.tcv) continue;                // thread-uniform
-            const double2 *U = a.blob + op.data_off;
-            const int rcm = op.rcm, rcv = op.rcv;
-            switch (op.mask) {
-#define DCASE(M) case M: reg_dense<M>(v, U, rcm, rcv); break;
-                DCASE(1) DCASE(2) DCASE(3) DCASE(4) DCASE(5) DCASE(6) DCASE(7) DCASE(8)
-                DCASE(9) DCASE(10) DCASE(11) DCASE(12) DCASE(13) DCASE(14) DCASE(15)
-#undef DCASE
-                default: break;
-            }
-        } else {
-            uint64_t base = 0;
-            for (int i = 0; i < op.ng; i++) base |= ((gbase >> op.g_bit[i]) & 1ull) << op.g_out[i];
-            for (int i = 0; i < op.nt; i++) base |= (uint64_t)((tb >> op.t_pos[i]) & 1u) << op.t_out[i];
-            if (op.kind == 1) {
-                const double2 *tab = a.blob + op.data_off;
-#pragma unroll
-                for (int j = 0; j < kRegAmps; j++) {
-                    uint32_t idx = (uint32_t)base;
-                    for (int i = 0; i < op.nr; i++) idx |= (uint32_t)((j >> op.r_bit[i]) & 1) << op.r_out[i];
-                    v[j] = cmul(__ldg(&tab[idx]), v[j]);
-                }
-            } else {
-                switch (op.mask) {
-                    case 1: reg_recip<0>(v, op, base); break;
-                    case 2: reg_recip<1>(v, op, base); break;
-                    case 4: reg_recip<2>(v, op, base); break;
-                    case 8: reg_recip<3>(v, op, base); break;
-                    default: break;
-                }
-            }
-        }
-    }
+__device__ __forceinline__ uint64_t gather_runs(uint64_t x, int n, const uint8_t *src, const uint8_t *len,
+                                                const uint8_t *dst) {
+    uint64_t o = 0;
+    for (int i = 0; i < n; i++) o |= ((x >> src[i]) & ((1ull << len[i]) - 1ull)) << dst[i];
+    return o;
 }
 
 __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
@@ -344,27 +348,38 @@ __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
     const int nthr = (int)blockDim.x;            // = NT / 16
     double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);
     double2 *buf1 = buf0 + NT;
+    RegOp *sops = reinterpret_cast<RegOp *>(buf1 + NT);
+    const int nops = a.nops;
+    uint64_t *tinfo = reinterpret_cast<uint64_t *>(sops + nops);     // per op: tile part (bit 63: skip)
     const int SA = (T + 1) / 2, SB = T - SA;
-    uint64_t *depA = reinterpret_cast<uint64_t *>(buf1 + NT);
+    uint64_t *depA = tinfo + nops;
     uint64_t *depB = depA + (1 << SA);
+    {   // stage op descriptors (16-byte vectors)
+        const int4 *src = reinterpret_cast<const int4 *>(a.ops);
+        int4 *dst = reinterpret_cast<int4 *>(sops);
+        const int nv = nops * (int)(sizeof(RegOp) / 16);
+        for (int i = threadIdx.x; i < nv; i += nthr) dst[i] = src[i];
+    }
+    const uint32_t maskA = (1u << SA) - 1u;
+    __shared__ int s_tbits[16];
+    for (int i = threadIdx.x; i < 16; i += nthr) s_tbits[i] = a.tbits[i];
+    __syncthreads();
     for (int u = threadIdx.x; u < (1 << SA); u += nthr) {
         uint64_t d = 0;
         for (int i = 0; i < SA; i++)
-            if ((u >> i) & 1) d |= 1ull << a.tbits[i];
+            if ((u >> i) & 1) d |= 1ull << s_tbits[i];
         depA[u] = d;
     }
     for (int u = threadIdx.x; u < (1 << SB); u += nthr) {
         uint64_t d = 0;
         for (int i = 0; i < SB; i++)
-            if ((u >> i) & 1) d |= 1ull << a.tbits[SA + i];
+            if ((u >> i) & 1) d |= 1ull << s_tbits[SA + i];
         depB[u] = d;
     }
-    const uint32_t maskA = (1u << SA) - 1u;
-    __syncthreads();
 
     auto tile_base = [&](uint64_t tile) {
         uint64_t b = tile;
-        for (int i = 0; i < T; i++) b = insz(b, a.tbits[i]);
+        for (int i = 0; i < T; i++) b = insz(b, s_tbits[i]);
         return b;
     };
     auto prefetch = [&](uint64_t tile, double2 *dst) {
@@ -372,6 +387,7 @@ __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
         for (uint32_t u = threadIdx.x; u < NT; u += nthr)
             cp_async16(&dst[swz(u)], &a.psi[base | depA[u & maskA] | depB[u >> SA]]);
     };
+    __syncthreads();
 
     uint64_t tile = blockIdx.x;
     if (tile < a.n_tiles) prefetch(tile, buf0);
@@ -382,10 +398,17 @@ __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
         const uint64_t next = tile + gridDim.x;
         if (next < a.n_tiles) prefetch(next, nxt);
         cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
         const uint64_t base = tile_base(tile);
         const uint64_t gbase = a.rank_base | base;
+        // tile prologue: control check and tile part of the index of every op
+        for (int i = threadIdx.x; i < nops; i += nthr) {
+            const RegOp &op = sops[i];
+            uint64_t t = gather_runs(gbase, op.ngr, op.g_src, op.g_len, op.g_dst);
+            if ((gbase & op.gcm) != op.gcv) t |= 1ull << 63;
+            tinfo[i] = t;
+        }
+        cp_async_wait<1>();
+        __syncthreads();
         for (int p = 0; p < a.nphase; p++) {
             const RegPhase &ph = a.phases[p];
             uint32_t tb = 0;                          // tile-local index bits of this thread
@@ -402,7 +425,42 @@ __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
             double2 v[kRegAmps];
 #pragma unroll
             for (int j = 0; j < kRegAmps; j++) v[j] = cur[swz(tb | rd[j])];
-            apply_phase_ops(v, a, ph, tb, gbase);
+            for (int oi = ph.op0; oi < ph.op1; oi++) {
+                const uint64_t ti = tinfo[oi];
+                if (ti >> 63) continue;                                    // CTA-uniform skip
+                const RegOp &op = sops[oi];
+                if (op.kind == 0) {
+                    if ((tb & op.tcm) != op.tcv) continue;                // thread controls
+                    const double2 *U = a.blob + op.data_off;
+                    const int rcm = op.rcm, rcv = op.rcv;
+                    const bool real = op.is_signed != 0;      // dense ops reuse is_signed as the real flag
+                    switch (op.mask) {
+#define DCASE(M) case M: reg_dense_dispatch<M>(v, U, rcm, rcv, real); break;
+                        DCASE(1) DCASE(2) DCASE(3) DCASE(4) DCASE(5) DCASE(6) DCASE(7) DCASE(8)
+                        DCASE(9) DCASE(10) DCASE(11) DCASE(12) DCASE(13) DCASE(14) DCASE(15)
+#undef DCASE
+                        default: break;
+                    }
+                } else {
+                    const uint64_t b = ti | gather_runs(tb, op.ntr, op.t_src, op.t_len, op.t_dst);
+                    if (op.kind == 1) {
+                        const double2 *tab = a.blob + op.data_off;
+                        double2 ph_[kRegAmps];
+#pragma unroll
+                        for (int j = 0; j < kRegAmps; j++) ph_[j] = __ldg(&tab[(uint32_t)b | op.ridx[j]]);
+#pragma unroll
+                        for (int j = 0; j < kRegAmps; j++) v[j] = cmul(ph_[j], v[j]);
+                    } else {
+                        switch (op.mask) {
+                            case 1: reg_recip<0>(v, op, b); break;
+                            case 2: reg_recip<1>(v, op, b); break;
+                            case 4: reg_recip<2>(v, op, b); break;
+                            case 8: reg_recip<3>(v, op, b); break;
+                            default: break;
+                        }
+                    }
+                }
+            }
 #pragma unroll
             for (int j = 0; j < kRegAmps; j++) cur[swz(tb | rd[j])] = v[j];
             __syncthreads();
@@ -415,13 +473,14 @@ __global__ void __launch_bounds__(256) k_tile(const TileArgs a) {
     cp_async_wait<0>();
 }
 
-size_t tile_smem_bytes(int T) {
+size_t tile_smem_bytes(int T, int nops) {
     const int SA = (T + 1) / 2, SB = T - SA;
-    return 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
+    return 2 * sizeof(double2) * ((size_t)1 << T) + (sizeof(RegOp) + 8) * (size_t)nops +
+           sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
 }
 
 cudaError_t launch_tile(const TileArgs &a, cudaStream_t s) {
-    const size_t smem = tile_smem_bytes(a.T);
+    const size_t smem = tile_smem_bytes(a.T, a.nops);
     const int threads = 1 << (a.T - kRegBits);
     cudaError_t e = cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

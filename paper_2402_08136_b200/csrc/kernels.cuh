@@ -71,15 +71,16 @@ struct ProductArgs {             // a3: product-state initialisation (prep + H l
 constexpr int kRegBits = 4;
 constexpr int kRegAmps = 1 << kRegBits;
 
-struct RegOp {
+struct alignas(16) RegOp {       // staged in shared memory by every CTA
     int kind;                    // 0 dense/controlled, 1 diagonal, 2 recip
     int mask;                    // dense: register-bit mask of the targets; recip: 1 << (anc register bit)
     int rcm, rcv;                // dense: register-bit controls (mask / required values)
     uint32_t tcm, tcv;           // dense: controls on thread-held tile positions (tile-local masks)
     uint64_t gcm, gcv;           // controls outside the tile (global index bits): op skipped unless match
-    int nr, r_bit[4], r_out[4];  // diag/recip: register bits -> output bit (table index / clock value)
-    int nt, t_pos[16], t_out[16];// diag/recip: tile positions held by threads -> output bit
-    int ng, g_bit[62], g_out[62];// diag/recip: global-index bits outside the tile -> output bit
+    uint32_t ridx[kRegAmps];     // diag/recip: register-slot part of the table index / clock value
+    int ntr, ngr;                // bit runs: thread part (tile-local positions), tile part (global index)
+    uint8_t t_src[12], t_len[12], t_dst[12];
+    uint8_t g_src[48], g_len[48], g_dst[48];
     int n_c, is_signed;
     double dL, snap;
     uint64_t data_off;           // matrix (register-bit order) / table offset in the blob (double2 units)
@@ -98,7 +99,8 @@ struct TileArgs {
     int tbits[16];               // sorted physical local bits of the tile
     int nphase;
     const RegPhase *phases;      // device
-    const RegOp *ops;            // device
+    int nops;                    // ops of this step (all phases)
+    const RegOp *ops;            // device, this step's ops (phase op0/op1 index into it)
     const double2 *blob;         // program data blob
     uint64_t rank_base;
 };
@@ -110,7 +112,7 @@ cudaError_t launch_recip(const RecipArgs &a, cudaStream_t s);
 cudaError_t launch_product(const ProductArgs &a, cudaStream_t s);
 cudaError_t launch_zero_init(double2 *psi, uint64_t n, int set_first, cudaStream_t s);
 cudaError_t launch_tile(const TileArgs &a, cudaStream_t s);
-size_t tile_smem_bytes(int T);
+size_t tile_smem_bytes(int T, int nops);
 
 // Deterministic reductions. partial has >= kRedBlocks doubles; result written to out (device).
 constexpr int kRedBlocks = 1184;   // 148 SMs x 8

@@ -42,7 +42,8 @@ class sv_gate(ctypes.Structure):
 
 
 class sv_fuse_options(ctypes.Structure):
-    _fields_ = [("fusion_kmax", ctypes.c_int), ("diag_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int)]
+    _fields_ = [("fusion_kmax", ctypes.c_int), ("diag_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
+                ("tile_jit", ctypes.c_int)]
 
 
 class sv_plan_report(ctypes.Structure):
@@ -52,7 +53,8 @@ class sv_plan_report(ctypes.Structure):
 
 class hhl_options(ctypes.Structure):
     _fields_ = [("clock_qubits", ctypes.c_int), ("fusion_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
-                ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("qpe_mode", ctypes.c_int)]
+                ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("tile_jit", ctypes.c_int),
+                ("qpe_mode", ctypes.c_int)]
 
 
 class hhl_report(ctypes.Structure):
@@ -175,8 +177,8 @@ class _GateArray:
         self.n = len(gates)
 
 
-def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0):
-    return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits))
+def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0, tile_jit=0):
+    return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits), int(tile_jit))
 
 
 def nccl_unique_id() -> bytes:
@@ -247,9 +249,9 @@ class State:
         ga = _GateArray(gates)
         _check(load().sv_apply_fused(self._h, ga.arr, ga.n))
 
-    def apply_circuit(self, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0) -> dict:
+    def apply_circuit(self, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0) -> dict:
         ga = _GateArray(gates)
-        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
         rep = sv_plan_report()
         _check(load().sv_apply_circuit(self._h, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(rep)))
         return {f: getattr(rep, f) for f, _ in rep._fields_}
@@ -285,9 +287,9 @@ class Program:
         self.report = report
 
     @classmethod
-    def create(cls, state: State, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0):
+    def create(cls, state: State, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0):
         ga = _GateArray(gates)
-        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
         h = ctypes.c_void_p()
         rep = sv_plan_report()
         _check(load().sv_program_create(state.handle, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(h),
@@ -337,10 +339,11 @@ class Program:
 STEP_KINDS = ["init_zero", "init_product", "dense", "diagonal", "recip_ry", "tile", "exchange"]
 
 
-def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax=0, tile_qubits=0):
-    """Host-only: fuse + schedule a logical gate list (no GPU needed). Returns (text, report)."""
+def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0):
+    """Host-only: fuse + schedule a logical gate list (no GPU needed). Returns (text, report).
+    tile_jit=1 also generates and NVRTC-compiles (sm_100a) every tile pass."""
     ga = _GateArray(gates)
-    o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits)
+    o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
     buf = ctypes.create_string_buffer(1 << 22)
     rep = sv_plan_report()
     _check(load().sv_schedule_dump(int(n_qubits), int(world), ga.arr, ga.n, ctypes.byref(o), buf, len(buf),
@@ -348,9 +351,9 @@ def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax
     return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
 
 
-def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, qpe_mode=0):
+def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0, qpe_mode=0):
     return hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap), int(init_fold),
-                       int(qpe_mode))
+                       int(tile_jit), int(qpe_mode))
 
 
 def hhl_plan_size(A, b, **kw):

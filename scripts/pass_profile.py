@@ -17,13 +17,16 @@ ap.add_argument("--config", default="S30")
 ap.add_argument("--kmax", type=int, nargs="+", default=[4])
 ap.add_argument("--tile", type=int, nargs="+", default=[12])
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--qpe", type=int, nargs="+", default=[0])
+ap.add_argument("--jit", type=int, nargs="+", default=[0])
 ap.add_argument("--verbose", action="store_true")
 a = ap.parse_args()
 A, b, nc = configs.get(a.config)
 st = pkg.State(configs.n_qubits(a.config))
-for k in a.kmax:
-    for T in a.tile:
-        prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=k, tile_qubits=T)
+import itertools  # noqa: E402
+for q, k, T, J in itertools.product(a.qpe, a.kmax, a.tile, a.jit):
+    if True:
+        prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=k, tile_qubits=T, qpe_mode=q, tile_jit=J)
         prog.set_timing(True)
         for _ in range(a.reps):
             prog.run()
@@ -31,9 +34,10 @@ for k in a.kmax:
         dump = prog.dump().splitlines()
         heads = [ln for ln in dump if not ln.startswith("  ")]
         total = sum(x[0] for x in t)
-        print(f"== {a.config} kmax={k} tile={T}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
+        import time as _t
+        print(f"== {a.config} qpe={q} kmax={k} tile={T} jit={J}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
               f"total {total:.1f} ms")
-        if a.verbose or True:
+        if a.verbose:
             for (ms, kind, by, la), h in zip(t, heads):
                 print(f"   {ms:9.3f} ms  {by / ms / 1e6 if ms > 0 else 0:8.1f} GB/s  {h[:100]}")
         prog.destroy()

@@ -16,7 +16,8 @@ from workloads import configs, synthetic
 
 pytestmark = pytest.mark.gpu
 
-MODES = [dict(tile_qubits=-1), dict(tile_qubits=6), dict(tile_qubits=10)]
+MODES = [dict(tile_qubits=-1), dict(tile_qubits=6, tile_jit=-1), dict(tile_qubits=10, tile_jit=-1),
+         dict(tile_qubits=9, tile_jit=1)]
 
 
 def run_both(n, gates, psi0=None, fused=True, **kw):
@@ -120,7 +121,9 @@ def test_basis_gate_stream_paper_fusion():
 @pytest.mark.parametrize("name", ["C1", "C2", "C3p", "C3"])
 @pytest.mark.parametrize("opts", [dict(), dict(tile_qubits=-1), dict(fusion_kmax=-1, tile_qubits=-1),
                                   dict(fusion_kmax=2, tile_qubits=8), dict(init_fold=-1), dict(qpe_mode=1),
-                                  dict(qpe_mode=1, tile_qubits=-1), dict(qpe_mode=1, fusion_kmax=1, tile_qubits=11)])
+                                  dict(qpe_mode=1, tile_qubits=-1), dict(qpe_mode=1, fusion_kmax=1, tile_qubits=11),
+                                  dict(qpe_mode=1, fusion_kmax=1, tile_qubits=10, tile_jit=1),
+                                  dict(fusion_kmax=2, tile_qubits=10, tile_jit=1)])
 def test_hhl_configs_full_state(name, opts):
     """C1-C3 (configs[0..2]) + C3p (Table 1 14-bus): every amplitude within 1e-10 of the oracle,
     identical post-selection index set, |dP| <= 1e-12, x within 1e-10."""
@@ -210,7 +213,7 @@ def test_many_tiles_ragged():
     n = 22
     gates = synthetic.random_circuit(n, 40, seed=22, kmax=3)
     psi0 = synthetic.random_state(n, 22)
-    for mode in (dict(tile_qubits=-1), dict(tile_qubits=12)):
+    for mode in (dict(tile_qubits=-1), dict(tile_qubits=12, tile_jit=-1), dict(tile_qubits=12, tile_jit=1)):
         got, ref, _ = run_both(n, gates, psi0, fusion_kmax=4, **mode)
         assert np.abs(got - ref).max() < 1e-10
 
