@@ -175,7 +175,8 @@ def run_ours(args):
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     cfg = args.config or ("S30" if world == 1 else f"S{30 + int(math.log2(world))}")
     A, b, nc = configs.get(cfg)
-    opts = dict(clock_qubits=nc, fusion_kmax=args.kmax, tile_qubits=args.tile)
+    opts = dict(clock_qubits=nc, fusion_kmax=args.kmax, tile_qubits=args.tile, qpe_mode=args.qpe,
+                tile_jit=args.jit)
     stream = torch.cuda.current_stream()
 
     st = pkg.State(configs.n_qubits(cfg), world=world, rank=rank, device=local, nccl_id=nccl_id)
@@ -274,6 +275,7 @@ def run_ours(args):
                            "n_clock": rep["n_clock"], "system": "IEEE 14-bus DC B (MATPOWER case14), 16x16",
                            "n_logical_gates": rep["n_logical"], "n_fused_ops": rep["n_fused"],
                            "n_passes": rep["n_passes"], "fusion_kmax": args.kmax, "tile_qubits": args.tile,
+                           "qpe_mode": ["textbook", "eigenbasis"][args.qpe], "tile_jit": args.jit,
                            "l2": "state (16 GiB/GPU) >> 126 MB L2; no flush needed",
                            "hhl_circuit_time_ms": ms_step, "p_success": ps,
                            "hbm_pass_gbs": rep["pass_bytes"] / world / (ms_step * 1e-3) / 1e9},
@@ -292,8 +294,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
-    ap.add_argument("--kmax", type=int, default=4)
-    ap.add_argument("--tile", type=int, default=12)
+    ap.add_argument("--kmax", type=int, default=1)
+    ap.add_argument("--tile", type=int, default=11)
+    ap.add_argument("--qpe", type=int, default=1, help="0 textbook c-U chain, 1 eigenbasis rewrite (SURVEY f2)")
+    ap.add_argument("--jit", type=int, default=0, help="tile pass specialisation: 0 auto, 1 on, -1 off")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -270,7 +270,9 @@ static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const
                 v.data[(size_t)r * N + c] = transpose ? p.V[c + (size_t)N * r] : p.V[r + (size_t)N * c];
         return v;
     };
-    const int chunk = std::max(1, 12 - nb);
+    // chunks of 4 clock bits: tables of 2^(n_b+4) entries (4 KB at n_b = 4) stay L1-resident in the
+    // tile passes (12-qubit tables thrash L1 when several are live in one pass)
+    const int chunk = std::max(1, std::min(4, 12 - nb));
     std::vector<Gate> diags;
     for (int j0 = 0; j0 < nc; j0 += chunk) {
         const int cj = std::min(chunk, nc - j0);

@@ -146,6 +146,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
+    int wide_ops = 0;          // dense ops with >= 3 targets: unrolled when few, rolled (bounded code) when many
+    for (auto &op : ops)
+        if (op.kind == 0 && ((op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1)) >= 3)
+            wide_ops++;
     std::ostringstream k;
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
@@ -214,9 +218,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     k << "        {";
                     for (int cc = 0; cc < D; cc++) k << " const double2 i" << cc << " = v" << (g | dep_slot(cc, M)) << ";";
                     k << "\n";
-                    if (K >= 3) {
-                        // wide op: rolled row loop (bounded code size / compile time); outputs via a small array
-                        k << "          double2 o[" << D << "];\n          #pragma unroll 1\n          for (int r = 0; r < " << D
+                    if (K >= 3 && wide_ops > 4) {
+                        // many wide ops: rolled row loop (bounded code / compile time); each output row goes
+                        // straight to this thread's own smem slot, then the D slots are reloaded
+                        int Rpos[4], nrp = 0;
+                        for (int i = 0; i < 4; i++)
+                            if ((M >> i) & 1) Rpos[nrp++] = P.R[i];
+                        const int base_slot = rd[g];
+                        k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
                           << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = U + r * " << D << ";";
                         for (int cc = 0; cc < D; cc++) {
                             if (real)
@@ -226,15 +235,21 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 k << " { const double2 w = __ldg(Ur + " << cc << "); ax = fma(w.x, i" << cc << ".x, ax); ax = fma(-w.y, i"
                                   << cc << ".y, ax); ay = fma(w.x, i" << cc << ".y, ay); ay = fma(w.y, i" << cc << ".x, ay); }";
                         }
-                        k << " o[r] = mk(ax, ay); }\n";
-                        for (int r = 0; r < D; r++) k << "          v" << (g | dep_slot(r, M)) << " = o[" << r << "];\n";
+                        k << " const u32 slot = " << base_slot << "u";
+                        for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
+                        k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
+                        for (int r = 0; r < D; r++) {
+                            const int j = g | dep_slot(r, M);
+                            k << "          v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+                        }
                         k << "        }\n";
                         continue;
                     }
                     for (int r = 0; r < D; r++) {
                         k << "          { double ax = 0.0, ay = 0.0;";
                         for (int cc = 0; cc < D; cc++) {
-                            std::string u = "u" + std::to_string(r * D + cc);
+                            std::string u = K <= 2 ? ("u" + std::to_string(r * D + cc))
+                                                   : ("__ldg(U + " + std::to_string(r * D + cc) + ")");
                             if (real) {
                                 k << " ax = fma(" << u << ".x, i" << cc << ".x, ax); ay = fma(" << u << ".x, i" << cc
                                   << ".y, ay);";
