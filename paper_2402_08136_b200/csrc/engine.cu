@@ -146,8 +146,8 @@ static int index_in(const std::vector<int> &v, int x) {
 
 static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec) {
     // group factors (physical bits) into <= 4 chunks of <= 12 bits, each a tensor-product table
-    std::vector<const ProductFactor *> fs;
-    for (auto &f : st.factors) fs.push_back(&f);
+    std::vector<const ProductFactor *> fs, ds;
+    for (auto &f : st.factors) (f.diag ? ds : fs).push_back(&f);
     std::sort(fs.begin(), fs.end(), [](const ProductFactor *a, const ProductFactor *b) {
         return *std::min_element(a->qubits.begin(), a->qubits.end()) <
                *std::min_element(b->qubits.begin(), b->qubits.end());
@@ -194,6 +194,25 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
         p->d_tabs.push_back(d);
         p->h2d_bytes += sizeof(double2) * ct[c].size();
         a.tab[c] = d;
+    }
+    if (ds.size() > 8) fail(SV_E_ARG, "too many folded diagonals");
+    a.ndiag = (int)ds.size();
+    for (size_t k = 0; k < ds.size(); k++) {
+        const ProductFactor &f = *ds[k];
+        a.dn[k] = (int)f.qubits.size();
+        bool contig = true;
+        for (size_t j = 0; j < f.qubits.size(); j++) {
+            a.dbits[k][j] = f.qubits[j];
+            if (f.qubits[j] != f.qubits[0] + (int)j) contig = false;
+        }
+        a.dcontig[k] = contig;
+        double2 *d = nullptr;
+        cuda_check(cudaMalloc(&d, sizeof(double2) * f.vec.size()), "cudaMalloc(init diagonal)");
+        cuda_check(cudaMemcpy(d, f.vec.data(), sizeof(double2) * f.vec.size(), cudaMemcpyHostToDevice),
+                   "upload init diagonal");
+        p->d_tabs.push_back(d);
+        p->h2d_bytes += sizeof(double2) * f.vec.size();
+        a.dtab[k] = d;
     }
 }
 

@@ -414,11 +414,13 @@ static std::vector<cplx> embed_dense(const std::vector<cplx> &m, const std::vect
 // ------------------------------------------------------------ product fold ----
 size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors) {
     std::vector<char> touched(n, 0);
+    const bool diag_phase = false;
     factors.clear();
     size_t i = 0;
     for (; i < gates.size(); i++) {
         const Gate &g = gates[i];
         if (g.kind != Kind::Dense) break;
+        if (diag_phase) break;
         bool fresh = true;
         for (int q : g.targets) fresh &= !touched[q];
         if (!fresh) {
@@ -444,6 +446,19 @@ size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<Pr
         f.vec.resize(d);
         for (size_t r = 0; r < d; r++) f.vec[r] = g.data[r * d];     // column 0: U|0>
         for (int q : g.targets) touched[q] = 1;
+        factors.push_back(std::move(f));
+    }
+    // diagonal gates right after the product state: folded as per-amplitude phase tables
+    for (; i < gates.size(); i++) {
+        const Gate &g = gates[i];
+        if (g.kind != Kind::Diagonal || g.targets.size() > 12) break;
+        size_t nd = 0;
+        for (auto &f : factors) nd += f.diag;
+        if (nd >= 8) break;
+        ProductFactor f;
+        f.qubits = g.targets;
+        f.vec = g.data;
+        f.diag = true;
         factors.push_back(std::move(f));
     }
     return i;

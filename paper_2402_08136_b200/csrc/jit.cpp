@@ -215,29 +215,39 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 for (int g = 0; g < 16; g++) {
                     if (g & M) continue;
                     if ((g & op.rcm) != op.rcv) continue;
-                    k << "        {";
-                    for (int cc = 0; cc < D; cc++) k << " const double2 i" << cc << " = v" << (g | dep_slot(cc, M)) << ";";
-                    k << "\n";
-                    if (K >= 3 && wide_ops > 4) {
-                        // many wide ops: rolled row loop (bounded code / compile time); each output row goes
-                        // straight to this thread's own smem slot, then the D slots are reloaded
+                    if (K >= 3) {
+                        // wide op: inputs straight from the v registers, each output row goes to this
+                        // thread's own smem slot, then the D slots are reloaded (no input copies: keeps
+                        // the pass's register footprint, hence occupancy, unchanged)
                         int Rpos[4], nrp = 0;
                         for (int i = 0; i < 4; i++)
                             if ((M >> i) & 1) Rpos[nrp++] = P.R[i];
-                        const int base_slot = rd[g];
-                        k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
-                          << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = U + r * " << D << ";";
-                        for (int cc = 0; cc < D; cc++) {
-                            if (real)
-                                k << " { const double w = __ldg(&Ur[" << cc << "].x); ax = fma(w, i" << cc << ".x, ax); ay = fma(w, i"
-                                  << cc << ".y, ay); }";
-                            else
-                                k << " { const double2 w = __ldg(Ur + " << cc << "); ax = fma(w.x, i" << cc << ".x, ax); ax = fma(-w.y, i"
-                                  << cc << ".y, ax); ay = fma(w.x, i" << cc << ".y, ay); ay = fma(w.y, i" << cc << ".x, ay); }";
+                        auto row = [&](const std::string &Ur) {
+                            std::ostringstream o;
+                            for (int cc = 0; cc < D; cc++) {
+                                const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
+                                if (real)
+                                    o << " { const double w = __ldg(&" << Ur << "[" << cc << "].x); ax = fma(w, " << in
+                                      << ".x, ax); ay = fma(w, " << in << ".y, ay); }";
+                                else
+                                    o << " { const double2 w = __ldg(" << Ur << " + " << cc << "); ax = fma(w.x, " << in
+                                      << ".x, ax); ax = fma(-w.y, " << in << ".y, ax); ay = fma(w.x, " << in
+                                      << ".y, ay); ay = fma(w.y, " << in << ".x, ay); }";
+                            }
+                            return o.str();
+                        };
+                        k << "        {\n";
+                        if (wide_ops > 4) {
+                            k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
+                              << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = U + r * " << D << ";" << row("Ur")
+                              << " const u32 slot = " << rd[g] << "u";
+                            for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
+                            k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
+                        } else {
+                            for (int r = 0; r < D; r++)
+                                k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
+                                  << row("Ur") << " cur[swz(tb | " << rd[g | dep_slot(r, M)] << "u)] = mk(ax, ay); }\n";
                         }
-                        k << " const u32 slot = " << base_slot << "u";
-                        for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
-                        k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
                         for (int r = 0; r < D; r++) {
                             const int j = g | dep_slot(r, M);
                             k << "          v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
@@ -245,6 +255,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         k << "        }\n";
                         continue;
                     }
+                    k << "        {";
+                    for (int cc = 0; cc < D; cc++) k << " const double2 i" << cc << " = v" << (g | dep_slot(cc, M)) << ";";
+                    k << "\n";
                     for (int r = 0; r < D; r++) {
                         k << "          { double ax = 0.0, ay = 0.0;";
                         for (int cc = 0; cc < D; cc++) {

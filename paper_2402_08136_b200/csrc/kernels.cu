@@ -187,6 +187,15 @@ __global__ void __launch_bounds__(kThreads) k_product(const ProductArgs a) {
                 }
                 amp = c == 0 ? __ldg(&a.tab[c][idx]) : cmul(amp, __ldg(&a.tab[c][idx]));
             }
+            for (int d = 0; d < a.ndiag; d++) {
+                uint32_t idx = 0;
+                if (a.dcontig[d]) {
+                    idx = (uint32_t)((gi >> a.dbits[d][0]) & ((1ull << a.dn[d]) - 1ull));
+                } else {
+                    for (int j = 0; j < a.dn[d]; j++) idx |= (uint32_t)((gi >> a.dbits[d][j]) & 1ull) << j;
+                }
+                amp = cmul(__ldg(&a.dtab[d][idx]), amp);
+            }
         }
         a.psi[i] = amp;
     }

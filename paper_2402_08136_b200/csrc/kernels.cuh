@@ -61,6 +61,11 @@ struct ProductArgs {             // a3: product-state initialisation (prep + H l
     int cn[4];
     int ccontig[4];              // chunk bits contiguous: lo = cbits[c][0]
     const double2 *tab[4];       // chunk tables (2^cn entries)
+    int ndiag;                   // diagonal gates folded after the product state (SURVEY f2 phase tables)
+    int dbits[8][12];            // global-index bits of diagonal d, table bit j
+    int dn[8];
+    int dcontig[8];
+    const double2 *dtab[8];
 };
 
 // Tile pass v2: a CTA holds 2^T amplitudes of one tile in shared memory

@@ -79,6 +79,7 @@ std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o);
 struct ProductFactor {
     std::vector<int> qubits;      // logical qubits, qubits[0] = LSB of the factor index
     std::vector<cplx> vec;        // 2^|qubits| amplitudes (= column 0 of the factor's matrix)
+    bool diag = false;            // a diagonal gate applied after the product state (vec = its table)
 };
 size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors);
 
