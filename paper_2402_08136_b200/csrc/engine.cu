@@ -144,75 +144,99 @@ static int index_in(const std::vector<int> &v, int x) {
     return it == v.end() ? -1 : (int)(it - v.begin());
 }
 
+// Product-state init (+ folded leading diagonals): every factor is a table over its own bits;
+// factors are grouped into <= 4 group tables of <= 14 index bits (L2-resident), each entry the
+// product of its members, so the init kernel does <= 4 lookups and 3 complex products per amplitude.
 static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec) {
-    // group factors (physical bits) into <= 4 chunks of <= 12 bits, each a tensor-product table
-    std::vector<const ProductFactor *> fs, ds;
-    for (auto &f : st.factors) (f.diag ? ds : fs).push_back(&f);
+    std::vector<const ProductFactor *> fs;
+    for (auto &f : st.factors)
+        if (!f.diag) fs.push_back(&f);
     std::sort(fs.begin(), fs.end(), [](const ProductFactor *a, const ProductFactor *b) {
         return *std::min_element(a->qubits.begin(), a->qubits.end()) <
                *std::min_element(b->qubits.begin(), b->qubits.end());
     });
-    std::vector<std::vector<int>> cb;
-    std::vector<std::vector<cplx>> ct;
+    for (auto &f : st.factors)
+        if (f.diag) fs.push_back(&f);
     uint64_t covered = 0;
-    for (const ProductFactor *f : fs) {
-        if (cb.empty() || cb.back().size() + f->qubits.size() > 12) {
-            cb.emplace_back();
-            ct.push_back({cplx(1.0, 0.0)});
+    for (auto *f : fs)
+        if (!f->diag)
+            for (int q : f->qubits) covered |= 1ull << q;
+    struct Group {
+        std::vector<int> bits;
+        std::vector<const ProductFactor *> mem;
+    };
+    std::vector<Group> groups;
+    for (auto *f : fs) {
+        int best = -1, best_ov = -1;
+        size_t best_u = 0;
+        for (size_t gi = 0; gi < groups.size(); gi++) {
+            std::vector<int> u = groups[gi].bits;
+            int ov = 0;
+            for (int q : f->qubits) {
+                if (std::find(u.begin(), u.end(), q) == u.end()) u.push_back(q);
+                else ov++;
+            }
+            if (u.size() > 14) continue;
+            if (ov > best_ov || (ov == best_ov && u.size() < best_u)) {
+                best = (int)gi;
+                best_ov = ov;
+                best_u = u.size();
+            }
         }
-        auto &bits = cb.back();
-        auto &tab = ct.back();
-        const size_t lo = tab.size();
-        std::vector<cplx> nt(lo * f->vec.size());
-        for (size_t x = 0; x < nt.size(); x++) nt[x] = tab[x % lo] * f->vec[x / lo];
-        tab.swap(nt);
-        for (int q : f->qubits) {
-            bits.push_back(q);
-            covered |= 1ull << q;
+        if (best < 0) {
+            if (groups.size() == 4) fail(SV_E_ARG, "product initialisation needs more than 4 group tables");
+            groups.push_back({});
+            best = (int)groups.size() - 1;
         }
+        for (int q : f->qubits)
+            if (std::find(groups[best].bits.begin(), groups[best].bits.end(), q) == groups[best].bits.end())
+                groups[best].bits.push_back(q);
+        groups[best].mem.push_back(f);
     }
-    if (cb.size() > 4) fail(SV_E_ARG, "product initialisation needs more than 4 chunks");
     dev::ProductArgs &a = rec.prod;
     a.psi = sv->psi;
     a.n_amps = sv->local_amps();
     a.rank_base = (uint64_t)sv->rank << sv->nloc;
     const uint64_t all = sv->n >= 64 ? ~0ull : ((1ull << sv->n) - 1ull);
     a.zero_mask = all & ~covered;
-    a.nchunks = (int)cb.size();
-    for (size_t c = 0; c < cb.size(); c++) {
-        a.cn[c] = (int)cb[c].size();
-        bool contig = true;
-        for (size_t j = 0; j < cb[c].size(); j++) {
-            a.cbits[c][j] = cb[c][j];
-            if (cb[c][j] != cb[c][0] + (int)j) contig = false;
+    a.ngroups = (int)groups.size();
+    for (size_t gi = 0; gi < groups.size(); gi++) {
+        Group &G = groups[gi];
+        std::sort(G.bits.begin(), G.bits.end());
+        const size_t nb = G.bits.size();
+        std::vector<cplx> tab((size_t)1 << nb);
+        std::vector<std::vector<int>> pos(G.mem.size());
+        for (size_t m = 0; m < G.mem.size(); m++)
+            for (int q : G.mem[m]->qubits)
+                pos[m].push_back((int)(std::find(G.bits.begin(), G.bits.end(), q) - G.bits.begin()));
+        for (size_t x = 0; x < tab.size(); x++) {
+            cplx v(1.0, 0.0);
+            for (size_t m = 0; m < G.mem.size(); m++) {
+                size_t idx = 0;
+                for (size_t j = 0; j < pos[m].size(); j++)
+                    if ((x >> pos[m][j]) & 1) idx |= (size_t)1 << j;
+                v *= G.mem[m]->vec[idx];
+            }
+            tab[x] = v;
         }
-        a.ccontig[c] = contig;
-        double2 *d = nullptr;
-        cuda_check(cudaMalloc(&d, sizeof(double2) * ct[c].size()), "cudaMalloc(product table)");
-        cuda_check(cudaMemcpy(d, ct[c].data(), sizeof(double2) * ct[c].size(), cudaMemcpyHostToDevice),
-                   "upload product table");
-        p->d_tabs.push_back(d);
-        p->h2d_bytes += sizeof(double2) * ct[c].size();
-        a.tab[c] = d;
-    }
-    if (ds.size() > 8) fail(SV_E_ARG, "too many folded diagonals");
-    a.ndiag = (int)ds.size();
-    for (size_t k = 0; k < ds.size(); k++) {
-        const ProductFactor &f = *ds[k];
-        a.dn[k] = (int)f.qubits.size();
-        bool contig = true;
-        for (size_t j = 0; j < f.qubits.size(); j++) {
-            a.dbits[k][j] = f.qubits[j];
-            if (f.qubits[j] != f.qubits[0] + (int)j) contig = false;
+        int nr = 0;   // runs of consecutive bits
+        for (size_t j = 0; j < nb; j++) {
+            if (nr > 0 && G.bits[j] == a.rsrc[gi][nr - 1] + a.rlen[gi][nr - 1]) {
+                a.rlen[gi][nr - 1]++;
+                continue;
+            }
+            a.rsrc[gi][nr] = (uint8_t)G.bits[j];
+            a.rdst[gi][nr] = (uint8_t)j;
+            a.rlen[gi][nr] = 1;
+            nr++;
         }
-        a.dcontig[k] = contig;
+        a.nruns[gi] = nr;
         double2 *d = nullptr;
-        cuda_check(cudaMalloc(&d, sizeof(double2) * f.vec.size()), "cudaMalloc(init diagonal)");
-        cuda_check(cudaMemcpy(d, f.vec.data(), sizeof(double2) * f.vec.size(), cudaMemcpyHostToDevice),
-                   "upload init diagonal");
+        cuda_check(cudaMalloc(&d, sizeof(double2) * tab.size()), "cudaMalloc(init table)");
+        cuda_check(cudaMemcpy(d, tab.data(), sizeof(double2) * tab.size(), cudaMemcpyHostToDevice), "upload init table");
         p->d_tabs.push_back(d);
-        p->h2d_bytes += sizeof(double2) * f.vec.size();
-        a.dtab[k] = d;
+        p->h2d_bytes += sizeof(double2) * tab.size();
+        a.tab[gi] = d;
     }
 }
 

@@ -11,6 +11,8 @@
 // (in-process, keyed by the exact source text).
 #include <dlfcn.h>
 
+#include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -342,6 +344,18 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     std::vector<char> cubin(cs);
     n.cubin(prog, cubin.data());
     n.destroy(&prog);
+    if (const char *dir = getenv("HHLSV_JIT_DUMP")) {      // developer aid: keep source + cubin
+        static std::atomic<int> seq{0};
+        const std::string stem = std::string(dir) + "/pass" + std::to_string(seq++);
+        if (FILE *f = fopen((stem + ".cu").c_str(), "w")) {
+            fwrite(full.data(), 1, full.size(), f);
+            fclose(f);
+        }
+        if (FILE *f = fopen((stem + ".cubin").c_str(), "wb")) {
+            fwrite(cubin.data(), 1, cubin.size(), f);
+            fclose(f);
+        }
+    }
     return cubin;
 }
 }  // namespace

@@ -178,23 +178,11 @@ __global__ void __launch_bounds__(kThreads) k_product(const ProductArgs a) {
         double2 amp = make_double2(0.0, 0.0);
         if (!(gi & a.zero_mask)) {
             amp = make_double2(1.0, 0.0);
-            for (int c = 0; c < a.nchunks; c++) {
+            for (int g = 0; g < a.ngroups; g++) {
                 uint32_t idx = 0;
-                if (a.ccontig[c]) {
-                    idx = (uint32_t)((gi >> a.cbits[c][0]) & ((1ull << a.cn[c]) - 1ull));
-                } else {
-                    for (int j = 0; j < a.cn[c]; j++) idx |= (uint32_t)((gi >> a.cbits[c][j]) & 1ull) << j;
-                }
-                amp = c == 0 ? __ldg(&a.tab[c][idx]) : cmul(amp, __ldg(&a.tab[c][idx]));
-            }
-            for (int d = 0; d < a.ndiag; d++) {
-                uint32_t idx = 0;
-                if (a.dcontig[d]) {
-                    idx = (uint32_t)((gi >> a.dbits[d][0]) & ((1ull << a.dn[d]) - 1ull));
-                } else {
-                    for (int j = 0; j < a.dn[d]; j++) idx |= (uint32_t)((gi >> a.dbits[d][j]) & 1ull) << j;
-                }
-                amp = cmul(__ldg(&a.dtab[d][idx]), amp);
+                for (int r = 0; r < a.nruns[g]; r++)
+                    idx |= (uint32_t)((gi >> a.rsrc[g][r]) & ((1ull << a.rlen[g][r]) - 1ull)) << a.rdst[g][r];
+                amp = g == 0 ? __ldg(&a.tab[g][idx]) : cmul(amp, __ldg(&a.tab[g][idx]));
             }
         }
         a.psi[i] = amp;

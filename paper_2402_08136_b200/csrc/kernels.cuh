@@ -51,21 +51,15 @@ struct RecipArgs {               // a7: eigenvalue-inversion RY, multiplexed by 
     uint64_t lmask;
 };
 
-struct ProductArgs {             // a3: product-state initialisation (prep + H layer folded)
+struct ProductArgs {             // a3: product-state initialisation (+ folded leading diagonals)
     double2 *psi;
     uint64_t n_amps;
     uint64_t rank_base;          // rank << nloc (global index of local 0)
-    uint64_t zero_mask;          // global-index bits that must be 0 (uncovered qubits)
-    int nchunks;
-    int cbits[4][16];            // physical (global-index) bits of chunk c, table bit j
-    int cn[4];
-    int ccontig[4];              // chunk bits contiguous: lo = cbits[c][0]
-    const double2 *tab[4];       // chunk tables (2^cn entries)
-    int ndiag;                   // diagonal gates folded after the product state (SURVEY f2 phase tables)
-    int dbits[8][12];            // global-index bits of diagonal d, table bit j
-    int dn[8];
-    int dcontig[8];
-    const double2 *dtab[8];
+    uint64_t zero_mask;          // global-index bits that must be 0 (qubits no product factor covers)
+    int ngroups;                 // amplitude = prod_g tab_g[index_g(global index)]
+    int nruns[4];                // index_g = OR over runs of ((gi >> src) & (2^len - 1)) << dst
+    uint8_t rsrc[4][16], rlen[4][16], rdst[4][16];
+    const double2 *tab[4];       // group tables (<= 2^14 entries, L2-resident)
 };
 
 // Tile pass v2: a CTA holds 2^T amplitudes of one tile in shared memory
