@@ -206,6 +206,7 @@ typedef struct {
     double recip_snap;  /* reciprocal snapping tolerance (qlsarepo: 1e-5); < 0 -> default 1e-5 */
     int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; -1: don't */
     int tile_jit;       /* as sv_fuse_options.tile_jit */
+    int diag_kmax;      /* max qubits of a fused diagonal (0 -> 12 for HHL programs) */
     int qpe_mode;       /* 0: textbook circuit (c-U^(2^j) blocks, Fig. 5); 1: eigenbasis rewrite:
                            c-U_j = V diag(e^{2 pi i frac(2^j phi_s)}) V^T, so the controlled chain becomes
                            V^T, <= 12-qubit diagonal phase tables over (system, clock chunk), V — the same

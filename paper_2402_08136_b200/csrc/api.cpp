@@ -328,6 +328,8 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     FuseOptions fo;
     if (opt && opt->fusion_kmax != 0) fo.kmax = opt->fusion_kmax < 0 ? 0 : opt->fusion_kmax;
     if (fo.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
+    fo.diag_kmax = 12;
+    if (opt && opt->diag_kmax > 0) fo.diag_kmax = std::min(12, opt->diag_kmax);
     std::vector<Gate> fused = fuse(rest, fo);
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;

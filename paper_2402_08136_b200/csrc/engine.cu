@@ -514,7 +514,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
                     JitPass jp;
                     jp.name = "hhlsv_tile";
-                    jp.src = gen_tile_kernel(jp.name, a, lph, lops);
+                    jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra);
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
                 }

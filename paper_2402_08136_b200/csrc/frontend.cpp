@@ -256,9 +256,12 @@ static void append_qft(std::vector<Gate> &out, const std::vector<int> &q, bool i
 // Eigenbasis form of the controlled-evolution chain:
 //   prod_j c-U_j = (V (x) I) D (V^T (x) I),  D[s, m] = exp(2 pi i sum_j m_j frac(2^j phi_s)),
 // emitted as V^T on the system register, then one diagonal table per chunk of clock bits
-// (system qubits + <= 12 - n_b clock qubits), then V. conj = the inverse chain.
+// (system qubits + up to 4 clock qubits). The inverse chain is D^dagger then V.
 static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const std::vector<int> &sys,
                                const std::vector<int> &clk, bool inverse) {
+    // forward chain: V^T, D ; inverse chain: D^dagger, V. The V closing the forward chain and the
+    // V^T opening the inverse chain cancel (V V^T = I): everything between them (IQFT, RECIP_RY,
+    // QFT) acts on clock/ancilla qubits only and commutes with V (x) I.
     const int N = p.N, nb = p.n_b, nc = p.n_c;
     auto dense_V = [&](bool transpose) {
         Gate v;
@@ -294,9 +297,9 @@ static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const
             }
         diags.push_back(std::move(d));
     }
-    g.push_back(dense_V(true));            // V^T
+    if (!inverse) g.push_back(dense_V(true));            // V^T
     for (auto &d : diags) g.push_back(std::move(d));
-    g.push_back(dense_V(false));           // V
+    if (inverse) g.push_back(dense_V(false));            // V
 }
 
 std::vector<Gate> hhl_build(const HHLPlanHost &p, int qpe_mode) {

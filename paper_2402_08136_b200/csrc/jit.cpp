@@ -144,7 +144,7 @@ bool jit_available(std::string *why) {
 
 // ---------------------------------------------------------------- codegen ----
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
-                            const std::vector<dev::RegOp> &ops) {
+                            const std::vector<dev::RegOp> &ops, size_t *smem_extra) {
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
@@ -152,8 +152,23 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     for (auto &op : ops)
         if (op.kind == 0 && ((op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1)) >= 3)
             wide_ops++;
+    // wide-op matrices staged once per (persistent) CTA in shared memory when few (<= 4 x 4 KB)
+    std::map<int, size_t> wstage;      // op index -> offset (double2 units) in the staging region
+    size_t wtot = 0;
+    if (wide_ops <= 4)
+        for (size_t i = 0; i < ops.size(); i++) {
+            const auto &op = ops[i];
+            const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            if (op.kind == 0 && Kk >= 3) {
+                wstage[(int)i] = wtot;
+                wtot += (size_t)1 << (2 * Kk);
+            }
+        }
+    if (smem_extra) *smem_extra = wtot * sizeof(double2);
     std::ostringstream k;
-    k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ") " << name
+    const size_t smem_cta = 2 * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16;
+    const int min_blocks = std::max(1, std::min(4, (int)((227 * 1024) / smem_cta)));
+    k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
@@ -165,6 +180,15 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     k << "  for (int u = threadIdx.x; u < " << (1 << SB) << "; u += " << NTHR << ") { u64 d = 0;";
     for (int i = 0; i < SB; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[SA + i] << ";";
     k << " depB[u] = d; }\n";
+    if (wtot) {
+        k << "  double2 *wm = reinterpret_cast<double2 *>(depB + " << (1 << SB) << ");\n";
+        for (auto &kv : wstage) {
+            const auto &op = ops[kv.first];
+            const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            k << "  for (int i = threadIdx.x; i < " << (1 << (2 * Kk)) << "; i += " << NTHR << ") wm[" << kv.second
+              << " + i] = blob[" << op.data_off << "ull + i];\n";
+        }
+    }
     k << "  auto tile_base = [](u64 t) { u64 b = t;";
     for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
     k << " return b; };\n";
@@ -238,17 +262,41 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             }
                             return o.str();
                         };
+                        auto row_s = [&](const std::string &Ur) {      // matrix row in shared memory
+                            std::ostringstream o;
+                            for (int cc = 0; cc < D; cc++) {
+                                const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
+                                if (real)
+                                    o << " { const double w = " << Ur << "[" << cc << "].x; ax = fma(w, " << in
+                                      << ".x, ax); ay = fma(w, " << in << ".y, ay); }";
+                                else
+                                    o << " { const double2 w = " << Ur << "[" << cc << "]; ax = fma(w.x, " << in
+                                      << ".x, ax); ax = fma(-w.y, " << in << ".y, ax); ay = fma(w.x, " << in
+                                      << ".y, ay); ay = fma(w.y, " << in << ".x, ay); }";
+                            }
+                            return o.str();
+                        };
                         k << "        {\n";
-                        if (wide_ops > 4) {
+                        auto ws0 = wstage.find(oi);
+                        if (true) {   // rolled row loop: bounded registers (inputs stay in v) and code size
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
-                              << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = U + r * " << D << ";" << row("Ur")
+                              << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = "
+                              << (ws0 != wstage.end() ? "wm + " + std::to_string(ws0->second) : std::string("U"))
+                              << " + r * " << D << ";" << (ws0 != wstage.end() ? row_s("Ur") : row("Ur"))
                               << " const u32 slot = " << rd[g] << "u";
                             for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
                             k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
                         } else {
-                            for (int r = 0; r < D; r++)
-                                k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
-                                  << row("Ur") << " cur[swz(tb | " << rd[g | dep_slot(r, M)] << "u)] = mk(ax, ay); }\n";
+                            auto ws = wstage.find(oi);
+                            for (int r = 0; r < D; r++) {
+                                if (ws != wstage.end())
+                                    k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = wm + " << ws->second + r * D
+                                      << ";" << row_s("Ur");
+                                else
+                                    k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
+                                      << row("Ur");
+                                k << " cur[swz(tb | " << rd[g | dep_slot(r, M)] << "u)] = mk(ax, ay); }\n";
+                            }
                         }
                         for (int r = 0; r < D; r++) {
                             const int j = g | dep_slot(r, M);
@@ -407,11 +455,15 @@ void jit_build(std::vector<JitPass> &passes) {
     }
 }
 
+size_t jit_smem_bytes(int T, size_t extra) {
+    const int SA = (T + 1) / 2, SB = T - SA;
+    return 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB)) + extra;
+}
+
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
                        int T, cudaStream_t s) {
     const int threads = 1 << (T - dev::kRegBits);
-    const int SA = (T + 1) / 2, SB = T - SA;
-    const size_t smem = 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB));
+    const size_t smem = jit_smem_bytes(T, p.smem_extra);
     const void *f = reinterpret_cast<const void *>(p.kern);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -13,14 +13,16 @@ struct JitPass {
     std::string name;
     std::string src;
     cudaKernel_t kern = nullptr;
+    size_t smem_extra = 0;     // bytes of staged wide-op matrices after the dep tables
 };
 
 bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
-                            const std::vector<dev::RegOp> &ops);
+                            const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
                        int T, cudaStream_t s);
+size_t jit_smem_bytes(int T, size_t extra);
 
 }  // namespace hhlsv

@@ -54,7 +54,7 @@ class sv_plan_report(ctypes.Structure):
 class hhl_options(ctypes.Structure):
     _fields_ = [("clock_qubits", ctypes.c_int), ("fusion_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
                 ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("tile_jit", ctypes.c_int),
-                ("qpe_mode", ctypes.c_int)]
+                ("diag_kmax", ctypes.c_int), ("qpe_mode", ctypes.c_int)]
 
 
 class hhl_report(ctypes.Structure):
@@ -351,9 +351,10 @@ def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax
     return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
 
 
-def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0, qpe_mode=0):
+def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0, diag_kmax=0,
+          qpe_mode=0):
     return hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap), int(init_fold),
-                       int(tile_jit), int(qpe_mode))
+                       int(tile_jit), int(diag_kmax), int(qpe_mode))
 
 
 def hhl_plan_size(A, b, **kw):
