@@ -415,7 +415,8 @@ static std::vector<cplx> embed_dense(const std::vector<cplx> &m, const std::vect
                                      const std::vector<int> &u);
 
 // ------------------------------------------------------------ product fold ----
-size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors) {
+size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors,
+                           bool fold_diagonals) {
     std::vector<char> touched(n, 0);
     const bool diag_phase = false;
     factors.clear();
@@ -452,7 +453,7 @@ size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<Pr
         factors.push_back(std::move(f));
     }
     // diagonal gates right after the product state: folded as per-amplitude phase tables
-    for (; i < gates.size(); i++) {
+    for (; fold_diagonals && i < gates.size(); i++) {
         const Gate &g = gates[i];
         if (g.kind != Kind::Diagonal || g.targets.size() > 12) break;
         size_t nd = 0;

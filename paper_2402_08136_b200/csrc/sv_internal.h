@@ -81,7 +81,8 @@ struct ProductFactor {
     std::vector<cplx> vec;        // 2^|qubits| amplitudes (= column 0 of the factor's matrix)
     bool diag = false;            // a diagonal gate applied after the product state (vec = its table)
 };
-size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors);
+size_t fold_product_prefix(const std::vector<Gate> &gates, int n, std::vector<ProductFactor> &factors,
+                           bool fold_diagonals = true);
 
 // ---------------------------------------------------------------- program ----
 enum class StepKind : int { InitZero, InitProduct, Dense, Diagonal, RecipRY, Tile, Exchange };

@@ -20,14 +20,15 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--qpe", type=int, nargs="+", default=[0])
 ap.add_argument("--jit", type=int, nargs="+", default=[0])
 ap.add_argument("--dk", type=int, nargs="+", default=[0])
+ap.add_argument("--fold", type=int, nargs="+", default=[0])
 ap.add_argument("--verbose", action="store_true")
 a = ap.parse_args()
 A, b, nc = configs.get(a.config)
 st = pkg.State(configs.n_qubits(a.config))
 import itertools  # noqa: E402
-for q, k, T, J, DK in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk):
+for q, k, T, J, DK, FO in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk, a.fold):
     if True:
-        prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=k, tile_qubits=T, qpe_mode=q, tile_jit=J, diag_kmax=DK)
+        prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=k, tile_qubits=T, qpe_mode=q, tile_jit=J, diag_kmax=DK, init_fold=FO)
         prog.set_timing(True)
         for _ in range(a.reps):
             prog.run()
@@ -36,7 +37,7 @@ for q, k, T, J, DK in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk):
         heads = [ln for ln in dump if not ln.startswith("  ")]
         total = sum(x[0] for x in t)
         import time as _t
-        print(f"== {a.config} qpe={q} kmax={k} tile={T} jit={J} dk={DK}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
+        print(f"== {a.config} qpe={q} kmax={k} tile={T} jit={J} dk={DK} fold={FO}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
               f"total {total:.1f} ms")
         if a.verbose:
             for (ms, kind, by, la), h in zip(t, heads):
