@@ -102,6 +102,24 @@ def _local_gate(g, tg, cb, nloc, rank):
     raise ValueError(g["kind"])
 
 
+def _recip_local(psi, nloc, rank, g, anc, clock):
+    """Reciprocal RY on a shard: ancilla local, clock bits local or global (value from the rank)."""
+    assert anc < nloc
+    nc = len(clock)
+    for i0 in range(1 << nloc):
+        if (i0 >> anc) & 1:
+            continue
+        m = 0
+        for j, b in enumerate(clock):
+            bit = ((rank >> (b - nloc)) & 1) if b >= nloc else ((i0 >> b) & 1)
+            m |= bit << j
+        sv = sim.recip_s(m, nc, g["delta"], g.get("signed", 1), g.get("snap", 0.0))
+        th = 2 * np.arcsin(sv)
+        c, s = np.cos(th / 2), np.sin(th / 2)
+        x0, x1 = psi[i0], psi[i0 | (1 << anc)]
+        psi[i0], psi[i0 | (1 << anc)] = c * x0 - s * x1, s * x0 + c * x1
+
+
 def _worker(rank, world, port, n, gates, fk, tile, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -133,7 +151,8 @@ def _worker(rank, world, port, n, gates, fk, tile, out_q):
             gate = next(it)
             tg, cb = _phys_bits(st[1])
             if gate["kind"] == "recip_ry":
-                raise AssertionError("recip_ry not used in this emulation")
+                _recip_local(psi, nloc, rank, gate, tg[0], cb)
+                continue
             lg = _local_gate(gate, tg, cb, nloc, rank)
             if lg is None:
                 continue
@@ -174,11 +193,6 @@ def _run(n, gates, world, fk=0, tile=-1):
     return logical
 
 
-def _strip(gates):
-    """The emulation maps dump lines 1:1 to gates: no fusion, no recip (rank-split m is tested on GPU)."""
-    return [g for g in gates if g["kind"] != "recip_ry"]
-
-
 @pytest.mark.parametrize("world", [2, 4])
 def test_random_circuit_sharded_gloo(world):
     n = 7
@@ -188,11 +202,14 @@ def test_random_circuit_sharded_gloo(world):
     assert np.abs(got - ref).max() < 1e-12
 
 
-def test_hhl_circuit_sharded_gloo():
-    """The C2 HHL gate list (9 qubits, clock MSBs global on 2 ranks) minus the reciprocal rotation."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_hhl_circuit_sharded_gloo(world):
+    """The whole C2 HHL gate list (9 qubits): on 2 ranks the ancilla is global (the reciprocal
+    rotation forces an exchange), on 4 ranks also the clock MSB (its H gates force exchanges;
+    its c-U control and the CP phases resolve per rank)."""
     A, b, nc = configs.get("C2")
     p = ohhl.plan(A, b, nc)
-    gates = _strip(ohhl.build(p))
-    got = _run(p.n, gates, 2)
+    gates = ohhl.build(p)
+    got = _run(p.n, gates, world)
     ref = sim.run(gates, p.n)
     assert np.abs(got - ref).max() < 1e-12
