@@ -59,7 +59,10 @@ typedef struct sv_state sv_state;   /* opaque; library-owned until sv_destroy */
  * sharded by its top log2(world) PHYSICAL qubits; rank r holds the 2^(n-g) amplitudes
  * whose top g physical bits equal r. `nccl_id` points at the 128-byte ncclUniqueId
  * that rank 0 created with sv_nccl_unique_id() and broadcast to all ranks (e.g. with
- * torch.distributed). world must be a power of two. NULL dist = 1 GPU, no NCCL. */
+ * torch.distributed). world must be a power of two. NULL dist = 1 GPU, no NCCL.
+ * world > 1 with nccl_id == NULL creates VIRTUAL shards: all `world` shards live in this process
+ * on one GPU and global-qubit exchanges are device copies — the same scheduler, rank-resolved
+ * kernels and exchange packing as the NCCL path, testable on a single GPU. */
 typedef struct {
     int world;
     int rank;

@@ -32,8 +32,8 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
         device = dist->device;
         if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world)
             fail(SV_E_ARG, "sv_dist: world must be a power of two and 0 <= rank < world");
-        if (world > 1 && !dist->nccl_id) fail(SV_E_ARG, "sv_dist: nccl_id required for world > 1");
     }
+    const bool virt = world > 1 && !dist->nccl_id;
     int g = 0;
     while ((1 << g) < world) g++;
     if (n < 1 || n - g < 1 || n > 62) fail(SV_E_ARG, "n_qubits out of range");
@@ -52,12 +52,34 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
     const size_t bytes = sizeof(double2) << sv->nloc;
     size_t freeb = 0, totb = 0;
     cuda_check(cudaMemGetInfo(&freeb, &totb), "cudaMemGetInfo");
-    if (bytes > freeb) fail(SV_E_OOM, "state does not fit in device memory");
-    cuda_check(cudaMalloc(&sv->psi, bytes), "cudaMalloc(state)");
+    if (bytes * (virt ? world : 1) > freeb) fail(SV_E_OOM, "state does not fit in device memory");
+    if (virt) {
+        sv->vworld = world;
+        sv->world = 1;
+        for (int r = 0; r < world; r++) {
+            std::unique_ptr<sv_state> v(new sv_state());
+            v->n = n;
+            v->g = g;
+            v->nloc = n - g;
+            v->world = 1;
+            v->rank = r;
+            v->device = device;
+            v->stream = stream;
+            v->phys = sv->phys;
+            cuda_check(cudaMalloc(&v->psi, bytes), "cudaMalloc(virtual shard)");
+            v->red_len = dev::kRedBlocks;
+            cuda_check(cudaMalloc(&v->d_red, sizeof(double) * v->red_len), "cudaMalloc(red)");
+            cuda_check(cudaMalloc(&v->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
+            sv->views.push_back(v.release());
+        }
+        sv->psi = sv->views[0]->psi;
+    } else {
+        cuda_check(cudaMalloc(&sv->psi, bytes), "cudaMalloc(state)");
+    }
     sv->red_len = dev::kRedBlocks;
     cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * sv->red_len), "cudaMalloc(red)");
     cuda_check(cudaMalloc(&sv->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
-    if (world > 1) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
+    if (world > 1 && !virt) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
     state_reset(sv.get());
     return sv.release();
 }
@@ -65,6 +87,11 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
 void state_destroy(sv_state *sv) {
     if (!sv) return;
     cudaStreamSynchronize(sv->stream);
+    if (sv->vworld > 1) {
+        for (auto *v : sv->views) state_destroy(v);
+        sv->views.clear();
+        sv->psi = nullptr;
+    }
     cudaFree(sv->psi);
     cudaFree(sv->d_red);
     cudaFree(sv->d_scalar);
@@ -77,6 +104,10 @@ void state_destroy(sv_state *sv) {
 
 void state_reset(sv_state *sv) {
     std::iota(sv->phys.begin(), sv->phys.end(), 0);
+    if (sv->vworld > 1) {
+        for (auto *v : sv->views) state_reset(v);
+        return;
+    }
     cuda_check(dev::launch_zero_init(sv->psi, sv->local_amps(), sv->rank == 0, sv->stream), "init zero");
 }
 
@@ -135,6 +166,34 @@ static void exchange(sv_state *sv, int gbit, int lbit) {
                        "exchange copy");
         else
             cuda_check(dev::launch_unpack(sv->psi, sv->d_xrecv, lbit, val, off, cnt, sv->stream), "unpack");
+    }
+}
+
+// Virtual sharding: the same exchange between in-process shards (pack both halves, swap).
+static void virtual_exchange(sv_state *sv, int gbit, int lbit) {
+    const int gb = gbit - sv->nloc;
+    const uint64_t half = sv->local_amps() >> 1;
+    const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);
+    if (sv->x_len < chunk) {
+        cudaFree(sv->d_xsend);
+        cudaFree(sv->d_xrecv);
+        sv->d_xsend = sv->d_xrecv = nullptr;
+        cuda_check(cudaMalloc(&sv->d_xsend, sizeof(double2) * chunk), "cudaMalloc(xsend)");
+        cuda_check(cudaMalloc(&sv->d_xrecv, sizeof(double2) * chunk), "cudaMalloc(xrecv)");
+        sv->x_len = chunk;
+    }
+    for (int r = 0; r < sv->vworld; r++) {
+        const int q = r ^ (1 << gb);
+        if (q < r) continue;
+        sv_state *A = sv->views[r], *B = sv->views[q];
+        const int va = 1 - ((r >> gb) & 1), vb = 1 - ((q >> gb) & 1);
+        for (uint64_t off = 0; off < half; off += chunk) {
+            const uint64_t cnt = std::min(chunk, half - off);
+            cuda_check(dev::launch_pack(A->psi, sv->d_xsend, lbit, va, off, cnt, sv->stream), "vpack");
+            cuda_check(dev::launch_pack(B->psi, sv->d_xrecv, lbit, vb, off, cnt, sv->stream), "vpack");
+            cuda_check(dev::launch_unpack(A->psi, sv->d_xrecv, lbit, va, off, cnt, sv->stream), "vunpack");
+            cuda_check(dev::launch_unpack(B->psi, sv->d_xsend, lbit, vb, off, cnt, sv->stream), "vunpack");
+        }
     }
 }
 
@@ -376,6 +435,24 @@ void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blo
 
 sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,
                            const CompileOptions &co, uint64_t n_logical) {
+    if (sv->vworld > 1) {
+        std::unique_ptr<sv_program> p(new sv_program());
+        p->sv = sv;
+        p->n_logical = n_logical;
+        p->resets = init != nullptr;
+        p->phys_in = p->resets ? std::vector<int>() : sv->phys;
+        try {
+            for (auto *v : sv->views) {
+                v->phys = sv->phys;
+                p->subs.push_back(program_create(v, ops, init, co, n_logical));
+            }
+        } catch (...) {
+            for (auto *q : p->subs) program_destroy(q);
+            throw;
+        }
+        p->sched = p->subs[0]->sched;
+        return p.release();
+    }
     std::unique_ptr<sv_program> p(new sv_program());
     p->sv = sv;
     p->n_logical = n_logical;
@@ -576,9 +653,42 @@ uint64_t sv_program::launches() const {
 
 namespace hhlsv {
 
+static void launch_rec(sv_state *sv, sv_program *p, const LaunchRec &r) {
+    if (r.skip) return;
+    switch (r.kind) {
+        case StepKind::InitZero: cuda_check(dev::launch_zero_init(sv->psi, sv->local_amps(), sv->rank == 0, sv->stream), "init"); break;
+        case StepKind::InitProduct: cuda_check(dev::launch_product(r.prod, sv->stream), "product init"); break;
+        case StepKind::Dense: cuda_check(dev::launch_dense(r.dense, sv->stream), "dense"); break;
+        case StepKind::Diagonal: cuda_check(dev::launch_diag(r.diag, sv->stream), "diagonal"); break;
+        case StepKind::RecipRY: cuda_check(dev::launch_recip(r.recip, sv->stream), "recip_ry"); break;
+        case StepKind::Tile:
+            if (r.jit >= 0)
+                cuda_check(jit_launch(p->jit[r.jit], r.tile.psi, r.tile.blob, r.tile.n_tiles, r.tile.rank_base, r.tile.T,
+                                      sv->stream),
+                           "tile (jit)");
+            else
+                cuda_check(dev::launch_tile(r.tile, sv->stream), "tile");
+            break;
+        case StepKind::Exchange: break;
+    }
+}
+
 void program_run(sv_state *sv, sv_program *p) {
     if (p->sv != sv) fail(SV_E_ARG, "program belongs to another state");
     if (!p->resets && sv->phys != p->phys_in) fail(SV_E_ARG, "qubit map changed since the program was created");
+    if (!p->subs.empty()) {             // virtual sharding: step-interleaved over the shards
+        const size_t ns = p->subs[0]->recs.size();
+        for (size_t i = 0; i < ns; i++) {
+            if (p->subs[0]->recs[i].kind == StepKind::Exchange) {
+                virtual_exchange(sv, p->subs[0]->recs[i].gbit, p->subs[0]->recs[i].lbit);
+                continue;
+            }
+            for (size_t r = 0; r < p->subs.size(); r++) launch_rec(sv->views[r], p->subs[r], p->subs[r]->recs[i]);
+        }
+        sv->phys = p->sched.phys_out;
+        for (auto *v : sv->views) v->phys = sv->phys;
+        return;
+    }
     if (p->timing && p->ev.size() != 2 * p->recs.size()) {
         for (auto e : p->ev) cudaEventDestroy(e);
         p->ev.assign(2 * p->recs.size(), nullptr);
@@ -630,6 +740,7 @@ void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *la
 void program_destroy(sv_program *p) {
     if (!p) return;
     if (p->sv) cudaStreamSynchronize(p->sv->stream);
+    for (auto *q : p->subs) program_destroy(q);
     cudaFree(p->d_blob);
     cudaFree(p->d_ops);
     cudaFree(p->d_phases);
@@ -644,6 +755,11 @@ static void allreduce_if_sharded(sv_state *sv, double *dbuf, size_t count) {
 }
 
 double state_norm2(sv_state *sv) {
+    if (sv->vworld > 1) {
+        double t = 0.0;
+        for (auto *v : sv->views) t += state_norm2(v);
+        return t;
+    }
     cuda_check(dev::launch_norm2(sv->psi, sv->local_amps(), sv->d_red, sv->d_scalar, sv->stream), "norm2");
     allreduce_if_sharded(sv, sv->d_scalar, 1);
     double h = 0.0;
@@ -654,6 +770,17 @@ double state_norm2(sv_state *sv) {
 
 void state_probabilities(sv_state *sv, const int *qubits, int nq, double *out) {
     if (nq < 0 || nq > 26 || (nq > 0 && !qubits) || !out) fail(SV_E_ARG, "probabilities: bad qubit list");
+    if (sv->vworld > 1) {
+        const size_t nout = (size_t)1 << nq;
+        std::vector<double> part(nout);
+        std::fill(out, out + nout, 0.0);
+        for (auto *v : sv->views) {
+            v->phys = sv->phys;
+            state_probabilities(v, qubits, nq, part.data());
+            for (size_t i = 0; i < nout; i++) out[i] += part[i];
+        }
+        return;
+    }
     std::vector<int> q(qubits, qubits + nq);
     for (int i = 0; i < nq; i++) {
         if (q[i] < 0 || q[i] >= sv->n) fail(SV_E_ARG, "probabilities: qubit out of range");
@@ -706,6 +833,16 @@ void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out) {
     const uint64_t N = 1ull << sv->n;
     if (first > N || count > N - first) fail(SV_E_RANGE, "read: range outside the state");
     if (count && !out) fail(SV_E_ARG, "read: null output");
+    if (sv->vworld > 1) {
+        std::vector<double> part(2 * count);
+        std::fill(out, out + 2 * count, 0.0);
+        for (auto *v : sv->views) {
+            v->phys = sv->phys;
+            state_read(v, first, count, part.data());
+            for (uint64_t i = 0; i < 2 * count; i++) out[i] += part[i];
+        }
+        return;
+    }
     const uint64_t chunk = 1ull << 22;
     ensure_io(sv, std::min(count, chunk));
     for (uint64_t off = 0; off < count; off += chunk) {
@@ -731,6 +868,13 @@ void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in)
     const uint64_t N = 1ull << sv->n;
     if (first > N || count > N - first) fail(SV_E_RANGE, "write: range outside the state");
     if (count && !in) fail(SV_E_ARG, "write: null input");
+    if (sv->vworld > 1) {
+        for (auto *v : sv->views) {
+            v->phys = sv->phys;
+            state_write(v, first, count, in);
+        }
+        return;
+    }
     const uint64_t chunk = 1ull << 22;
     ensure_io(sv, std::min(count, chunk));
     for (uint64_t off = 0; off < count; off += chunk) {
@@ -760,6 +904,21 @@ void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, do
         if (fv[i] != 0 && fv[i] != 1) fail(SV_E_ARG, "postselect: values must be 0/1");
         fmask |= 1ull << fq[i];
         if (fv[i]) fixed |= 1ull << fq[i];
+    }
+    if (sv->vworld > 1) {
+        std::vector<double> part(2 * n_out);
+        std::fill(amps, amps + 2 * n_out, 0.0);
+        for (auto *v : sv->views) {
+            v->phys = sv->phys;
+            state_postselect(v, fq, fv, nfixed, part.data(), idx, n_out, nullptr);
+            for (uint64_t i = 0; i < 2 * n_out; i++) amps[i] += part[i];
+        }
+        if (prob) {
+            double s = 0.0;
+            for (uint64_t e = 0; e < 2 * n_out; e++) s += amps[e] * amps[e];
+            *prob = s;
+        }
+        return;
     }
     dev::GatherArgs a{};
     int nfree = 0;

@@ -27,6 +27,10 @@ struct sv_state {
     double2 *d_xsend = nullptr, *d_xrecv = nullptr;  // exchange buffers
     size_t x_len = 0;
     hhlsv::Comm comm;
+    // virtual sharding (world > 1 without an NCCL id): all shards in this process on one GPU,
+    // one view per virtual rank, exchanges by device copies (tests the rank-dependent paths)
+    int vworld = 1;
+    std::vector<sv_state *> views;
     uint64_t local_amps() const { return 1ull << nloc; }
 };
 
@@ -60,6 +64,7 @@ struct sv_program {
     std::vector<double2 *> d_tabs;    // product-init tables (owned)
     double h2d_bytes = 0;             // uploaded at creation
     std::vector<hhlsv::JitPass> jit;  // specialised tile passes
+    std::vector<sv_program *> subs;   // virtual sharding: one program per view
     bool timing = false;
     std::vector<cudaEvent_t> ev;      // 2 per rec when timing
     uint64_t launches() const;

@@ -270,3 +270,41 @@ def test_s30_engine_parity_oracle_gates(s30_reference):
     sl = st.read(base, 1 << p.n_b)
     assert np.abs(sl - xt).max() < 1e-10
     assert abs(float(np.sum(np.abs(sl) ** 2)) - P) < 1e-12
+
+
+# ------------------------------------------------ virtual shards (multi-GPU logic)
+VMODES = [dict(tile_qubits=-1), dict(tile_qubits=8, tile_jit=-1), dict(tile_qubits=8, tile_jit=1)]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("mode", VMODES)
+def test_virtual_shards_random_circuits(world, mode):
+    """world > 1 without NCCL: the sharded scheduler (exchanges, rank-resolved controls/diagonals),
+    the rank_base paths of every kernel and the pack/unpack exchange, vs the unsharded oracle."""
+    n = 12
+    for seed in range(2):
+        gates = synthetic.random_circuit(n, 80, seed=500 + seed + 10 * world, kmax=3)
+        psi0 = synthetic.random_state(n, seed)
+        st = pkg.State(n, world=world)
+        st.write(psi0)
+        st.apply_circuit(gates, fusion_kmax=2, **mode)
+        ref = sim.run(gates, n, psi0)
+        assert np.abs(st.read() - ref).max() < 1e-10
+        for qs in ([n - 1], [0, n - 1, n - 2], list(range(4))):
+            assert np.abs(st.probabilities(qs) - sim.marginal(ref, n, qs)).max() < 1e-12
+        assert abs(st.norm2() - 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("opts", [dict(), dict(qpe_mode=1), dict(tile_qubits=-1), dict(tile_jit=1, tile_qubits=9)])
+def test_virtual_shards_hhl(world, opts):
+    A, b, nc = configs.get("C3")
+    xo, po, psi_o, p = ohhl.solve(A, b, nc)
+    st = pkg.State(p.n, world=world)
+    prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, **opts)
+    prog.run()
+    assert np.abs(st.read() - psi_o).max() < 1e-10
+    x, ps = prog.readout()
+    assert abs(ps - po) < 1e-12 and np.abs(x - xo).max() < 1e-10
+    x2, rep = pkg.hhl_solve(A, b, clock_qubits=nc, world=world, **opts)
+    assert np.abs(x2 - xo).max() < 1e-10
