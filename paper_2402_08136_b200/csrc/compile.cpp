@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <cstdlib>
 #include <sstream>
 
 #include "sv_internal.h"
@@ -56,7 +57,9 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
     }
     const int T = std::min(o.tile_qubits, nloc);
     const bool tiles = o.tile_qubits > 0 && nloc >= o.reg_bits + 3;
-    const int wmin = std::min(o.wmin, T - o.reg_bits);
+    int wmin_opt = o.wmin;   // default 4: 256-byte segments keep light passes at full HBM speed
+    if (const char *e = getenv("HHLSV_WMIN")) wmin_opt = atoi(e);     // developer experiments
+    const int wmin = std::min(wmin_opt, T - o.reg_bits);
     const int R = o.reg_bits;
 
     // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.

@@ -405,6 +405,24 @@ void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blo
             } else if (g.kind == Kind::Diagonal) {
                 r.kind = 1;
                 for (size_t j = 0; j < g.targets.size(); j++) route(g.targets[j], (int)j);
+                // "control-like" table bits: entry == 1 whenever the bit is 0 (every CP ladder of the
+                // (I)QFT). Amplitudes with such a bit 0 are left untouched: register bits skip slots,
+                // thread bits / out-of-tile bits guard the op (halves the FP64 work of the ladders).
+                for (size_t j = 0; j < g.targets.size(); j++) {
+                    bool unit = true;
+                    for (size_t idx = 0; idx < g.data.size() && unit; idx++)
+                        if (!((idx >> j) & 1) && g.data[idx] != cplx(1.0, 0.0)) unit = false;
+                    if (!unit) continue;
+                    const int b = g.targets[j];
+                    const int tp = index_in(st.tile_bits, b);
+                    const int rg = regbit(b);
+                    if (rg >= 0) r.rcm |= 1 << rg;
+                    else if (tp >= 0) r.tcm |= 1u << tp;
+                    else r.gcm |= 1ull << b;
+                }
+                r.rcv = r.rcm;
+                r.tcv = r.tcm;
+                r.gcv = r.gcm;
                 r.data_off = push_data(g.data);
             } else {
                 r.kind = 2;

@@ -223,7 +223,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             const dev::RegOp &op = ops[oi];
             std::ostringstream cond;
             if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
-            if (op.kind == 0 && op.tcm) {
+            if ((op.kind == 0 || op.kind == 1) && op.tcm) {
                 if (op.gcm) cond << " && ";
                 cond << "((tb & " << op.tcm << "u) == " << op.tcv << "u)";
             }
@@ -332,8 +332,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 if (op.kind == 1) {
                     k << "        const double2 *D = blob + " << op.data_off << "ull;\n";
                     for (int j = 0; j < 16; j++)
-                        k << "        const double2 d" << j << " = __ldg(D + (ib | " << op.ridx[j] << "u));\n";
-                    for (int j = 0; j < 16; j++) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
+                        if ((j & op.rcm) == op.rcv)
+                            k << "        const double2 d" << j << " = __ldg(D + (ib | " << op.ridx[j] << "u));\n";
+                    for (int j = 0; j < 16; j++)
+                        if ((j & op.rcm) == op.rcv) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
                 } else {
                     int A = 0;
                     while (!((op.mask >> A) & 1)) A++;
