@@ -259,7 +259,7 @@ sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t
                 a.T = (int)st.tile_bits.size();
                 for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
                 size_t ph0 = 0, opb = 0;
-                lower_tile_step(st, a, blob, rops, phases, ph0, opb);
+                lower_tile_step(st, a, blob, rops, phases, ph0, opb, true, 0.5);
                 std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
                 std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
                 std::string err;

@@ -206,7 +206,7 @@ static int index_in(const std::vector<int> &v, int x) {
 // Product-state init (+ folded leading diagonals): every factor is a table over its own bits;
 // factors are grouped into <= 4 group tables of <= 14 index bits (L2-resident), each entry the
 // product of its members, so the init kernel does <= 4 lookups and 3 complex products per amplitude.
-static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec) {
+static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec, double scale) {
     std::vector<const ProductFactor *> fs;
     for (auto &f : st.factors)
         if (!f.diag) fs.push_back(&f);
@@ -276,7 +276,7 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
                     if ((x >> pos[m][j]) & 1) idx |= (size_t)1 << j;
                 v *= G.mem[m]->vec[idx];
             }
-            tab[x] = v;
+            tab[x] = gi == 0 ? v * scale : v;
         }
         int nr = 0;   // runs of consecutive bits
         for (size_t j = 0; j < nb; j++) {
@@ -299,10 +299,26 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
     }
 }
 
+// A real 1-qubit gate a·[[1, 1], [1, -1]] (Hadamard up to scale): executed as an unscaled
+// butterfly (2 adds per amplitude instead of 4 FP64 ops), the factor a deferred to one global
+// scale applied by the init kernel or the first tile pass (all gates are linear).
+bool is_butterfly(const Gate &g, double *a) {
+    if (g.kind != Kind::Dense || g.targets.size() != 1 || g.data.size() != 4) return false;
+    for (auto &z : g.data)
+        if (z.imag() != 0.0) return false;
+    const double x = g.data[0].real();
+    if (x == 0.0 || g.data[1].real() != x || g.data[2].real() != x || g.data[3].real() != -x) return false;
+    if (a) *a = x;
+    return true;
+}
+
 // Host-side lowering of one Tile step into register phases + op descriptors (also used by the
 // host-only schedule check). Appends to blob/rops/phases; returns the first phase/op index.
+// butterflies: lower Hadamard-like gates to unscaled butterflies (JIT only); prescale != 1: scale
+// every amplitude by it at the start of the pass (the deferred butterfly factors).
 void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blob, std::vector<dev::RegOp> &rops,
-                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out) {
+                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out, bool butterflies,
+                     double prescale) {
     auto push_data = [&](const std::vector<cplx> &d) {
         size_t off = blob.size();
         for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
@@ -320,9 +336,23 @@ void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blo
         for (int tp = 0; tp < a.T; tp++)
             if (std::find(Rt.begin(), Rt.end(), tp) == Rt.end()) ph.tpos[nt++] = tp;
         ph.op0 = (int)(rops.size() - opbase);
+        if (pi == 0 && prescale != 1.0) {
+            dev::RegOp sc{};
+            sc.kind = 3;
+            sc.data_off = push_data({cplx(prescale, 0.0)});
+            rops.push_back(sc);
+        }
         for (size_t oi = st.phase_start[pi]; oi < st.phase_start[pi + 1]; oi++) {
             const Gate &g = st.tile_ops[oi];
             dev::RegOp r{};
+            if (butterflies && is_butterfly(g, nullptr)) {
+                const int rb = index_in(Rp, g.targets[0]);
+                if (rb < 0) fail(SV_E_ARG, "internal: butterfly target not in registers");
+                r.kind = 4;
+                r.mask = 1 << rb;
+                rops.push_back(r);
+                continue;
+            }
             auto regbit = [&](int phys_bit) { return index_in(Rp, phys_bit); };
             // route the bits of an index (table index / clock value): register slots ->
             // ridx[], thread-held tile positions and out-of-tile bits -> bit runs
@@ -492,6 +522,19 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     std::vector<double2> blob;
     std::vector<dev::RegOp> rops;
     std::vector<dev::RegPhase> phases;
+    // deferred butterfly scale (JIT tile passes only): applied by the init or the first tile pass
+    double bscale = 1.0;
+    bool has_init = false;
+    if (use_jit)
+        for (const Step &st : p->sched.steps) {
+            has_init |= st.kind == StepKind::InitProduct;
+            if (st.kind != StepKind::Tile) continue;
+            for (const Gate &g : st.tile_ops) {
+                double x = 0.0;
+                if (is_butterfly(g, &x)) bscale *= x;
+            }
+        }
+    double pending_scale = has_init ? 1.0 : bscale;
     auto push_data = [&](const std::vector<cplx> &d) {
         size_t off = blob.size();
         for (auto &z : d) blob.push_back(make_double2(z.real(), z.imag()));
@@ -507,7 +550,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         rec.bytes = st.bytes;
         switch (st.kind) {
             case StepKind::InitZero: break;
-            case StepKind::InitProduct: build_product(sv, p.get(), st, rec); break;
+            case StepKind::InitProduct: build_product(sv, p.get(), st, rec, bscale); break;
             case StepKind::Exchange:
                 rec.gbit = st.gbit;
                 rec.lbit = st.lbit;
@@ -603,7 +646,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 a.n_tiles = 1ull << (nloc - a.T);
                 a.rank_base = rank_base;
                 size_t ph0 = 0, opbase = 0;
-                lower_tile_step(st, a, blob, rops, phases, ph0, opbase);
+                lower_tile_step(st, a, blob, rops, phases, ph0, opbase, use_jit, pending_scale);
+                pending_scale = 1.0;
                 if (use_jit) {
                     std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());

@@ -80,7 +80,9 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
 void program_run(sv_state *sv, sv_program *p);
 void program_destroy(sv_program *p);
 void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blob, std::vector<dev::RegOp> &rops,
-                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out);
+                     std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out, bool butterflies,
+                     double prescale);
+bool is_butterfly(const Gate &g, double *a);
 void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out);
 void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out);
 void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in);

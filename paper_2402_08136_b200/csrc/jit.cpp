@@ -229,7 +229,19 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             const std::string c = cond.str();
             k << "      " << (c.empty() ? "{" : "if (" + c + ") {") << " // op " << oi << "\n";
-            if (op.kind == 0) {
+            if (op.kind == 3) {          // deferred global scale
+                k << "        const double sc = __ldg(&blob[" << op.data_off << "ull].x);\n";
+                for (int j = 0; j < 16; j++) k << "        v" << j << " = mk(v" << j << ".x * sc, v" << j << ".y * sc);\n";
+            } else if (op.kind == 4) {   // unscaled butterfly (Hadamard-like gate)
+                int A = 0;
+                while (!((op.mask >> A) & 1)) A++;
+                for (int j = 0; j < 16; j++) {
+                    if ((j >> A) & 1) continue;
+                    const int j1 = j | (1 << A);
+                    k << "        { const double2 x0 = v" << j << ", x1 = v" << j1 << "; v" << j
+                      << " = mk(x0.x + x1.x, x0.y + x1.y); v" << j1 << " = mk(x0.x - x1.x, x0.y - x1.y); }\n";
+                }
+            } else if (op.kind == 0) {
                 const int M = op.mask;
                 int K = 0;
                 for (int i = 0; i < 4; i++) K += (M >> i) & 1;
