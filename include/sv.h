@@ -207,8 +207,8 @@ typedef struct {
     int fusion_kmax;    /* 0 -> library default (4) ; -1 -> no fusion */
     int tile_qubits;    /* 0 -> library default ; -1 -> one pass per fused op */
     double recip_snap;  /* reciprocal snapping tolerance (qlsarepo: 1e-5); < 0 -> default 1e-5 */
-    int init_fold;      /* 0 (default): fold the leading product-state gates and the diagonal gates right after
-                           them into the init kernel; 1: product gates only; -1: no folding */
+    int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; 1: also the
+                           diagonal gates right after them; -1: no folding */
     int tile_jit;       /* as sv_fuse_options.tile_jit */
     int diag_kmax;      /* max qubits of a fused diagonal (0 -> 12 for HHL programs) */
     int qpe_mode;       /* 0: textbook circuit (c-U^(2^j) blocks, Fig. 5); 1: eigenbasis rewrite:

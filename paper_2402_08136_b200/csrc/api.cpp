@@ -323,7 +323,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     std::vector<Gate> gates = hhl_build(p, opt ? opt->qpe_mode : 0);
     const bool fold = !opt || opt->init_fold >= 0;
     std::vector<ProductFactor> factors;
-    size_t nf = fold ? fold_product_prefix(gates, p.n, factors, !opt || opt->init_fold != 1) : 0;
+    size_t nf = fold ? fold_product_prefix(gates, p.n, factors, opt && opt->init_fold == 1) : 0;
     std::vector<Gate> rest(gates.begin() + nf, gates.end());
     FuseOptions fo;
     if (opt && opt->fusion_kmax != 0) fo.kmax = opt->fusion_kmax < 0 ? 0 : opt->fusion_kmax;

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <numeric>
 #include <cstdlib>
+#include <set>
 #include <sstream>
 
 #include "sv_internal.h"
@@ -39,7 +40,129 @@ static Gate to_physical(const Gate &g, const std::vector<int> &phys) {
     return p;
 }
 
-Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> *init, int n, int nloc,
+// Qubits an op acts on NON-diagonally (mixes) and diagonally (controls, phase qubits).
+static void roles(const Gate &g, std::vector<int> &nd, std::vector<int> &dg) {
+    nd.clear();
+    dg.clear();
+    switch (g.kind) {
+        case Kind::Dense: nd = g.targets; break;
+        case Kind::Controlled: nd = g.targets; dg = g.controls; break;
+        case Kind::Diagonal: dg = g.targets; break;
+        case Kind::RecipRY: nd = g.targets; dg = g.controls; break;
+        case Kind::Swap: nd = g.targets; break;
+    }
+}
+
+// Commutation-aware reordering for tile packing. Two ops must keep their
+// relative order iff they share a qubit that at least one of them acts on non-diagonally (ops
+// on disjoint qubits commute; diagonal actions — controls, phases — commute with each other).
+// Greedy list scheduling then fills each T-qubit pass with every ready op whose non-diagonal
+// targets still fit, so e.g. the final Hadamard layer is absorbed into the QFT passes instead
+// of needing passes of its own. Returns a topological order of `ops` (the state is unchanged
+// up to rounding: only commuting ops are exchanged).
+static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const std::vector<int> &phys, int T,
+                                           int wmin, int R) {
+    const size_t m = ops.size();
+    std::vector<std::vector<size_t>> succ(m);
+    std::vector<int> indeg(m, 0);
+    {
+        std::vector<std::vector<int>> ndv(m), dgv(m);
+        for (size_t i = 0; i < m; i++) roles(ops[i], ndv[i], dgv[i]);
+        const int nq = (int)phys.size();
+        // per qubit: last non-diagonal user, and diagonal users since then
+        std::vector<long> last_nd(nq, -1);
+        std::vector<std::vector<size_t>> diag_since(nq);
+        auto edge = [&](size_t a, size_t b) {
+            if (a == b) return;
+            succ[a].push_back(b);
+            indeg[b]++;
+        };
+        for (size_t i = 0; i < m; i++) {
+            for (int q : ndv[i]) {
+                if (last_nd[q] >= 0) edge((size_t)last_nd[q], i);
+                for (size_t d : diag_since[q]) edge(d, i);
+            }
+            for (int q : dgv[i])
+                if (last_nd[q] >= 0) edge((size_t)last_nd[q], i);
+            for (int q : ndv[i]) {
+                last_nd[q] = (long)i;
+                diag_since[q].clear();
+            }
+            for (int q : dgv[i]) diag_since[q].push_back(i);
+        }
+        for (auto &v : succ) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        }
+        std::fill(indeg.begin(), indeg.end(), 0);
+        for (auto &v : succ)
+            for (size_t b : v) indeg[b]++;
+    }
+    auto pnd = [&](const Gate &g) {
+        std::vector<int> nd, dg;
+        roles(g, nd, dg);
+        for (int &q : nd) q = phys[q];
+        return nd;
+    };
+    auto fits = [&](const std::vector<int> &v) {
+        int high = 0;
+        for (int b : v) high += b >= wmin;
+        return (int)v.size() <= T && high <= T - wmin;
+    };
+    std::vector<Gate> out;
+    out.reserve(m);
+    std::vector<char> done(m, 0);
+    std::set<size_t> ready;
+    for (size_t i = 0; i < m; i++)
+        if (indeg[i] == 0) ready.insert(i);
+    auto take = [&](size_t i) {
+        done[i] = 1;
+        ready.erase(i);
+        out.push_back(ops[i]);
+        for (size_t b : succ[i])
+            if (--indeg[b] == 0) ready.insert(b);
+    };
+    while (!ready.empty()) {
+        // a swap or an op too wide for a tile is scheduled alone, in original order
+        size_t first = *ready.begin();
+        const Gate &g0 = ops[first];
+        if (g0.kind == Kind::Swap ||
+            ((g0.kind == Kind::Dense || g0.kind == Kind::Controlled) && (int)g0.targets.size() > R)) {
+            take(first);
+            continue;
+        }
+        std::vector<int> cur;
+        bool added = true;
+        while (added) {
+            added = false;
+            for (auto it = ready.begin(); it != ready.end();) {
+                const size_t i = *it;
+                const Gate &g = ops[i];
+                if (g.kind == Kind::Swap ||
+                    ((g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R)) {
+                    ++it;
+                    continue;
+                }
+                std::vector<int> u = cur;
+                for (int b : pnd(g))
+                    if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
+                if (!fits(u)) {
+                    ++it;
+                    continue;
+                }
+                cur = u;
+                ++it;           // take() may insert successors after `it`: they are seen in this scan
+                take(i);
+                added = true;
+            }
+        }
+        // pass boundary: the in-order packer below re-derives the same passes from this order
+    }
+    if (out.size() != m) fail(SV_E_ARG, "internal: dependency cycle in reorder_for_tiles");
+    return out;
+}
+
+Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFactor> *init, int n, int nloc,
                  const std::vector<int> &phys_in, const CompileOptions &o) {
     Schedule s;
     std::vector<int> phys = phys_in;
@@ -61,6 +184,10 @@ Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> 
     if (const char *e = getenv("HHLSV_WMIN")) wmin_opt = atoi(e);     // developer experiments
     const int wmin = std::min(wmin_opt, T - o.reg_bits);
     const int R = o.reg_bits;
+    // single-rank tile schedules: commutation-aware reordering for packing (multi-rank keeps the
+    // input order so exchanges follow the circuit)
+    const bool reorder = tiles && o.reorder && nloc == n;
+    const std::vector<Gate> ops = reorder ? reorder_for_tiles(ops_in, phys_in, T, wmin, R) : ops_in;
 
     // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.
     std::vector<std::vector<size_t>> uses(n);

@@ -133,6 +133,7 @@ struct CompileOptions {
     int wmin = 4;              // tiles always hold the lowest wmin physical bits (256 B segments)
     int reg_bits = 4;          // qubits held in registers per thread in a tile phase (16 amplitudes)
     int jit = 0;               // 0 auto, 1 always, -1 never (NVRTC-specialised tile passes)
+    bool reorder = true;       // commutation-aware op reordering for tile packing (single rank)
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.
