@@ -226,8 +226,16 @@ def run_ours(args):
     dom_avg = dom_ms / max(1, dom_n)
     achieved = dom_bytes / (dom_avg * 1e-3) / 1e9
     kind_names = pkg.sv.STEP_KINDS
+    traffic = None
+    try:   # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("kernel") == "hhlsv_tile" and kind_names[dom_kind] == "tile":
+            traffic = float(tr["dram_bytes_per_launch"])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": kind_names[dom_kind], "avg_launch_ms": dom_avg,
+                "traffic": traffic, "kernel": kind_names[dom_kind], "avg_launch_ms": dom_avg,
                 "bytes_per_launch": dom_bytes, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                 "share_of_step": dom_ms / args.steps / ms_step}
 
