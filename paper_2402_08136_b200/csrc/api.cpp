@@ -318,9 +318,12 @@ sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_optio
 static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
                              hhl_report *rep, double *b_norm_out) {
     const double t0 = now_s();
+    prof_mark("build_hhl start");
     HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
+    prof_mark("hhl_plan");
     std::vector<Gate> gates = hhl_build(p, opt ? opt->qpe_mode : 0);
+    prof_mark("hhl_build");
     const bool fold = !opt || opt->init_fold >= 0;
     std::vector<ProductFactor> factors;
     size_t nf = fold ? fold_product_prefix(gates, p.n, factors, opt && opt->init_fold == 1) : 0;
@@ -331,10 +334,12 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     fo.diag_kmax = 12;
     if (opt && opt->diag_kmax > 0) fo.diag_kmax = std::min(12, opt->diag_kmax);
     std::vector<Gate> fused = fuse(rest, fo);
+    prof_mark("fold + fuse");
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
     if (opt) co.jit = opt->tile_jit;
     sv_program *prog = program_create(sv, fused, &factors, co, gates.size());
+    prof_mark("program_create");
     if (rep) {
         std::memset(rep, 0, sizeof(*rep));
         rep->lambda_min = p.lam_min;
@@ -403,8 +408,10 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         if (opt) o = *opt;
         if (clock_qubits > 0) o.clock_qubits = clock_qubits;
         if (!opt) o.recip_snap = -1.0;
+        prof_mark("hhl_solve start");
         HHLPlanHost p = hhl_plan(A, b, N, o.clock_qubits, opt_snap(&o));
         sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream);
+        prof_mark("state_create");
         sv_program *prog = nullptr;
         try {
             hhl_report r{};
@@ -415,6 +422,7 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
             r.norm2 = state_norm2(sv);
             readout(sv, &r, N, bn, x_out, &r.p_success);
             r.t_sim_s = now_s() - t0;
+            prof_mark("run + readout");
             if (rep) *rep = r;
         } catch (...) {
             program_destroy(prog);
@@ -423,6 +431,7 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         }
         program_destroy(prog);
         state_destroy(sv);
+        prof_mark("destroy");
     });
 }
 

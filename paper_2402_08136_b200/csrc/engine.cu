@@ -19,6 +19,28 @@ static void nccl_check(int rc, const char *what) {
 }
 
 // ------------------------------------------------------------------ state ----
+// State buffers come from the device's stream-ordered memory pool with an unbounded release
+// threshold: freeing a 16 GiB state and creating the next one (hhl_solve called repeatedly)
+// reuses the pool instead of unmapping/remapping pages (HHLSV_NO_POOL=1 disables).
+static cudaError_t state_alloc(void **p, size_t bytes, cudaStream_t s, int device) {
+    static const bool no_pool = getenv("HHLSV_NO_POOL") != nullptr;
+    if (no_pool) return cudaMalloc(p, bytes);
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    e = cudaMallocAsync(p, bytes, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e;
+}
+static void state_free(void *p, cudaStream_t s) {
+    static const bool no_pool = getenv("HHLSV_NO_POOL") != nullptr;
+    if (!p) return;
+    if (no_pool) cudaFree(p);
+    else cudaFreeAsync(p, s);
+}
+
 sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
@@ -66,7 +88,7 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
             v->device = device;
             v->stream = stream;
             v->phys = sv->phys;
-            cuda_check(cudaMalloc(&v->psi, bytes), "cudaMalloc(virtual shard)");
+            cuda_check(state_alloc((void **)&v->psi, bytes, stream, device), "alloc(virtual shard)");
             v->red_len = dev::kRedBlocks;
             cuda_check(cudaMalloc(&v->d_red, sizeof(double) * v->red_len), "cudaMalloc(red)");
             cuda_check(cudaMalloc(&v->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
@@ -74,7 +96,7 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
         }
         sv->psi = sv->views[0]->psi;
     } else {
-        cuda_check(cudaMalloc(&sv->psi, bytes), "cudaMalloc(state)");
+        cuda_check(state_alloc((void **)&sv->psi, bytes, stream, device), "alloc(state)");
     }
     sv->red_len = dev::kRedBlocks;
     cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * sv->red_len), "cudaMalloc(red)");
@@ -92,7 +114,7 @@ void state_destroy(sv_state *sv) {
         sv->views.clear();
         sv->psi = nullptr;
     }
-    cudaFree(sv->psi);
+    state_free(sv->psi, sv->stream);
     cudaFree(sv->d_red);
     cudaFree(sv->d_scalar);
     cudaFree(sv->d_io);
@@ -515,6 +537,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     if (c2.tile_qubits > 12) c2.tile_qubits = 12;
     const bool use_jit = co.jit > 0 || (co.jit == 0 && sv->nloc >= 18);
     p->sched = compile(ops, init, sv->n, sv->nloc, p->phys_in, c2);
+    prof_mark("  compile");
     const int nloc = sv->nloc;
     const uint64_t rank_base = (uint64_t)sv->rank << nloc;
     auto rank_bit = [&](int phys_bit) -> int { return (int)((rank_base >> phys_bit) & 1ull); };
@@ -688,7 +711,9 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
     }
+    prof_mark("  lower + upload");
     if (!p->jit.empty()) jit_build(p->jit);
+    prof_mark("  jit_build");
     for (auto &t : tiles) {
         p->recs[t.rec].tile.phases = p->d_phases + t.op0;
         p->recs[t.rec].tile.ops = p->d_ops + t.opbase;

@@ -11,6 +11,9 @@
 // up to kmax targets, diagonal stays diagonal up to diag_kmax qubits, controlled ops with
 // equal controls merge their target blocks), SWAPs seen through by relabelling.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -23,6 +26,16 @@ namespace hhlsv {
 
 // ------------------------------------------------------------------ errors ----
 void fail(sv_status code, const std::string &msg) { throw Error{code, msg}; }
+
+void prof_mark(const char *stage) {
+    static const bool on = getenv("HHLSV_PROFILE") != nullptr;
+    if (!on) return;
+    using clk = std::chrono::steady_clock;
+    static thread_local clk::time_point last = clk::now();
+    const auto now = clk::now();
+    fprintf(stderr, "[hhlsv] %-28s %8.3f ms\n", stage, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
 
 double alg_bytes(const Gate &g, int n) {
     const double full = 32.0 * std::ldexp(1.0, n);     // read + write 16 B per amplitude

@@ -46,6 +46,8 @@ struct Error {
     std::string msg;
 };
 [[noreturn]] void fail(sv_status code, const std::string &msg);
+// Developer stage timer: with HHLSV_PROFILE=1 in the environment prints "<stage> <ms>" to stderr.
+void prof_mark(const char *stage);
 
 // Validation of one ABI gate -> internal Gate (copies the data).
 Gate gate_from_abi(const sv_gate &g, int n_qubits);
