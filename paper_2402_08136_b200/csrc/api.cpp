@@ -410,7 +410,8 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         if (!opt) o.recip_snap = -1.0;
         prof_mark("hhl_solve start");
         HHLPlanHost p = hhl_plan(A, b, N, o.clock_qubits, opt_snap(&o));
-        sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream);
+        // the HHL program starts with its own initialisation step: no |0...0> fill needed
+        sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream, false);
         prof_mark("state_create");
         sv_program *prog = nullptr;
         try {

@@ -41,7 +41,7 @@ static void state_free(void *p, cudaStream_t s) {
     else cudaFreeAsync(p, s);
 }
 
-sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
+sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zero_init) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();
@@ -102,7 +102,7 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream) {
     cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * sv->red_len), "cudaMalloc(red)");
     cuda_check(cudaMalloc(&sv->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
     if (world > 1 && !virt) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
-    state_reset(sv.get());
+    if (zero_init) state_reset(sv.get());
     return sv.release();
 }
 

@@ -72,7 +72,7 @@ struct sv_program {
 
 namespace hhlsv {
 void cuda_check(cudaError_t e, const char *what);
-sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream);
+sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zero_init = true);
 void state_destroy(sv_state *sv);
 void state_reset(sv_state *sv);
 sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,

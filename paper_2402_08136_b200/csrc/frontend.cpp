@@ -551,8 +551,19 @@ static bool try_merge(Gate &cur, const Gate &nx, const FuseOptions &o) {
     if (cur.kind == Kind::Diagonal && nx.kind == Kind::Diagonal) {
         auto u = union_of(cur.targets, nx.targets);
         if ((int)u.size() > o.diag_kmax) return false;
-        auto a = embed_diag(cur.data, cur.targets, u), b = embed_diag(nx.data, nx.targets, u);
-        for (size_t i = 0; i < a.size(); i++) a[i] *= b[i];
+        // cur.targets is a prefix of u: its table tiles over the appended bits; nx's bits are
+        // gathered per entry (few bits for the CP ladders being merged)
+        const size_t du = (size_t)1 << u.size(), mc = cur.data.size() - 1;
+        std::vector<int> pos(nx.targets.size());
+        for (size_t i = 0; i < nx.targets.size(); i++)
+            pos[i] = (int)(std::find(u.begin(), u.end(), nx.targets[i]) - u.begin());
+        std::vector<cplx> a(du);
+        for (size_t x = 0; x < du; x++) {
+            size_t j = 0;
+            for (size_t i = 0; i < pos.size(); i++)
+                if ((x >> pos[i]) & 1) j |= (size_t)1 << i;
+            a[x] = cur.data[x & mc] * nx.data[j];
+        }
         cur.targets = u;
         cur.data = std::move(a);
         return true;
