@@ -39,7 +39,7 @@ typedef enum {
     SV_E_ARG = 1,          /* bad argument: n < 1, qubit out of range/duplicated, k too large, null ptr, zero b */
     SV_E_RANGE = 2,        /* index range outside the state */
     SV_E_NOTUNITARY = 3,   /* ||U U^† - I||_max > 1e-10 (SPEC S:33 gate invariant) */
-    SV_E_NOTHERMITIAN = 4, /* A not symmetric within 1e-10 (Hermitian embedding is NEXT f3) */
+    SV_E_NOTHERMITIAN = 4, /* reserved (non-symmetric A is Hermitian-embedded) */
     SV_E_CLOCK = 5,        /* delta = 0: clock register too small for kappa (R5) */
     SV_E_ZEROPROB = 6,     /* post-selection probability < 1e-12 */
     SV_E_OOM = 7,          /* state or workspace does not fit in device memory */
@@ -226,9 +226,11 @@ typedef struct {
     double alg_bytes, pass_bytes;
     double t_frontend_s, t_sim_s;
     double h2d_bytes, d2h_bytes;   /* host<->device bytes of one solve (program upload, slice read) */
+    int x_offset;                  /* Hermitian embedding of a non-symmetric A: x = lower half of the slice */
 } hhl_report;
 
-/* Build the HHL circuit for A (N×N, row-major, real symmetric) and b (N) and return it as a
+/* Build the HHL circuit for A (N×N, row-major, real; a non-symmetric A is embedded as
+ * [[0, A], [A^T, 0]] [0; x] = [b; 0]) and b (N) and return it as a
  * program for `sv` (which must have n_b + n_c + 1 qubits; call hhl_plan_size first).
  * On return *b_norm, *lambda_min are what hhl_recover needs. */
 sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_options *opt, int *n_data,

@@ -39,6 +39,7 @@ class HHLPlan:
     phi: np.ndarray         # phi_s = lambda_s t / (2 pi)
     snap: float
     gates: list = field(default_factory=list)
+    x_offset: int = 0       # Hermitian embedding: the solution sits in the lower half
 
 
 def pad_system(A, b):
@@ -120,17 +121,31 @@ def controlled_evolution(V, phi, j):
     return (V * np.exp(2j * np.pi * f)[None, :]) @ V.conj().T
 
 
+def hermitize(Ap, bp):
+    """PAPER.md:168-183 step 1(c): [[0, A], [A^T, 0]] [0; x] = [b; 0] (real A: A^dagger = A^T)."""
+    N = Ap.shape[0]
+    H = np.zeros((2 * N, 2 * N))
+    H[:N, N:] = Ap
+    H[N:, :N] = Ap.T
+    return H, np.concatenate([bp, np.zeros(N)])
+
+
 def plan(A, b, clock_qubits: int | None = None, snap: float = 1e-5) -> HHLPlan:
-    """Steps 1-2 of the procedure box: normalise b, pad, eigen-analyse, choose n_c, delta, t."""
+    """Steps 1-2 of the procedure box: normalise b, pad (step 1b), Hermitize a non-symmetric A
+    (step 1c, after the expansion as Table 1's 30-bus* n_data = 6 implies), eigen-analyse,
+    choose n_c, delta, t."""
     A = np.asarray(A, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
-    if not np.allclose(A, A.T, atol=1e-10, rtol=0):
-        raise ValueError("A must be symmetric (Hermitian embedding is NEXT f3)")
     bn = float(np.linalg.norm(b))
     if bn == 0.0:
         raise ValueError("zero b")
     n0 = A.shape[0]
     Ap, bp, nb = pad_system(A, b)
+    x_offset = 0
+    if not np.allclose(Ap, Ap.T, atol=1e-10, rtol=0):
+        x_offset = Ap.shape[0]
+        Ap, bp = hermitize(Ap, bp)
+        nb += 1
     lam, V = np.linalg.eigh(Ap)
     alam = np.abs(lam)
     lam_min, lam_max = float(alam.min()), float(alam.max())
@@ -143,7 +158,8 @@ def plan(A, b, clock_qubits: int | None = None, snap: float = 1e-5) -> HHLPlan:
     t = 2.0 * math.pi * delta / lam_min / 2.0      # qlsarepo evolution time with neg_vals (R4)
     phi = (lam / lam_min) * (delta / 2.0)          # = lambda t / (2 pi), lam_min -> delta/2 exactly (R13)
     p = HHLPlan(A=Ap, b_hat=bp / bn, b_norm=bn, n_orig=n0, n_b=nb, n_c=nc, n=nb + nc + 1, lam=lam, V=V,
-                lam_min=lam_min, lam_max=lam_max, kappa=kappa, delta=delta, t=t, phi=phi, snap=snap)
+                lam_min=lam_min, lam_max=lam_max, kappa=kappa, delta=delta, t=t, phi=phi, snap=snap,
+                x_offset=x_offset)
     return p
 
 
@@ -180,12 +196,13 @@ def postselect(psi: np.ndarray, p: HHLPlan):
 
 def recover(slice_amps: np.ndarray, p_succ: float, p: HHLPlan) -> np.ndarray:
     """PAPER.md:193-198 step 4 read per F3/R8: ||x|| = sqrt(P_succ)/lambda_min,
-    x = ||x|| ||b|| |x>, |x> = slice/sqrt(P_succ); padding stripped (real part)."""
+    x = ||x|| ||b|| |x>, |x> = slice/sqrt(P_succ); padding stripped (real part); for a Hermitized
+    system the lower half is x."""
     if p_succ < 1e-12:
         raise ValueError("zero success probability")
     x_ket = slice_amps / math.sqrt(p_succ)
     x = (math.sqrt(p_succ) / p.lam_min) * p.b_norm * x_ket
-    return np.real(x[: p.n_orig])
+    return np.real(x[p.x_offset: p.x_offset + p.n_orig])
 
 
 def solve(A, b, clock_qubits=None, snap=1e-5):

@@ -357,6 +357,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
         rep->pass_bytes = prog->sched.pass_bytes;
         rep->h2d_bytes = prog->h2d_bytes;
         rep->d2h_bytes = 16.0 * (double)(1ull << p.n_b) + 8.0;
+        rep->x_offset = p.x_offset;
         rep->t_frontend_s = now_s() - t0;
     }
     if (b_norm_out) *b_norm_out = p.b_norm;
@@ -390,7 +391,7 @@ static void readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, d
     if (P < 1e-12) fail(SV_E_ZEROPROB, "post-selection probability below 1e-12");
     // x = ||b|| sqrt(P)/lambda_min * slice/sqrt(P)   (PAPER.md:193-198 read per F3/R8)
     if (x_out)
-        for (int i = 0; i < N; i++) x_out[i] = b_norm * amps[2 * i] / rep->lambda_min;
+        for (int i = 0; i < N; i++) x_out[i] = b_norm * amps[2 * (rep->x_offset + i)] / rep->lambda_min;
 }
 
 sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_success) {

@@ -178,23 +178,41 @@ HHLPlanHost hhl_plan(const double *A, const double *b, int N0, int clock_qubits,
     if (!A || !b || N0 < 1) fail(SV_E_ARG, "hhl: null A/b or N < 1");
     HHLPlanHost p;
     p.n_orig = N0;
+    bool symmetric = true;
     for (int i = 0; i < N0; i++)
         for (int j = 0; j < N0; j++)
-            if (std::fabs(A[i * N0 + j] - A[j * N0 + i]) > 1e-10)
-                fail(SV_E_NOTHERMITIAN, "hhl: A is not symmetric (Hermitian embedding is NEXT f3)");
+            if (std::fabs(A[i * N0 + j] - A[j * N0 + i]) > 1e-10) symmetric = false;
     double bn = 0.0;
     for (int i = 0; i < N0; i++) bn += b[i] * b[i];
     bn = std::sqrt(bn);
     if (!(bn > 0.0)) fail(SV_E_ARG, "hhl: b is zero");
     int nb = 1;
     while ((1 << nb) < N0) nb++;
-    const int N = 1 << nb;
+    int Np = 1 << nb;
+    // step 1(b): identity padding; step 1(c): [[0, A], [A^T, 0]] [0; x] = [b; 0] when A is not
+    // symmetric, after the expansion (Table 1's 30-bus* n_data = 6)
+    std::vector<double> Ap((size_t)Np * Np, 0.0);
+    for (int i = 0; i < Np; i++) Ap[(size_t)i * Np + i] = 1.0;
+    for (int i = 0; i < N0; i++)
+        for (int j = 0; j < N0; j++) Ap[(size_t)i * Np + j] = A[i * N0 + j];
+    int N = Np;
+    if (!symmetric) {
+        nb += 1;
+        N = 2 * Np;
+        p.x_offset = Np;
+    }
     p.N = N;
     p.n_b = nb;
     p.A.assign((size_t)N * N, 0.0);
-    for (int i = 0; i < N; i++) p.A[(size_t)i * N + i] = 1.0;
-    for (int i = 0; i < N0; i++)
-        for (int j = 0; j < N0; j++) p.A[(size_t)i * N + j] = A[i * N0 + j];
+    if (symmetric) {
+        p.A = Ap;
+    } else {
+        for (int i = 0; i < Np; i++)
+            for (int j = 0; j < Np; j++) {
+                p.A[(size_t)i * N + (Np + j)] = Ap[(size_t)i * Np + j];
+                p.A[(size_t)(Np + j) * N + i] = Ap[(size_t)i * Np + j];
+            }
+    }
     p.b_hat.assign(N, 0.0);
     for (int i = 0; i < N0; i++) p.b_hat[i] = b[i] / bn;
     p.b_norm = bn;

@@ -63,6 +63,7 @@ struct HHLPlanHost {
     double lam_min = 0, lam_max = 0, kappa = 0, delta = 0, t = 0;
     std::vector<double> phi;         // phi_s = (lam_s/lam_min)(delta/2)
     double snap = 1e-5;
+    int x_offset = 0;                // Hermitian embedding: x is the lower half
 };
 
 HHLPlanHost hhl_plan(const double *A, const double *b, int N, int clock_qubits, double snap);

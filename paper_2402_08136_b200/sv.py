@@ -64,7 +64,7 @@ class hhl_report(ctypes.Structure):
                 ("n_total", ctypes.c_int), ("n_logical", ctypes.c_uint64), ("n_fused", ctypes.c_uint64),
                 ("n_passes", ctypes.c_uint64), ("alg_bytes", ctypes.c_double), ("pass_bytes", ctypes.c_double),
                 ("t_frontend_s", ctypes.c_double), ("t_sim_s", ctypes.c_double), ("h2d_bytes", ctypes.c_double),
-                ("d2h_bytes", ctypes.c_double)]
+                ("d2h_bytes", ctypes.c_double), ("x_offset", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

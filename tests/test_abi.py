@@ -74,9 +74,8 @@ def test_plan_errors(lib):
     with pytest.raises(pkg.SVError) as e:
         pkg.hhl_plan_size(A, np.zeros(4))
     assert e.value.status == "SV_E_ARG"
-    with pytest.raises(pkg.SVError) as e:
-        pkg.hhl_plan_size(np.array([[1.0, 2.0], [0.0, 1.0]]), np.ones(2))
-    assert e.value.status == "SV_E_NOTHERMITIAN"
+    # non-symmetric A: Hermitian embedding doubles the system register
+    assert pkg.hhl_plan_size(np.array([[1.0, 2.0], [0.0, 1.0]]), np.ones(2))[0] == 2
 
 
 def test_gate_validation(lib):

@@ -286,3 +286,28 @@ def test_alpha_geometric_equals_fft():
             assert np.abs(a - b).max() < 1e-12          # FFT sums 2^nc rounded terms
             p2 = cf.alpha_abs2(phi, nc)
             assert np.abs(p2 - np.abs(b) ** 2).max() < 5e-12
+
+
+def test_hermitian_embedding_exact():
+    """[[0, A], [A^T, 0]] [0; x] = [b; 0]. A = [[0, 1], [3, 0]] has singular values
+    1 and 3, so the embedded eigenvalues +-1, +-3 are representable (negative ones through the sign
+    qubit) and HHL is exact: x = solve(A, b)."""
+    A = np.array([[0.0, 1.0], [3.0, 0.0]])
+    b = np.array([0.6, 0.8])
+    x, ps, psi, p = hhl.solve(A, b)
+    assert (p.n_b, p.x_offset) == (2, 2)
+    assert sorted(np.round(p.lam, 12)) == [-3, -1, 1, 3]
+    assert np.abs(x - np.linalg.solve(A, b)).max() < 1e-12
+    # the upper half of the post-selected vector is 0 (the [0; x] structure)
+    sl, _ = hhl.postselect(psi, p)
+    assert np.abs(sl[:2]).max() < 1e-12
+
+
+def test_hermitian_embedding_random():
+    """A seeded non-symmetric 4x4 system: relative error shrinks with the clock register."""
+    g = synthetic.rng(3)
+    A = g.standard_normal((4, 4)) + 4 * np.eye(4)
+    b = g.standard_normal(4)
+    xt = np.linalg.solve(A, b)
+    errs = [np.linalg.norm(hhl.solve(A, b, nc)[0] - xt) / np.linalg.norm(xt) for nc in (6, 8, 10)]
+    assert errs[0] > errs[2] and errs[2] < 5e-3
