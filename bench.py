@@ -316,7 +316,7 @@ def main():
     ap.add_argument("--tile", type=int, default=11)
     ap.add_argument("--qpe", type=int, default=1, help="0 textbook c-U chain, 1 eigenbasis rewrite (SURVEY f2)")
     ap.add_argument("--jit", type=int, default=0, help="tile pass specialisation: 0 auto, 1 on, -1 off")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
