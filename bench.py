@@ -313,7 +313,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None)
     ap.add_argument("--kmax", type=int, default=1)
-    ap.add_argument("--tile", type=int, default=11)
+    ap.add_argument("--tile", type=int, default=12)
     ap.add_argument("--qpe", type=int, default=1, help="0 textbook c-U chain, 1 eigenbasis rewrite (SURVEY f2)")
     ap.add_argument("--jit", type=int, default=0, help="tile pass specialisation: 0 auto, 1 on, -1 off")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -132,29 +132,35 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
             continue;
         }
         std::vector<int> cur;
-        bool added = true;
-        while (added) {
-            added = false;
-            for (auto it = ready.begin(); it != ready.end();) {
-                const size_t i = *it;
+        for (;;) {
+            // pick the ready op that adds the fewest new tile bits (free ones first), then the
+            // earliest in circuit order: keeps room in the pass for ops that become ready later
+            size_t best = SIZE_MAX;
+            int best_new = 1 << 20;
+            std::vector<int> best_u;
+            for (size_t i : ready) {
                 const Gate &g = ops[i];
                 if (g.kind == Kind::Swap ||
-                    ((g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R)) {
-                    ++it;
+                    ((g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R))
                     continue;
-                }
                 std::vector<int> u = cur;
+                int nnew = 0;
                 for (int b : pnd(g))
-                    if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
-                if (!fits(u)) {
-                    ++it;
-                    continue;
+                    if (std::find(u.begin(), u.end(), b) == u.end()) {
+                        u.push_back(b);
+                        nnew++;
+                    }
+                if (!fits(u)) continue;
+                if (nnew < best_new) {
+                    best = i;
+                    best_new = nnew;
+                    best_u = u;
+                    if (nnew == 0) break;      // ready is ordered: the earliest free op
                 }
-                cur = u;
-                ++it;           // take() may insert successors after `it`: they are seen in this scan
-                take(i);
-                added = true;
             }
+            if (best == SIZE_MAX) break;
+            cur = best_u;
+            take(best);
         }
         // pass boundary: the in-order packer below re-derives the same passes from this order
     }
@@ -180,7 +186,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     }
     const int T = std::min(o.tile_qubits, nloc);
     const bool tiles = o.tile_qubits > 0 && nloc >= o.reg_bits + 3;
-    int wmin_opt = o.wmin;   // default 4: 256-byte segments keep light passes at full HBM speed
+    int wmin_opt = o.wmin;   // default 3 (128-byte segments): more tile bits for op targets per pass
     if (const char *e = getenv("HHLSV_WMIN")) wmin_opt = atoi(e);     // developer experiments
     const int wmin = std::min(wmin_opt, T - o.reg_bits);
     const int R = o.reg_bits;

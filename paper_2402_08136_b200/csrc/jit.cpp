@@ -164,16 +164,23 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 wtot += (size_t)1 << (2 * Kk);
             }
         }
-    if (smem_extra) *smem_extra = wtot * sizeof(double2);
+    // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
+    // compute phases (default; measured faster than double buffering at half the occupancy),
+    // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
+    int nbuf = 1;
+    if (const char *e = getenv("HHLSV_JIT_NBUF")) nbuf = atoi(e) == 2 ? 2 : 1;
+    const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16;
+    if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
+    int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 512 / NTHR));
+    if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
     std::ostringstream k;
-    const size_t smem_cta = 2 * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16;
-    const int min_blocks = std::max(1, std::min(4, (int)((227 * 1024) / smem_cta)));
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-    k << "  double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);\n  double2 *buf1 = buf0 + NT;\n";
-    k << "  u64 *depA = reinterpret_cast<u64 *>(buf1 + NT);\n  u64 *depB = depA + " << (1 << SA) << ";\n";
+    k << "  double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);\n  double2 *buf1 = buf0 + " << (nbuf == 2 ? "NT" : "0")
+      << ";\n";
+    k << "  u64 *depA = reinterpret_cast<u64 *>(buf0 + " << nbuf << " * NT);\n  u64 *depB = depA + " << (1 << SA) << ";\n";
     k << "  for (int u = threadIdx.x; u < " << (1 << SA) << "; u += " << NTHR << ") { u64 d = 0;";
     for (int i = 0; i < SA; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[i] << ";";
     k << " depA[u] = d; }\n";
@@ -196,17 +203,25 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
       << "]; };\n";
     k << "  __syncthreads();\n";
     k << "  u64 tile = blockIdx.x;\n";
-    k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
-      << ") cp_async16(&buf0[swz(u)], &psi[addr(b0, u)]); }\n";
-    k << "  cp_async_commit();\n";
-    k << "  for (int it = 0; tile < n_tiles; tile += gridDim.x, it++) {\n";
-    k << "    double2 *cur = (it & 1) ? buf1 : buf0;\n    double2 *nxt = (it & 1) ? buf0 : buf1;\n";
-    k << "    const u64 next = tile + gridDim.x;\n";
-    k << "    if (next < n_tiles) { const u64 b1 = tile_base(next); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
-      << ") cp_async16(&nxt[swz(u)], &psi[addr(b1, u)]); }\n";
-    k << "    cp_async_commit();\n";
-    k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-    k << "    cp_async_wait1();\n    __syncthreads();\n";
+    if (nbuf == 2) {
+        k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+          << ") cp_async16(&buf0[swz(u)], &psi[addr(b0, u)]); }\n";
+        k << "  cp_async_commit();\n";
+        k << "  for (int it = 0; tile < n_tiles; tile += gridDim.x, it++) {\n";
+        k << "    double2 *cur = (it & 1) ? buf1 : buf0;\n    double2 *nxt = (it & 1) ? buf0 : buf1;\n";
+        k << "    const u64 next = tile + gridDim.x;\n";
+        k << "    if (next < n_tiles) { const u64 b1 = tile_base(next); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+          << ") cp_async16(&nxt[swz(u)], &psi[addr(b1, u)]); }\n";
+        k << "    cp_async_commit();\n";
+        k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
+        k << "    cp_async_wait1();\n    __syncthreads();\n";
+    } else {
+        k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
+        k << "    double2 *cur = buf0;\n";
+        k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
+        k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16(&cur[swz(u)], &psi[addr(base, u)]);\n";
+        k << "    cp_async_commit();\n    cp_async_wait0();\n    __syncthreads();\n";
+    }
     for (size_t p = 0; p < ph.size(); p++) {
         const dev::RegPhase &P = ph[p];
         k << "    { // phase " << p << "\n      const u32 tb = 0u";
@@ -469,9 +484,9 @@ void jit_build(std::vector<JitPass> &passes) {
     }
 }
 
-size_t jit_smem_bytes(int T, size_t extra) {
-    const int SA = (T + 1) / 2, SB = T - SA;
-    return 2 * sizeof(double2) * ((size_t)1 << T) + sizeof(uint64_t) * (((size_t)1 << SA) + ((size_t)1 << SB)) + extra;
+size_t jit_smem_bytes(int T, size_t total) {
+    (void)T;
+    return total;
 }
 
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,

@@ -13,7 +13,7 @@ struct JitPass {
     std::string name;
     std::string src;
     cudaKernel_t kern = nullptr;
-    size_t smem_extra = 0;     // bytes of staged wide-op matrices after the dep tables
+    size_t smem_extra = 0;     // total dynamic shared memory of the generated kernel (bytes)
 };
 
 bool jit_available(std::string *why);

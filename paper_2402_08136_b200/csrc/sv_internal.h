@@ -132,8 +132,8 @@ struct Step {
 struct Program;   // defined in engine.cu (device blob, launch records)
 
 struct CompileOptions {
-    int tile_qubits = 11;      // <= 0 : no tiles (one streaming pass per op)
-    int wmin = 4;              // tiles always hold the lowest wmin physical bits (256 B segments)
+    int tile_qubits = 12;      // <= 0 : no tiles (one streaming pass per op)
+    int wmin = 3;              // tiles always hold the lowest wmin physical bits (128 B segments)
     int reg_bits = 4;          // qubits held in registers per thread in a tile phase (16 amplitudes)
     int jit = 0;               // 0 auto, 1 always, -1 never (NVRTC-specialised tile passes)
     bool reorder = true;       // commutation-aware op reordering for tile packing (single rank)

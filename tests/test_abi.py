@@ -101,7 +101,7 @@ def _sched(n, gates, **kw):
 def test_fusion_counts_s30(lib):
     """Sequential greedy k<=4 fusion of the S30 circuit (after the folded prep + H layer):
     168 fused ops ('S30 -> 168'); with small-k fusion the tile scheduler packs
-    the 216 ops into <= 12 HBM passes whose tiles all hold the 4 lowest physical bits."""
+    the 216 ops into <= 12 HBM passes whose tiles all hold the 3 lowest physical bits."""
     A, b, nc = configs.get("S30")
     p = ohhl.plan(A, b, nc)
     g = ohhl.build(p)[1 + nc:]
@@ -111,10 +111,10 @@ def test_fusion_counts_s30(lib):
     assert rep2["n_fused"] == 168 and rep2["alg_bytes"] == rep["alg_bytes"]
     lines, rep3 = _sched(p.n, g, fusion_kmax=1, tile_qubits=12)
     assert rep3["n_passes"] <= 12
-    for ln in lines:                       # every tile keeps 256-byte contiguous segments
+    for ln in lines:                       # every tile keeps 128-byte contiguous segments
         if ln.startswith("TILE"):
             bits = [int(x) for x in ln.split()[1].split("=")[1].split(",")]
-            assert bits[:4] == [0, 1, 2, 3] and len(bits) == 12
+            assert bits[:3] == [0, 1, 2] and len(bits) == 12
 
 
 def test_swaps_are_relabels(lib):
