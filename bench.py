@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "HHL circuit sim time & fused-gate GB/s (fraction of HBM peak) at 1/2/4/8 B200"
+FP64_PEAK = 148 * 64 * 2 * 1.965e9          # flop/s, derived from unit counts and the max SM clock
 
 
 def measured_peaks():
@@ -192,6 +193,7 @@ def run_ours(args):
         x, ps = step()
     prog.set_timing(True)
     per_kind = {}
+    peak_gbs, _ = measured_peaks()
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -201,11 +203,14 @@ def run_ours(args):
         e0.record(stream)
         for _ in range(args.steps):
             x, ps = step()                      # readout synchronises the stream
-            for ms, kind, by, la in prog.timings():
-                d = per_kind.setdefault(kind, [0.0, 0, 0.0])
+            for ms, kind, by, la, fl in prog.timings(with_flops=True):
+                d = per_kind.setdefault(kind, [0.0, 0, 0.0, 0.0, 0.0])
                 d[0] += ms
                 d[1] += 1
                 d[2] = by
+                d[3] += fl
+                # per-launch roofline time: the slower of the HBM and the FP64 bound
+                d[4] += max(by / (peak_gbs * 1e9), fl / FP64_PEAK) * 1e3
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -223,7 +228,7 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     kind_exchange = 6
     dom = max(((k, v) for k, v in per_kind.items() if k != kind_exchange), key=lambda kv: kv[1][0])
-    dom_kind, (dom_ms, dom_n, dom_bytes) = dom
+    dom_kind, (dom_ms, dom_n, dom_bytes, dom_flops, dom_roof_ms) = dom
     dom_avg = dom_ms / max(1, dom_n)
     achieved = dom_bytes / (dom_avg * 1e-3) / 1e9
     kind_names = pkg.sv.STEP_KINDS
@@ -238,11 +243,17 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kind_names[dom_kind], "avg_launch_ms": dom_avg,
                 "bytes_per_launch": dom_bytes, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
-                "share_of_step": dom_ms / args.steps / ms_step}
+                "share_of_step": dom_ms / args.steps / ms_step,
+                # the tile passes also carry FP64 work: per launch the roofline time is
+                # max(bytes / HBM peak, flops / FP64 peak); combined_frac = roofline time / measured time
+                "fp64_tflops_achieved": dom_flops / (dom_ms * 1e-3) / 1e12,
+                "fp64_peak_tflops": FP64_PEAK / 1e12,
+                "fp64_peak_source": "derived: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (DESIGN.md §6)",
+                "combined_frac": dom_roof_ms / dom_ms}
 
     nvlink = None
     if kind_exchange in per_kind:      # global-qubit swaps: bytes each rank sends + receives per exchange
-        xms, xn, xby = per_kind[kind_exchange]
+        xms, xn, xby = per_kind[kind_exchange][:3]
         nvlink = {"exchanges_per_step": xn // max(1, args.steps), "ms_per_exchange": xms / max(1, xn),
                   "bytes_per_exchange": xby, "gbs": xby / (xms / max(1, xn) * 1e-3) / 1e9 if xms > 0 else None,
                   "share_of_step": xms / args.steps / ms_step}

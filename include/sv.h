@@ -170,10 +170,12 @@ sv_status sv_program_dump(sv_program *prog, char *buf, size_t buf_len);
  * kernel launch / exchange on the library stream; sv_program_timings returns the durations
  * (ms) of the last run (synchronises the stream) with each step's kind (0 init-zero,
  * 1 init-product, 2 dense/controlled, 3 diagonal, 4 recip-RY, 5 tile pass, 6 exchange),
- * its HBM bytes per launch and how many kernel launches it made. */
+ * its HBM bytes per launch, the FP64 flops it must execute (structure-aware: real matrices,
+ * butterflies and control-selected amplitudes counted as executed) and how many kernel
+ * launches it made. Any output pointer may be NULL. */
 sv_status sv_program_set_timing(sv_program *prog, int enable);
-sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, int *launches, size_t cap,
-                             size_t *n_out);
+sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, double *flops, int *launches,
+                             size_t cap, size_t *n_out);
 /* Number of kernel launches one sv_program_run makes on this rank, and the host->device
  * bytes uploaded when the program was created. */
 sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_bytes);

@@ -210,11 +210,11 @@ sv_status sv_program_set_timing(sv_program *prog, int enable) {
     });
 }
 
-sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, int *launches, size_t cap,
-                             size_t *n_out) {
+sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *bytes, double *flops, int *launches,
+                             size_t cap, size_t *n_out) {
     return guard([&] {
         if (!prog) fail(SV_E_ARG, "null program");
-        program_timings(prog, ms, kind, bytes, launches, cap, n_out);
+        program_timings(prog, ms, kind, bytes, flops, launches, cap, n_out);
     });
 }
 

@@ -220,6 +220,24 @@ static void virtual_exchange(sv_state *sv, int gbit, int lbit) {
 }
 
 // ---------------------------------------------------------------- program ----
+static int popc64(uint64_t x) { return __builtin_popcountll(x); }
+
+// FP64 flops per amplitude a register-phase op executes (complex MAC = 8, real x complex = 4,
+// complex multiply = 6, butterfly/scale = 2, reciprocal rotation ~6 per amplitude), times the
+// fraction of amplitudes its controls / control-like diagonal bits select.
+double regop_flops(const dev::RegOp &r) {
+    const double sel = std::ldexp(1.0, -(popc64((uint64_t)r.rcm) + popc64(r.tcm) + popc64(r.gcm)));
+    switch (r.kind) {
+        case 0: {
+            const int K = popc64((uint64_t)r.mask);
+            return (r.is_signed ? 4.0 : 8.0) * std::ldexp(1.0, K) * sel;
+        }
+        case 1: return 6.0 * sel;
+        case 2: return 6.0;
+        default: return 2.0;
+    }
+}
+
 static int index_in(const std::vector<int> &v, int x) {
     auto it = std::find(v.begin(), v.end(), x);
     return it == v.end() ? -1 : (int)(it - v.begin());
@@ -603,6 +621,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 a.nins = (int)ins.size();
                 for (size_t i = 0; i < ins.size(); i++) a.ins[i] = ins[i];
                 a.n_groups = 1ull << (nloc - (int)ins.size());
+                rec.flops = 8.0 * std::ldexp(1.0, st.k) * std::ldexp(1.0, st.k) * (double)a.n_groups;
                 a.U = reinterpret_cast<const double2 *>(push_data(g.data));
                 blob_fix.push_back(p->recs.size());
                 break;
@@ -625,6 +644,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     }
                 }
                 a.table_len = (int)g.data.size();
+                rec.flops = 6.0 * sv->local_amps();
                 a.table = reinterpret_cast<const double2 *>(push_data(g.data));
                 blob_fix.push_back(p->recs.size());
                 break;
@@ -634,6 +654,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 dev::RecipArgs &a = rec.recip;
                 a.psi = sv->psi;
                 a.n_pairs = sv->local_amps() >> 1;
+                rec.flops = 6.0 * sv->local_amps();
                 a.anc = g.targets[0];
                 a.n_c = (int)g.controls.size();
                 a.dL = g.delta * std::ldexp(1.0, a.n_c - (g.is_signed ? 1 : 0));
@@ -671,6 +692,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 size_t ph0 = 0, opbase = 0;
                 lower_tile_step(st, a, blob, rops, phases, ph0, opbase, use_jit, pending_scale);
                 pending_scale = 1.0;
+                for (size_t oi = opbase; oi < rops.size(); oi++) rec.flops += regop_flops(rops[oi]) * sv->local_amps();
                 if (use_jit) {
                     std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
@@ -809,7 +831,8 @@ void program_run(sv_state *sv, sv_program *p) {
     sv->phys = p->sched.phys_out;
 }
 
-void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out) {
+void program_timings(sv_program *p, float *ms, int *kind, double *bytes, double *flops, int *launches, size_t cap,
+                     size_t *n_out) {
     if (!p->timing || p->ev.size() != 2 * p->recs.size()) fail(SV_E_ARG, "timing not enabled or program not run");
     cuda_check(cudaStreamSynchronize(p->sv->stream), "timings sync");
     const size_t n = std::min(cap, p->recs.size());
@@ -819,6 +842,7 @@ void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *la
         if (ms) ms[i] = t;
         if (kind) kind[i] = (int)p->recs[i].kind;
         if (bytes) bytes[i] = p->recs[i].bytes;
+        if (flops) flops[i] = p->recs[i].flops;
         if (launches) launches[i] = rec_launches(p->sv, p->recs[i]);
     }
     if (n_out) *n_out = p->recs.size();

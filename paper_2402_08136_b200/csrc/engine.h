@@ -46,6 +46,7 @@ struct LaunchRec {
     dev::TileArgs tile{};
     int gbit = 0, lbit = 0;           // exchange
     int jit = -1;                     // tile: index into sv_program::jit (specialised kernel) or -1
+    double flops = 0;                 // FP64 flops the launch must execute (structure-aware count)
     double bytes = 0;
 };
 
@@ -83,7 +84,8 @@ void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blo
                      std::vector<dev::RegPhase> &phases, size_t &ph0_out, size_t &opbase_out, bool butterflies,
                      double prescale);
 bool is_butterfly(const Gate &g, double *a);
-void program_timings(sv_program *p, float *ms, int *kind, double *bytes, int *launches, size_t cap, size_t *n_out);
+void program_timings(sv_program *p, float *ms, int *kind, double *bytes, double *flops, int *launches, size_t cap,
+                     size_t *n_out);
 void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out);
 void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in);
 double state_norm2(sv_state *sv);

@@ -105,7 +105,7 @@ def load(path: str = LIB_PATH):
         "sv_program_run": [vp, vp], "sv_program_destroy": [vp],
         "sv_program_dump": [vp, ctypes.c_char_p, ctypes.c_size_t],
         "sv_program_set_timing": [vp, c_int],
-        "sv_program_timings": [vp, P(ctypes.c_float), P(c_int), P(c_dbl), P(c_int), ctypes.c_size_t,
+        "sv_program_timings": [vp, P(ctypes.c_float), P(c_int), P(c_dbl), P(c_dbl), P(c_int), ctypes.c_size_t,
                                P(ctypes.c_size_t)],
         "sv_program_stats": [vp, P(c_u64), P(c_u64)],
         "sv_schedule_dump": [c_int, c_int, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), ctypes.c_char_p,
@@ -307,16 +307,19 @@ class Program:
     def set_timing(self, enable: bool = True):
         _check(load().sv_program_set_timing(self._h, int(enable)))
 
-    def timings(self):
-        """Per-step (ms, kind, bytes, launches) of the last run (needs set_timing(True) before it)."""
+    def timings(self, with_flops: bool = False):
+        """Per-step (ms, kind, bytes, launches[, flops]) of the last run (needs set_timing(True) before it)."""
         n = ctypes.c_size_t()
-        _check(load().sv_program_timings(self._h, None, None, None, None, 0, ctypes.byref(n)))
+        _check(load().sv_program_timings(self._h, None, None, None, None, None, 0, ctypes.byref(n)))
         cap = n.value
         ms = (ctypes.c_float * max(1, cap))()
         kd = (ctypes.c_int * max(1, cap))()
         by = (ctypes.c_double * max(1, cap))()
+        fl = (ctypes.c_double * max(1, cap))()
         la = (ctypes.c_int * max(1, cap))()
-        _check(load().sv_program_timings(self._h, ms, kd, by, la, cap, ctypes.byref(n)))
+        _check(load().sv_program_timings(self._h, ms, kd, by, fl, la, cap, ctypes.byref(n)))
+        if with_flops:
+            return [(ms[i], kd[i], by[i], la[i], fl[i]) for i in range(cap)]
         return [(ms[i], kd[i], by[i], la[i]) for i in range(cap)]
 
     def stats(self):

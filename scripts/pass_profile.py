@@ -32,7 +32,7 @@ for q, k, T, J, DK, FO in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk, 
         prog.set_timing(True)
         for _ in range(a.reps):
             prog.run()
-            t = prog.timings()
+            t = prog.timings(with_flops=True)
         dump = prog.dump().splitlines()
         heads = [ln for ln in dump if not ln.startswith("  ")]
         total = sum(x[0] for x in t)
@@ -40,6 +40,8 @@ for q, k, T, J, DK, FO in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk, 
         print(f"== {a.config} qpe={q} kmax={k} tile={T} jit={J} dk={DK} fold={FO}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
               f"total {total:.1f} ms")
         if a.verbose:
-            for (ms, kind, by, la), h in zip(t, heads):
-                print(f"   {ms:9.3f} ms  {by / ms / 1e6 if ms > 0 else 0:8.1f} GB/s  {h[:100]}")
+            for (ms, kind, by, la, fl), h in zip(t, heads):
+                roof = max(by / 6533.2e9, fl / (148 * 64 * 2 * 1.965e9)) * 1e3
+                print(f"   {ms:9.3f} ms  {by / ms / 1e6 if ms > 0 else 0:8.1f} GB/s  {fl / 1e9:8.1f} GF  "
+                      f"roof {roof:6.2f} ms  {h[:80]}")
         prog.destroy()
