@@ -11,6 +11,7 @@
 // (in-process, keyed by the exact source text).
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -164,12 +165,51 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 wtot += (size_t)1 << (2 * Kk);
             }
         }
+    // Runs of >= 2 consecutive diagonal ops inside a phase are precomposed per tile: the CTA
+    // multiplies their tables, for the tile's fixed (out-of-tile) index bits, into a small
+    // shared sub-table over the run's varying tile bits V; each amplitude then does ONE lookup
+    // and ONE complex multiply for the whole run. Used when 2^|V| is small.
+    struct DRun { int p, a, b; std::vector<int> V; size_t off; };
+    std::vector<DRun> druns;
+    size_t dsub_max = 0;
+    auto op_vary = [&](const dev::RegOp &op, const dev::RegPhase &P) {
+        std::vector<int> v;
+        for (int i = 0; i < 4; i++)
+            if (op.ridx[1 << i]) v.push_back(P.R[i]);
+        for (int r = 0; r < op.ntr; r++)
+            for (int l = 0; l < op.t_len[r]; l++) v.push_back(op.t_src[r] + l);
+        return v;
+    };
+    for (size_t p = 0; p < ph.size(); p++) {
+        size_t used = 0;
+        for (int oi = ph[p].op0; oi < ph[p].op1;) {
+            if (ops[oi].kind != 1) {
+                oi++;
+                continue;
+            }
+            int oj = oi;
+            std::vector<int> V;
+            while (oj < ph[p].op1 && ops[oj].kind == 1) {
+                for (int b : op_vary(ops[oj], ph[p]))
+                    if (std::find(V.begin(), V.end(), b) == V.end()) V.push_back(b);
+                oj++;
+            }
+            std::sort(V.begin(), V.end());
+            if (oj - oi >= 2 && V.size() <= 9 && (int)V.size() <= T - 3) {
+                druns.push_back({(int)p, oi, oj, V, used});
+                used += (size_t)1 << V.size();
+            }
+            oi = oj;
+        }
+        dsub_max = std::max(dsub_max, used);
+    }
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
     // compute phases (default; measured faster than double buffering at half the occupancy),
     // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
     int nbuf = 1;
     if (const char *e = getenv("HHLSV_JIT_NBUF")) nbuf = atoi(e) == 2 ? 2 : 1;
-    const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16;
+    const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
+                            dsub_max * 16;
     if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
     int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 512 / NTHR));
     if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
@@ -196,6 +236,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
               << " + i] = blob[" << op.data_off << "ull + i];\n";
         }
     }
+    if (dsub_max)
+        k << "  double2 *dsub = reinterpret_cast<double2 *>(depB + " << (1 << SB) << ") + " << wtot << ";\n";
     k << "  auto tile_base = [](u64 t) { u64 b = t;";
     for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
     k << " return b; };\n";
@@ -233,8 +275,53 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (int i = 0; i < 4; i++)
                 if ((j >> i) & 1) rd[j] |= 1 << P.R[i];
         }
+        bool any_run = false;
+        for (auto &dr : druns) {
+            if (dr.p != (int)p) continue;
+            any_run = true;
+            const int nv = (int)dr.V.size();
+            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
+            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << dr.V[i] << ")";
+            k << ";\n        double2 acc = mk(1.0, 0.0);\n";
+            for (int oi = dr.a; oi < dr.b; oi++) {
+                const dev::RegOp &op = ops[oi];
+                k << "        { const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
+                  << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
+                for (int i = 0; i < 4; i++)
+                    if (op.ridx[1 << i]) {
+                        int ob = 0;
+                        while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
+                        k << " | ((u64)((loc >> " << P.R[i] << ") & 1u) << " << ob << ")";
+                    }
+                k << "; acc = cmul(acc, __ldg(blob + " << op.data_off << "ull + ib)); }\n";
+            }
+            k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
+        }
+        if (any_run) k << "      __syncthreads();\n";
         for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
         for (int oi = P.op0; oi < P.op1; oi++) {
+            const DRun *run = nullptr;
+            for (auto &dr : druns)
+                if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;
+            if (run) {
+                if (oi == run->a) {      // the whole run: one shared lookup + one complex multiply per slot
+                    const int nv = (int)run->V.size();
+                    k << "      { const u32 bt = 0u";
+                    for (int i = 0; i < nv; i++)
+                        if (std::find(P.R, P.R + 4, run->V[i]) == P.R + 4)
+                            k << " | (((tb >> " << run->V[i] << ") & 1u) << " << i << ")";
+                    k << "; // diagonal run of " << (run->b - run->a) << " ops\n";
+                    for (int j = 0; j < 16; j++) {
+                        int cj = 0;
+                        for (int i = 0; i < nv; i++)
+                            for (int r = 0; r < 4; r++)
+                                if (P.R[r] == run->V[i] && ((j >> r) & 1)) cj |= 1 << i;
+                        k << "        v" << j << " = cmul(dsub[" << run->off << " + (bt | " << cj << "u)], v" << j << ");\n";
+                    }
+                    k << "      }\n";
+                }
+                continue;
+            }
             const dev::RegOp &op = ops[oi];
             std::ostringstream cond;
             if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
