@@ -242,38 +242,18 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
     k << " return b; };\n";
     k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
-      << "]; };\n  (void)addr;\n";
-    // Element u = tid + i * NTHR of a tile (i < 16): its global offset is base | dt | C_i with
-    // dt = deposit(tid into the low T-4 tile bits) per thread and C_i = deposit(i into the top 4)
-    // a constant; its smem slot is swz(u) = swz(tid) ^ swz(i << (T-4)) (swz is linear over GF(2)).
-    auto swz_host = [](uint32_t u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); };
-    k << "  const u32 tid = threadIdx.x;\n  const u64 dt = 0ull";
-    for (int i = 0; i < T - dev::kRegBits; i++) k << " | ((u64)((tid >> " << i << ") & 1u) << " << a.tbits[i] << ")";
-    k << ";\n  const u32 stid = tid ^ (((tid >> 3) ^ (tid >> 6) ^ (tid >> 9) ^ (tid >> 12)) & 7u);\n";
-    std::vector<uint64_t> Ci(16);
-    std::vector<uint32_t> Ki(16);
-    for (int i = 0; i < 16; i++) {
-        uint64_t c = 0;
-        for (int b = 0; b < 4; b++)
-            if ((i >> b) & 1) c |= 1ull << a.tbits[T - dev::kRegBits + b];
-        Ci[i] = c;
-        Ki[i] = swz_host((uint32_t)i << (T - dev::kRegBits));
-    }
-    auto load_tile = [&](const char *buf, const char *b) {
-        std::ostringstream o;
-        for (int i = 0; i < 16; i++)
-            o << "    cp_async16(&" << buf << "[stid ^ " << Ki[i] << "u], &psi[" << b << " | dt | " << u64s(Ci[i]) << "]);\n";
-        return o.str();
-    };
+      << "]; };\n";
     k << "  __syncthreads();\n";
     k << "  u64 tile = blockIdx.x;\n";
     if (nbuf == 2) {
-        k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile);\n" << load_tile("buf0", "b0") << "  }\n";
+        k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+          << ") cp_async16(&buf0[swz(u)], &psi[addr(b0, u)]); }\n";
         k << "  cp_async_commit();\n";
         k << "  for (int it = 0; tile < n_tiles; tile += gridDim.x, it++) {\n";
         k << "    double2 *cur = (it & 1) ? buf1 : buf0;\n    double2 *nxt = (it & 1) ? buf0 : buf1;\n";
         k << "    const u64 next = tile + gridDim.x;\n";
-        k << "    if (next < n_tiles) { const u64 b1 = tile_base(next);\n" << load_tile("nxt", "b1") << "    }\n";
+        k << "    if (next < n_tiles) { const u64 b1 = tile_base(next); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
+          << ") cp_async16(&nxt[swz(u)], &psi[addr(b1, u)]); }\n";
         k << "    cp_async_commit();\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
         k << "    cp_async_wait1();\n    __syncthreads();\n";
@@ -281,7 +261,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
         k << "    double2 *cur = buf0;\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-        k << load_tile("cur", "base");
+        k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16(&cur[swz(u)], &psi[addr(base, u)]);\n";
         k << "    cp_async_commit();\n    cp_async_wait0();\n    __syncthreads();\n";
     }
     for (size_t p = 0; p < ph.size(); p++) {
@@ -318,8 +298,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
         }
         if (any_run) k << "      __syncthreads();\n";
-        k << "      const u32 stb = tb ^ (((tb >> 3) ^ (tb >> 6) ^ (tb >> 9) ^ (tb >> 12)) & 7u);\n";
-        for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[stb ^ " << swz_host((uint32_t)rd[j]) << "u];\n";
+        for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
         for (int oi = P.op0; oi < P.op1; oi++) {
             const DRun *run = nullptr;
             for (auto &dr : druns)
@@ -487,11 +466,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "      }\n";
         }
-        for (int j = 0; j < 16; j++) k << "      cur[stb ^ " << swz_host((uint32_t)rd[j]) << "u] = v" << j << ";\n";
+        for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
         k << "      __syncthreads();\n    }\n";
     }
-    for (int i = 0; i < 16; i++)
-        k << "    psi[base | dt | " << u64s(Ci[i]) << "] = cur[stid ^ " << Ki[i] << "u];\n";
+    k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
     k << "    __syncthreads();\n  }\n  cp_async_wait0();\n}\n";
     return k.str();
 }
