@@ -239,6 +239,12 @@ sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_optio
                         int *n_clock, int *n_total);
 sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
                             sv_program **out, hhl_report *rep);
+/* HOST-ONLY (no GPU needed): plan, build, fold and fuse the HHL circuit for (A, b) exactly as
+ * hhl_build_program does, schedule it for `world` ranks (power of two) and write the schedule
+ * text (one line per step, ops indented) into buf (NUL-terminated, truncated to buf_len).
+ * rep (may be NULL) receives the plan and schedule sizes; its timing fields are zero. */
+sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_options *opt, int world, char *buf,
+                            size_t buf_len, hhl_report *rep);
 /* Read out and recover x (PAPER.md:193-198 read per F3/R8): x = ||b|| sqrt(P)/lambda_min |x>,
  * |x> = slice / sqrt(P), padding stripped; x_out has N doubles (real part). */
 sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out,

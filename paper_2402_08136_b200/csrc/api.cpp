@@ -226,6 +226,32 @@ sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_b
     });
 }
 
+// Host-only: generate + NVRTC-compile every tile pass of a schedule; one log line per pass.
+static std::string jit_check_schedule(const Schedule &s) {
+    std::string why;
+    if (!jit_available(&why)) fail(SV_E_CUDA, "tile JIT unavailable: " + why);
+    std::string jitlog;
+    std::vector<double2> blob;
+    std::vector<dev::RegOp> rops;
+    std::vector<dev::RegPhase> phases;
+    for (const Step &st : s.steps) {
+        if (st.kind != StepKind::Tile) continue;
+        dev::TileArgs a{};
+        a.T = (int)st.tile_bits.size();
+        for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
+        size_t ph0 = 0, opb = 0;
+        lower_tile_step(st, a, blob, rops, phases, ph0, opb, true, 0.5);
+        std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
+        std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
+        std::string err;
+        auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops), err);
+        if (cubin.empty()) fail(SV_E_CUDA, err);
+        jitlog += "JIT_PASS phases=" + std::to_string(lph.size()) + " regops=" + std::to_string(lops.size()) +
+                  " cubin_bytes=" + std::to_string(cubin.size()) + "\n";
+    }
+    return jitlog;
+}
+
 sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
                            char *buf, size_t buf_len, sv_plan_report *rep) {
     return guard([&] {
@@ -246,28 +272,7 @@ sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
         }
-        std::string jitlog;
-        if (opt && opt->tile_jit > 0) {      // host-only: generate + NVRTC-compile every tile pass
-            std::string why;
-            if (!jit_available(&why)) fail(SV_E_CUDA, "tile JIT unavailable: " + why);
-            std::vector<double2> blob;
-            std::vector<dev::RegOp> rops;
-            std::vector<dev::RegPhase> phases;
-            for (const Step &st : s.steps) {
-                if (st.kind != StepKind::Tile) continue;
-                dev::TileArgs a{};
-                a.T = (int)st.tile_bits.size();
-                for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
-                size_t ph0 = 0, opb = 0;
-                lower_tile_step(st, a, blob, rops, phases, ph0, opb, true, 0.5);
-                std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
-                std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
-                std::string err;
-                auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops), err);
-                if (cubin.empty()) fail(SV_E_CUDA, err);
-                jitlog += "JIT_PASS cubin_bytes=" + std::to_string(cubin.size()) + "\n";
-            }
-        }
+        std::string jitlog = (opt && opt->tile_jit > 0) ? jit_check_schedule(s) : std::string();
         if (buf && buf_len) {
             std::string t = dump_schedule(s) + jitlog;
             std::string perm = "FINAL_MAP";
@@ -315,17 +320,13 @@ sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_optio
     });
 }
 
-static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
-                             hhl_report *rep, double *b_norm_out) {
-    const double t0 = now_s();
-    prof_mark("build_hhl start");
-    HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
-    if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
-    prof_mark("hhl_plan");
+// Host part of the HHL program: logical circuit, product-state prefix folded into init factors,
+// fusion of the rest. Shared by hhl_build_program and the host-only hhl_schedule_dump.
+static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options *opt,
+                                         std::vector<ProductFactor> &factors, size_t *n_logical) {
     std::vector<Gate> gates = hhl_build(p, opt ? opt->qpe_mode : 0);
     prof_mark("hhl_build");
     const bool fold = !opt || opt->init_fold >= 0;
-    std::vector<ProductFactor> factors;
     size_t nf = fold ? fold_product_prefix(gates, p.n, factors, opt && opt->init_fold == 1) : 0;
     std::vector<Gate> rest(gates.begin() + nf, gates.end());
     FuseOptions fo;
@@ -333,12 +334,29 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     if (fo.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
     fo.diag_kmax = 12;
     if (opt && opt->diag_kmax > 0) fo.diag_kmax = std::min(12, opt->diag_kmax);
-    std::vector<Gate> fused = fuse(rest, fo);
-    prof_mark("fold + fuse");
+    if (n_logical) *n_logical = gates.size();
+    return fuse(rest, fo);
+}
+
+static CompileOptions hhl_compile_opts(const hhl_options *opt) {
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
     if (opt) co.jit = opt->tile_jit;
-    sv_program *prog = program_create(sv, fused, &factors, co, gates.size());
+    return co;
+}
+
+static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
+                             hhl_report *rep, double *b_norm_out) {
+    const double t0 = now_s();
+    prof_mark("build_hhl start");
+    HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+    if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
+    prof_mark("hhl_plan");
+    std::vector<ProductFactor> factors;
+    size_t n_logical = 0;
+    std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
+    prof_mark("fold + fuse");
+    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt), n_logical);
     prof_mark("program_create");
     if (rep) {
         std::memset(rep, 0, sizeof(*rep));
@@ -350,7 +368,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
         rep->n_data = p.n_b;
         rep->n_clock = p.n_c;
         rep->n_total = p.n;
-        rep->n_logical = gates.size();
+        rep->n_logical = n_logical;
         rep->n_fused = prog->sched.n_fused;
         rep->n_passes = prog->sched.n_passes;
         rep->alg_bytes = prog->sched.alg_bytes;
@@ -392,6 +410,47 @@ static void readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, d
     // x = ||b|| sqrt(P)/lambda_min * slice/sqrt(P)   (PAPER.md:193-198 read per F3/R8)
     if (x_out)
         for (int i = 0; i < N; i++) x_out[i] = b_norm * amps[2 * (rep->x_offset + i)] / rep->lambda_min;
+}
+
+sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_options *opt, int world, char *buf,
+                            size_t buf_len, hhl_report *rep) {
+    return guard([&] {
+        if (world < 1 || (world & (world - 1))) fail(SV_E_ARG, "world must be a power of two");
+        int g = 0;
+        while ((1 << g) < world) g++;
+        HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+        if (p.n - g < 1) fail(SV_E_ARG, "too many ranks for this system");
+        std::vector<ProductFactor> factors;
+        size_t n_logical = 0;
+        std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
+        std::vector<int> phys(p.n);
+        for (int q = 0; q < p.n; q++) phys[q] = q;
+        Schedule s = compile(fused, nullptr, p.n, p.n - g, phys, hhl_compile_opts(opt));
+        if (rep) {
+            std::memset(rep, 0, sizeof(*rep));
+            rep->lambda_min = p.lam_min;
+            rep->lambda_max = p.lam_max;
+            rep->kappa = p.kappa;
+            rep->delta = p.delta;
+            rep->t_evol = p.t;
+            rep->n_data = p.n_b;
+            rep->n_clock = p.n_c;
+            rep->n_total = p.n;
+            rep->n_logical = n_logical;
+            rep->n_fused = s.n_fused;
+            rep->n_passes = s.n_passes;
+            rep->alg_bytes = s.alg_bytes;
+            rep->pass_bytes = s.pass_bytes;
+            rep->x_offset = p.x_offset;
+        }
+        if (buf && buf_len) {
+            std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s);
+            if (opt && opt->tile_jit > 0) t += jit_check_schedule(s);
+            size_t n = std::min(buf_len - 1, t.size());
+            std::memcpy(buf, t.data(), n);
+            buf[n] = 0;
+        }
+    });
 }
 
 sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_success) {

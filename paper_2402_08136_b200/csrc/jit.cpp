@@ -488,7 +488,19 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     Nvrtc &n = nvrtc();
     nvrtcProgram_t prog = nullptr;
     const std::string full = std::string(kPrelude) + src;
-    if (n.create(&prog, full.c_str(), "hhlsv_tile.cu", 0, nullptr, nullptr)) {
+    // developer aid (HHLSV_JIT_DUMP=dir): keep source + cubin, named by a hash of the source; the
+    // source path is the program name, so -lineinfo maps SASS to it (ncu --import-source)
+    std::string stem;
+    if (const char *dir = getenv("HHLSV_JIT_DUMP")) {
+        char hx[32];
+        snprintf(hx, sizeof hx, "%016zx", std::hash<std::string>()(full));
+        stem = std::string(dir) + "/tile_" + hx;
+        if (FILE *f = fopen((stem + ".cu").c_str(), "w")) {
+            fwrite(full.data(), 1, full.size(), f);
+            fclose(f);
+        }
+    }
+    if (n.create(&prog, full.c_str(), stem.empty() ? "hhlsv_tile.cu" : (stem + ".cu").c_str(), 0, nullptr, nullptr)) {
         err = "nvrtcCreateProgram failed";
         return {};
     }
@@ -508,13 +520,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     std::vector<char> cubin(cs);
     n.cubin(prog, cubin.data());
     n.destroy(&prog);
-    if (const char *dir = getenv("HHLSV_JIT_DUMP")) {      // developer aid: keep source + cubin
-        static std::atomic<int> seq{0};
-        const std::string stem = std::string(dir) + "/pass" + std::to_string(seq++);
-        if (FILE *f = fopen((stem + ".cu").c_str(), "w")) {
-            fwrite(full.data(), 1, full.size(), f);
-            fclose(f);
-        }
+    if (!stem.empty()) {
         if (FILE *f = fopen((stem + ".cubin").c_str(), "wb")) {
             fwrite(cubin.data(), 1, cubin.size(), f);
             fclose(f);

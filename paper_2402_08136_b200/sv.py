@@ -74,7 +74,8 @@ EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
            "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
-           "sv_norm2", "sv_postselect_slice", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve"]
+           "sv_norm2", "sv_postselect_slice", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve",
+           "hhl_schedule_dump"]
 
 _lib = None
 
@@ -114,6 +115,8 @@ def load(path: str = LIB_PATH):
         "sv_norm2": [vp, P(c_dbl)],
         "sv_postselect_slice": [vp, P(c_int), P(c_int), c_int, P(c_dbl), P(c_u64), c_u64, P(c_dbl)],
         "hhl_plan_size": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(c_int), P(c_int), P(c_int)],
+        "hhl_schedule_dump": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), c_int, ctypes.c_char_p, ctypes.c_size_t,
+                              P(hhl_report)],
         "hhl_build_program": [vp, P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(vp), P(hhl_report)],
         "hhl_readout": [vp, P(hhl_report), c_int, c_dbl, P(c_dbl), P(c_dbl)],
         "hhl_solve": [P(c_dbl), P(c_dbl), c_int, c_int, P(hhl_options), P(sv_dist), vp, P(c_dbl), P(hhl_report)],
@@ -368,6 +371,19 @@ def hhl_plan_size(A, b, **kw):
     _check(load().hhl_plan_size(_dp(A), _dp(b), b.size, ctypes.byref(o), ctypes.byref(nd), ctypes.byref(nc),
                                 ctypes.byref(nt)))
     return nd.value, nc.value, nt.value
+
+
+def hhl_schedule_dump(A, b, world: int = 1, **kw):
+    """Host-only: the schedule hhl_build_program would run for (A, b) on `world` ranks.
+    Returns (text, report dict)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    o = _opts(**kw)
+    buf = ctypes.create_string_buffer(1 << 22)
+    rep = hhl_report()
+    _check(load().hhl_schedule_dump(_dp(A), _dp(b), b.size, ctypes.byref(o), int(world), buf, len(buf),
+                                    ctypes.byref(rep)))
+    return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
 
 
 class HHLProgram(Program):

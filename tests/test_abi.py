@@ -149,3 +149,24 @@ def test_random_circuit_schedule_covers_all_ops(lib):
             n_ops = sum(1 for ln in lines if ln.startswith("  ") or ln.split()[0] in
                         ("DENSE", "CONTROLLED", "DIAGONAL", "RECIP_RY"))
             assert n_ops == rep["n_fused"]
+
+
+def test_hhl_schedule_dump_host_only(lib):
+    """hhl_schedule_dump plans the same circuit hhl_build_program runs, without a GPU: sizes agree
+    with hhl_plan_size (Table 1 14-bus: 4 + 8 + 1), the eigenbasis rewrite shrinks the
+    logical gate list, and on 2 ranks every non-diagonal op on the global qubit is preceded by an
+    EXCHANGE (f1 + e)."""
+    A, b = matpower.case14()
+    nd, nc, nt = pkg.hhl_plan_size(A, b)
+    txt0, r0 = pkg.hhl_schedule_dump(A, b, qpe_mode=0)
+    txt1, r1 = pkg.hhl_schedule_dump(A, b, qpe_mode=1)
+    for r in (r0, r1):
+        assert (r["n_data"], r["n_clock"], r["n_total"]) == (nd, nc, nt) == (4, 8, 13)
+        assert abs(r["kappa"] - 119.285) < 0.01
+    assert r1["n_logical"] < r0["n_logical"]
+    assert txt0.splitlines()[0].startswith("INIT_FACTORS")
+    txt2, r2 = pkg.hhl_schedule_dump(A, b, world=2, qpe_mode=1, tile_qubits=-1)
+    assert r2["n_fused"] == r1["n_fused"]
+    assert "EXCHANGE" in txt2
+    with pytest.raises(pkg.SVError):
+        pkg.hhl_schedule_dump(A, b, world=3)
