@@ -14,6 +14,7 @@
 //    applies all ops, and writes back. Without tiles, every op is one streaming pass.
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <numeric>
 #include <cstdlib>
 #include <set>
@@ -168,6 +169,88 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
     return out;
 }
 
+// Register phases of one tile pass. Ops inside a phase run on the 16 amplitudes a
+// thread holds in registers, spanned by <= R register bits; a phase boundary costs a round trip of
+// the tile through shared memory plus a barrier. The ops are list-scheduled over their commutation
+// DAG (same rule as reorder_for_tiles): the current phase takes the ready op that adds the fewest
+// new register bits (diagonal ops add none), the earliest on ties; when nothing fits, a new phase
+// starts. E.g. the final Hadamard layer joins the QFT phases instead of trailing in phases of its own.
+static void phase_schedule(std::vector<Gate> &ops, int R, std::vector<std::vector<int>> &phase_R,
+                           std::vector<size_t> &phase_start) {
+    const size_t m = ops.size();
+    std::vector<std::vector<size_t>> succ(m);
+    std::vector<int> indeg(m, 0);
+    std::vector<std::vector<int>> ndv(m), dgv(m);
+    for (size_t i = 0; i < m; i++) roles(ops[i], ndv[i], dgv[i]);
+    {
+        std::map<int, long> last_nd;
+        std::map<int, std::vector<size_t>> diag_since;
+        auto edge = [&](size_t a, size_t b) {
+            if (a != b) succ[a].push_back(b);
+        };
+        for (size_t i = 0; i < m; i++) {
+            for (int q : ndv[i]) {
+                auto it = last_nd.find(q);
+                if (it != last_nd.end()) edge((size_t)it->second, i);
+                for (size_t d : diag_since[q]) edge(d, i);
+            }
+            for (int q : dgv[i]) {
+                auto it = last_nd.find(q);
+                if (it != last_nd.end()) edge((size_t)it->second, i);
+            }
+            for (int q : ndv[i]) {
+                last_nd[q] = (long)i;
+                diag_since[q].clear();
+            }
+            for (int q : dgv[i]) diag_since[q].push_back(i);
+        }
+        for (auto &v : succ) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            for (size_t b : v) indeg[b]++;
+        }
+    }
+    std::set<size_t> ready;
+    for (size_t i = 0; i < m; i++)
+        if (indeg[i] == 0) ready.insert(i);
+    std::vector<Gate> out;
+    out.reserve(m);
+    std::vector<int> cur;
+    phase_R.clear();
+    phase_start.clear();
+    while (!ready.empty()) {
+        size_t best = SIZE_MAX;
+        int best_new = 1 << 20;
+        for (size_t i : ready) {
+            int nnew = 0;
+            for (int b : ndv[i])
+                if (std::find(cur.begin(), cur.end(), b) == cur.end()) nnew++;
+            if ((int)cur.size() + nnew > R) continue;
+            if (nnew < best_new) {
+                best = i;
+                best_new = nnew;
+                if (nnew == 0) break;
+            }
+        }
+        if (best == SIZE_MAX) {          // nothing fits: close the phase
+            phase_R.push_back(cur);
+            cur.clear();
+            continue;
+        }
+        if (out.empty() || phase_start.size() == phase_R.size()) phase_start.push_back(out.size());
+        for (int b : ndv[best])
+            if (std::find(cur.begin(), cur.end(), b) == cur.end()) cur.push_back(b);
+        out.push_back(ops[best]);
+        ready.erase(best);
+        for (size_t b : succ[best])
+            if (--indeg[b] == 0) ready.insert(b);
+    }
+    if (out.size() != m) fail(SV_E_ARG, "internal: dependency cycle in phase_schedule");
+    phase_R.push_back(cur);
+    phase_start.push_back(m);
+    ops = std::move(out);
+}
+
 Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFactor> *init, int n, int nloc,
                  const std::vector<int> &phys_in, const CompileOptions &o) {
     Schedule s;
@@ -216,25 +299,25 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
             if (std::find(set.begin(), set.end(), b) == set.end()) set.push_back(b);
         std::sort(set.begin(), set.end());
         tile.tile_bits = set;
-        // register phases: greedy, each phase's ops have their nd targets inside R (|R| <= reg_bits)
-        std::vector<int> cur;
-        for (size_t oi = 0; oi < tile.tile_ops.size(); oi++) {
-            std::vector<int> u = cur;
-            for (int b : nd_targets(tile.tile_ops[oi]))
-                if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
-            if (oi == 0 || (int)u.size() > R) {
-                if (oi > 0) tile.phase_R.push_back(cur);
-                tile.phase_start.push_back(oi);
-                u.clear();
-                for (int b : nd_targets(tile.tile_ops[oi])) u.push_back(b);
+        // register phases: each phase's ops have their nd targets inside R (|R| <= reg_bits)
+        phase_schedule(tile.tile_ops, R, tile.phase_R, tile.phase_start);
+        // Fill each phase's register set up to R bits with the highest tile bits (lanes keep the
+        // low ones), except bits a reciprocal rotation of the phase reads as clock bits: those would
+        // make its division + square root differ per register slot pair instead of per thread.
+        for (size_t pi = 0; pi < tile.phase_R.size(); pi++) {
+            auto &rr = tile.phase_R[pi];
+            std::vector<std::pair<int, int>> cand;      // (cost, -bit)
+            for (int b : set) {
+                if (std::find(rr.begin(), rr.end(), b) != rr.end()) continue;
+                int cost = 0;
+                for (size_t oi = tile.phase_start[pi]; oi < tile.phase_start[pi + 1]; oi++) {
+                    const Gate &g = tile.tile_ops[oi];
+                    if (g.kind == Kind::RecipRY && std::count(g.controls.begin(), g.controls.end(), b)) cost++;
+                }
+                cand.push_back({cost, -b});
             }
-            cur = u;
-        }
-        tile.phase_R.push_back(cur);
-        tile.phase_start.push_back(tile.tile_ops.size());
-        for (auto &rr : tile.phase_R) {       // fill with the highest tile bits (lanes keep the low ones)
-            for (int i = (int)set.size() - 1; (int)rr.size() < R && i >= 0; i--)
-                if (std::find(rr.begin(), rr.end(), set[i]) == rr.end()) rr.push_back(set[i]);
+            std::sort(cand.begin(), cand.end());
+            for (size_t i = 0; (int)rr.size() < R && i < cand.size(); i++) rr.push_back(-cand[i].second);
             std::sort(rr.begin(), rr.end());
         }
         tile.bytes = 32.0 * local_amps;
@@ -368,8 +451,12 @@ std::string dump_schedule(const Schedule &s) {
             case StepKind::RecipRY: os << "RECIP_RY anc=" << st.anc << " clock=" << bits(st.clock_bits) << "\n"; break;
             case StepKind::Exchange: os << "EXCHANGE global=" << st.gbit << " local=" << st.lbit << "\n"; break;
             case StepKind::Tile: {
-                os << "TILE bits=" << bits(st.tile_bits) << " ops=" << st.tile_ops.size() << "\n";
-                for (const Gate &g : st.tile_ops) {
+                os << "TILE bits=" << bits(st.tile_bits) << " ops=" << st.tile_ops.size() << " phases="
+                   << st.phase_R.size() << "\n";
+                for (size_t oi = 0; oi < st.tile_ops.size(); oi++) {
+                    const Gate &g = st.tile_ops[oi];
+                    for (size_t p = 0; p < st.phase_R.size(); p++)
+                        if (st.phase_start[p] == oi) os << " | phase R=" << bits(st.phase_R[p]) << "\n";
                     const char *nm = g.kind == Kind::Dense ? "dense" : g.kind == Kind::Controlled ? "controlled"
                                      : g.kind == Kind::Diagonal ? "diagonal" : "recip_ry";
                     os << "  " << nm << " t=" << bits(g.targets) << " c=" << bits(g.controls) << "\n";

@@ -733,6 +733,23 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
     }
+    if (const char *dir = getenv("HHLSV_EMU_DUMP")) {      // debug: launch list + blob for host emulation
+        if (FILE *f = fopen((std::string(dir) + "/blob.bin").c_str(), "wb")) {
+            fwrite(blob.data(), sizeof(double2), blob.size(), f);
+            fclose(f);
+        }
+        if (FILE *f = fopen((std::string(dir) + "/program.txt").c_str(), "w")) {
+            for (const LaunchRec &r : p->recs) {
+                if (r.kind == StepKind::Tile && r.jit >= 0)
+                    fprintf(f, "TILE %s %llu %d %llu %zu\n", jit_source_tag(p->jit[r.jit].src).c_str(),
+                            (unsigned long long)r.tile.n_tiles, r.tile.T, (unsigned long long)r.tile.rank_base,
+                            p->jit[r.jit].smem_extra);
+                else
+                    fprintf(f, "OTHER %d %d\n", (int)r.kind, (int)r.skip);
+            }
+            fclose(f);
+        }
+    }
     prof_mark("  lower + upload");
     if (!p->jit.empty()) jit_build(p->jit);
     prof_mark("  jit_build");

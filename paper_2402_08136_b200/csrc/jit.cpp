@@ -454,13 +454,27 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     int A = 0;
                     while (!((op.mask >> A) & 1)) A++;
                     k << "        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n";
+                    // one division + square root per distinct clock value among the slot pairs
+                    // (once per thread when no clock bit is a register bit)
+                    std::map<uint32_t, int> sc;
+                    for (int j = 0; j < 16; j++) {
+                        if ((j >> A) & 1) continue;
+                        if (sc.count(op.ridx[j])) continue;
+                        const int id = (int)sc.size();
+                        sc[op.ridx[j]] = id;
+                        k << "        const double s" << id << " = recip_s(ib | " << op.ridx[j] << "u, " << op.n_c
+                          << ", pr.x, " << op.is_signed << ", pr.y); const double c" << id << " = sqrt(fma(-s" << id
+                          << ", s" << id << ", 1.0));\n";
+                    }
                     for (int j = 0; j < 16; j++) {
                         if ((j >> A) & 1) continue;
                         const int j1 = j | (1 << A);
-                        k << "        { const double s = recip_s(ib | " << op.ridx[j] << "u, " << op.n_c << ", pr.x, "
-                          << op.is_signed << ", pr.y); const double c = sqrt(fma(-s, s, 1.0)); const double2 x0 = v"
-                          << j << ", x1 = v" << j1 << "; v" << j << " = mk(c * x0.x - s * x1.x, c * x0.y - s * x1.y); v"
-                          << j1 << " = mk(s * x0.x + c * x1.x, s * x0.y + c * x1.y); }\n";
+                        const std::string s = "s" + std::to_string(sc[op.ridx[j]]);
+                        const std::string c = "c" + std::to_string(sc[op.ridx[j]]);
+                        k << "        { const double2 x0 = v" << j << ", x1 = v" << j1 << "; v" << j << " = mk(" << c
+                          << " * x0.x - " << s << " * x1.x, " << c << " * x0.y - " << s << " * x1.y); v" << j1
+                          << " = mk(" << s << " * x0.x + " << c << " * x1.x, " << s << " * x0.y + " << c
+                          << " * x1.y); }\n";
                     }
                 }
             }
@@ -492,9 +506,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     // source path is the program name, so -lineinfo maps SASS to it (ncu --import-source)
     std::string stem;
     if (const char *dir = getenv("HHLSV_JIT_DUMP")) {
-        char hx[32];
-        snprintf(hx, sizeof hx, "%016zx", std::hash<std::string>()(full));
-        stem = std::string(dir) + "/tile_" + hx;
+        stem = std::string(dir) + "/" + jit_source_tag(src);
         if (FILE *f = fopen((stem + ".cu").c_str(), "w")) {
             fwrite(full.data(), 1, full.size(), f);
             fclose(f);
@@ -504,8 +516,13 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
         err = "nvrtcCreateProgram failed";
         return {};
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "--extra-device-vectorization"};
-    int rc = n.compile(prog, 4, opts);
+    // ptxas -O1: at -O2/-O3 ptxas miscompiles some of these kernels as NVRTC emits them (64-bit
+    // shared-window address arithmetic; nvcc's 32-bit form of the same source is fine): the
+    // binary faults with an illegal address although the source is clean (host emulation under
+    // ASan/UBSan, scripts/jit_emulate.py) and the same PTX runs correctly at -O0/-O1.
+    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O1"};
+    if (const char *x = getenv("HHLSV_JIT_OPT")) opts.back() = x;     // experiments
+    int rc = n.compile(prog, (int)opts.size(), opts.data());
     if (rc) {
         size_t ls = 0;
         n.logSize(prog, &ls);
@@ -529,6 +546,12 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     return cubin;
 }
 }  // namespace
+
+std::string jit_source_tag(const std::string &src) {
+    char hx[32];
+    snprintf(hx, sizeof hx, "%016zx", std::hash<std::string>()(std::string(kPrelude) + src));
+    return std::string("tile_") + hx;
+}
 
 std::vector<char> jit_compile_only(const std::string &src, std::string &err) {
     if (!nvrtc().ok) {

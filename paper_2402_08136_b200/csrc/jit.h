@@ -21,6 +21,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
+// Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.
+std::string jit_source_tag(const std::string &src);
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
                        int T, cudaStream_t s);
 size_t jit_smem_bytes(int T, size_t extra);
