@@ -92,6 +92,45 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// Shared memory through explicit 32-bit shared-window addresses (volatile asm keeps program order
+// between all shared accesses and barriers): nvcc's addressing form. NVRTC's default 64-bit
+// shared-pointer arithmetic trips a ptxas -O2/-O3 miscompilation on some of these kernels.
+__device__ __forceinline__ double2 lds(u32 a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y)); }
+__device__ __forceinline__ u64 lds64(u32 a) {
+    u64 v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(u32 a, u64 v) { asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v)); }
+__device__ __forceinline__ void bar() { asm volatile("bar.sync 0;" ::: "memory"); }
+struct SRef {
+    u32 a;
+    __device__ __forceinline__ operator double2() const { return lds(a); }
+    __device__ __forceinline__ void operator=(double2 v) const { sts(a, v); }
+};
+struct SArr {      // double2 array in shared memory
+    u32 b;
+    __device__ __forceinline__ SRef operator[](u32 i) const { return SRef{b + (i << 4)}; }
+    __device__ __forceinline__ SArr operator+(u32 o) const { return SArr{b + (o << 4)}; }
+    __device__ __forceinline__ u32 at(u32 i) const { return b + (i << 4); }
+};
+struct SRef64 {
+    u32 a;
+    __device__ __forceinline__ operator u64() const { return lds64(a); }
+    __device__ __forceinline__ void operator=(u64 v) const { sts64(a, v); }
+};
+struct SArr64 {
+    u32 b;
+    __device__ __forceinline__ SRef64 operator[](u32 i) const { return SRef64{b + (i << 3)}; }
+};
+__device__ __forceinline__ void cp_async16s(u32 s, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ double2 mk(double x, double y) { double2 r; r.x = x; r.y = y; return r; }
@@ -218,9 +257,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-    k << "  double2 *buf0 = reinterpret_cast<double2 *>(smem_raw);\n  double2 *buf1 = buf0 + " << (nbuf == 2 ? "NT" : "0")
-      << ";\n";
-    k << "  u64 *depA = reinterpret_cast<u64 *>(buf0 + " << nbuf << " * NT);\n  u64 *depB = depA + " << (1 << SA) << ";\n";
+    k << "  const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);\n";
+    k << "  const SArr buf0{sbase};\n  const SArr buf1{sbase + " << (nbuf == 2 ? "NT * 16u" : "0u") << "};\n";
+    k << "  const SArr64 depA{sbase + " << nbuf << "u * NT * 16u};\n  const SArr64 depB{sbase + " << nbuf
+      << "u * NT * 16u + " << (8 << SA) << "u};\n";
     k << "  for (int u = threadIdx.x; u < " << (1 << SA) << "; u += " << NTHR << ") { u64 d = 0;";
     for (int i = 0; i < SA; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[i] << ";";
     k << " depA[u] = d; }\n";
@@ -228,7 +268,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     for (int i = 0; i < SB; i++) k << " if (u & " << (1 << i) << ") d |= 1ull << " << a.tbits[SA + i] << ";";
     k << " depB[u] = d; }\n";
     if (wtot) {
-        k << "  double2 *wm = reinterpret_cast<double2 *>(depB + " << (1 << SB) << ");\n";
+        k << "  const SArr wm{depB.b + " << (8 << SB) << "u};\n";
         for (auto &kv : wstage) {
             const auto &op = ops[kv.first];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
@@ -237,32 +277,32 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         }
     }
     if (dsub_max)
-        k << "  double2 *dsub = reinterpret_cast<double2 *>(depB + " << (1 << SB) << ") + " << wtot << ";\n";
+        k << "  const SArr dsub{depB.b + " << (8 << SB) << "u + " << wtot * 16 << "u};\n";
     k << "  auto tile_base = [](u64 t) { u64 b = t;";
     for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
     k << " return b; };\n";
     k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
       << "]; };\n";
-    k << "  __syncthreads();\n";
+    k << "  bar();\n";
     k << "  u64 tile = blockIdx.x;\n";
     if (nbuf == 2) {
         k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
-          << ") cp_async16(&buf0[swz(u)], &psi[addr(b0, u)]); }\n";
+          << ") cp_async16s(buf0.at(swz(u)), &psi[addr(b0, u)]); }\n";
         k << "  cp_async_commit();\n";
         k << "  for (int it = 0; tile < n_tiles; tile += gridDim.x, it++) {\n";
-        k << "    double2 *cur = (it & 1) ? buf1 : buf0;\n    double2 *nxt = (it & 1) ? buf0 : buf1;\n";
+        k << "    const SArr cur = (it & 1) ? buf1 : buf0;\n    const SArr nxt = (it & 1) ? buf0 : buf1;\n";
         k << "    const u64 next = tile + gridDim.x;\n";
         k << "    if (next < n_tiles) { const u64 b1 = tile_base(next); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
-          << ") cp_async16(&nxt[swz(u)], &psi[addr(b1, u)]); }\n";
+          << ") cp_async16s(nxt.at(swz(u)), &psi[addr(b1, u)]); }\n";
         k << "    cp_async_commit();\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-        k << "    cp_async_wait1();\n    __syncthreads();\n";
+        k << "    cp_async_wait1();\n    bar();\n";
     } else {
         k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
-        k << "    double2 *cur = buf0;\n";
+        k << "    const SArr cur = buf0;\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-        k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16(&cur[swz(u)], &psi[addr(base, u)]);\n";
-        k << "    cp_async_commit();\n    cp_async_wait0();\n    __syncthreads();\n";
+        k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]);\n";
+        k << "    cp_async_commit();\n    cp_async_wait0();\n    bar();\n";
     }
     for (size_t p = 0; p < ph.size(); p++) {
         const dev::RegPhase &P = ph[p];
@@ -297,7 +337,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
         }
-        if (any_run) k << "      __syncthreads();\n";
+        if (any_run) k << "      bar();\n";
         for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
         for (int oi = P.op0; oi < P.op1; oi++) {
             const DRun *run = nullptr;
@@ -381,7 +421,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             for (int cc = 0; cc < D; cc++) {
                                 const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
                                 if (real)
-                                    o << " { const double w = " << Ur << "[" << cc << "].x; ax = fma(w, " << in
+                                    o << " { const double w = ((double2)" << Ur << "[" << cc << "]).x; ax = fma(w, " << in
                                       << ".x, ax); ay = fma(w, " << in << ".y, ay); }";
                                 else
                                     o << " { const double2 w = " << Ur << "[" << cc << "]; ax = fma(w.x, " << in
@@ -394,8 +434,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         auto ws0 = wstage.find(oi);
                         if (true) {   // rolled row loop: bounded registers (inputs stay in v) and code size
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
-                              << "; r++) { double ax = 0.0, ay = 0.0; const double2 *Ur = "
-                              << (ws0 != wstage.end() ? "wm + " + std::to_string(ws0->second) : std::string("U"))
+                              << "; r++) { double ax = 0.0, ay = 0.0; const auto Ur = "
+                              << (ws0 != wstage.end() ? "wm + " + std::to_string(ws0->second) + "u" : std::string("U"))
                               << " + r * " << D << ";" << (ws0 != wstage.end() ? row_s("Ur") : row("Ur"))
                               << " const u32 slot = " << rd[g] << "u";
                             for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
@@ -404,8 +444,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             auto ws = wstage.find(oi);
                             for (int r = 0; r < D; r++) {
                                 if (ws != wstage.end())
-                                    k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = wm + " << ws->second + r * D
-                                      << ";" << row_s("Ur");
+                                    k << "          { double ax = 0.0, ay = 0.0; const auto Ur = wm + " << ws->second + r * D
+                                      << "u;" << row_s("Ur");
                                 else
                                     k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
                                       << row("Ur");
@@ -481,10 +521,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      }\n";
         }
         for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
-        k << "      __syncthreads();\n    }\n";
+        k << "      bar();\n    }\n";
     }
     k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
-    k << "    __syncthreads();\n  }\n  cp_async_wait0();\n}\n";
+    k << "    bar();\n  }\n  cp_async_wait0();\n}\n";
     return k.str();
 }
 
@@ -516,11 +556,11 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
         err = "nvrtcCreateProgram failed";
         return {};
     }
-    // ptxas -O1: at -O2/-O3 ptxas miscompiles some of these kernels as NVRTC emits them (64-bit
-    // shared-window address arithmetic; nvcc's 32-bit form of the same source is fine): the
-    // binary faults with an illegal address although the source is clean (host emulation under
-    // ASan/UBSan, scripts/jit_emulate.py) and the same PTX runs correctly at -O0/-O1.
-    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O1"};
+    // Shared memory is addressed through explicit 32-bit shared-window addresses (lds/sts in the
+    // prelude): with NVRTC's default 64-bit shared-pointer arithmetic, ptxas -O2/-O3 miscompiled
+    // some tile kernels into illegal-address faults (source clean under host emulation with
+    // ASan/UBSan, scripts/jit_emulate.py; same PTX fine at -O1).
+    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O3"};
     if (const char *x = getenv("HHLSV_JIT_OPT")) opts.back() = x;     // experiments
     int rc = n.compile(prog, (int)opts.size(), opts.data());
     if (rc) {
