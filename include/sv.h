@@ -212,11 +212,13 @@ typedef struct {
     int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; 1: also the
                            diagonal gates right after them; -1: no folding */
     int tile_jit;       /* as sv_fuse_options.tile_jit */
-    int diag_kmax;      /* max qubits of a fused diagonal (0 -> 12 for HHL programs) */
+    int diag_kmax;      /* max qubits of a diagonal fused BEFORE scheduling (0 -> 4 with tile passes: the tile
+                           scheduler places small diagonals freely and merges those of one register phase
+                           into <= 8-qubit tables afterwards; 12 without tile passes) */
     int qpe_mode;       /* 0: textbook circuit (c-U^(2^j) blocks, Fig. 5); 1: eigenbasis rewrite:
                            c-U_j = V diag(e^{2 pi i frac(2^j phi_s)}) V^T, so the controlled chain becomes
-                           V^T, <= 12-qubit diagonal phase tables over (system, clock chunk), V — the same
-                           unitary (parity is checked against the textbook oracle) */
+                           V^T, one diagonal phase factor per clock bit over (system, clock bit), V — the
+                           same unitary (parity is checked against the textbook oracle) */
 } hhl_options;
 
 typedef struct {

@@ -332,7 +332,9 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     FuseOptions fo;
     if (opt && opt->fusion_kmax != 0) fo.kmax = opt->fusion_kmax < 0 ? 0 : opt->fusion_kmax;
     if (fo.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
-    fo.diag_kmax = 12;
+    // tile passes: keep diagonals small before scheduling (placed freely, merged per register phase
+    // afterwards); one HBM pass per op: merge them up front
+    fo.diag_kmax = (opt && opt->tile_qubits < 0) ? 12 : 4;
     if (opt && opt->diag_kmax > 0) fo.diag_kmax = std::min(12, opt->diag_kmax);
     if (n_logical) *n_logical = gates.size();
     return fuse(rest, fo);

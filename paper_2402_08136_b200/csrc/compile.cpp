@@ -251,6 +251,27 @@ static void phase_schedule(std::vector<Gate> &ops, int R, std::vector<std::vecto
     ops = std::move(out);
 }
 
+// Diagonal fusion after scheduling: inside a register phase, consecutive diagonal ops (they
+// commute, and the phase scheduler groups every ready one) become one table of <= kmax qubits:
+// one lookup + one complex multiply per amplitude for the group (table built on the host).
+static void merge_phase_diagonals(Step &tile, int kmax) {
+    std::vector<Gate> out;
+    std::vector<size_t> starts;
+    for (size_t p = 0; p + 1 < tile.phase_start.size(); p++) {
+        starts.push_back(out.size());
+        bool open = false;
+        for (size_t oi = tile.phase_start[p]; oi < tile.phase_start[p + 1]; oi++) {
+            Gate &g = tile.tile_ops[oi];
+            if (g.kind == Kind::Diagonal && open && merge_diagonal(out.back(), g, kmax)) continue;
+            open = g.kind == Kind::Diagonal;
+            out.push_back(std::move(g));
+        }
+    }
+    starts.push_back(out.size());
+    tile.tile_ops = std::move(out);
+    tile.phase_start = std::move(starts);
+}
+
 Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFactor> *init, int n, int nloc,
                  const std::vector<int> &phys_in, const CompileOptions &o) {
     Schedule s;
@@ -301,6 +322,9 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
         tile.tile_bits = set;
         // register phases: each phase's ops have their nd targets inside R (|R| <= reg_bits)
         phase_schedule(tile.tile_ops, R, tile.phase_R, tile.phase_start);
+        static const int dm_env = getenv("HHLSV_DIAG_MERGE") ? atoi(getenv("HHLSV_DIAG_MERGE")) : -1;   // experiments
+        const int dm = dm_env >= 0 ? dm_env : o.diag_merge;
+        if (dm > 0) merge_phase_diagonals(tile, dm);
         // Fill each phase's register set up to R bits with the highest tile bits (lanes keep the
         // low ones), except bits a reciprocal rotation of the phase reads as clock bits: those would
         // make its division + square root differ per register slot pair instead of per thread.
@@ -427,6 +451,17 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     }
     close_tile();
     s.phys_out = phys;
+    // fused-op count and algorithmic bytes of the ops actually executed (after the in-phase
+    // diagonal merge): each op counted as if it ran as its own HBM pass
+    s.n_fused = 0;
+    s.alg_bytes = 0.0;
+    for (const Step &st : s.steps)
+        if (st.kind == StepKind::Tile || st.kind == StepKind::Dense || st.kind == StepKind::Diagonal ||
+            st.kind == StepKind::RecipRY)
+            for (const Gate &g : st.tile_ops) {
+                s.n_fused++;
+                s.alg_bytes += alg_bytes(g, n);
+            }
     return s;
 }
 

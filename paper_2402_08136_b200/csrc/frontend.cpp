@@ -304,9 +304,13 @@ static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const
                 v.data[(size_t)r * N + c] = transpose ? p.V[c + (size_t)N * r] : p.V[r + (size_t)N * c];
         return v;
     };
-    // chunks of 4 clock bits: tables of 2^(n_b+4) entries (4 KB at n_b = 4) stay L1-resident in the
-    // tile passes (12-qubit tables thrash L1 when several are live in one pass)
-    const int chunk = std::max(1, std::min(4, 12 - nb));
+    // One factor per clock bit: D_j = diag over (system, clock bit j), 2^(n_b+1) entries. Fusion
+    // leaves them separate (HHL fusion caps diagonal merging at a few qubits), so the tile
+    // scheduler can place each factor in whichever pass holds its clock bit's QFT Hadamard; the
+    // factors of one register phase are then merged after scheduling (compile.cpp
+    // merge_phase_diagonals). Lets the final V join the last QFT pass.
+    int chunk = 1;
+    if (const char *e = getenv("HHLSV_EIGEN_CHUNK")) chunk = std::max(1, atoi(e));   // experiments
     std::vector<Gate> diags;
     for (int j0 = 0; j0 < nc; j0 += chunk) {
         const int cj = std::min(chunk, nc - j0);
@@ -564,28 +568,30 @@ static bool disjoint(const std::vector<int> &a, const std::vector<int> &b) {
 }
 
 // Try to merge `nx` (applied after `cur`) into `cur`. Returns true on success.
+bool merge_diagonal(Gate &cur, const Gate &nx, int diag_kmax) {
+    auto u = union_of(cur.targets, nx.targets);
+    if ((int)u.size() > diag_kmax) return false;
+    // cur.targets is a prefix of u: its table tiles over the appended bits; nx's bits are
+    // gathered per entry (few bits for the CP ladders being merged)
+    const size_t du = (size_t)1 << u.size(), mc = cur.data.size() - 1;
+    std::vector<int> pos(nx.targets.size());
+    for (size_t i = 0; i < nx.targets.size(); i++)
+        pos[i] = (int)(std::find(u.begin(), u.end(), nx.targets[i]) - u.begin());
+    std::vector<cplx> a(du);
+    for (size_t x = 0; x < du; x++) {
+        size_t j = 0;
+        for (size_t i = 0; i < pos.size(); i++)
+            if ((x >> pos[i]) & 1) j |= (size_t)1 << i;
+        a[x] = cur.data[x & mc] * nx.data[j];
+    }
+    cur.targets = u;
+    cur.data = std::move(a);
+    return true;
+}
+
 static bool try_merge(Gate &cur, const Gate &nx, const FuseOptions &o) {
     if (cur.kind == Kind::RecipRY || nx.kind == Kind::RecipRY) return false;
-    if (cur.kind == Kind::Diagonal && nx.kind == Kind::Diagonal) {
-        auto u = union_of(cur.targets, nx.targets);
-        if ((int)u.size() > o.diag_kmax) return false;
-        // cur.targets is a prefix of u: its table tiles over the appended bits; nx's bits are
-        // gathered per entry (few bits for the CP ladders being merged)
-        const size_t du = (size_t)1 << u.size(), mc = cur.data.size() - 1;
-        std::vector<int> pos(nx.targets.size());
-        for (size_t i = 0; i < nx.targets.size(); i++)
-            pos[i] = (int)(std::find(u.begin(), u.end(), nx.targets[i]) - u.begin());
-        std::vector<cplx> a(du);
-        for (size_t x = 0; x < du; x++) {
-            size_t j = 0;
-            for (size_t i = 0; i < pos.size(); i++)
-                if ((x >> pos[i]) & 1) j |= (size_t)1 << i;
-            a[x] = cur.data[x & mc] * nx.data[j];
-        }
-        cur.targets = u;
-        cur.data = std::move(a);
-        return true;
-    }
+    if (cur.kind == Kind::Diagonal && nx.kind == Kind::Diagonal) return merge_diagonal(cur, nx, o.diag_kmax);
     const bool cd = cur.kind == Kind::Dense || cur.kind == Kind::Diagonal;
     const bool nd = nx.kind == Kind::Dense || nx.kind == Kind::Diagonal;
     if (cd && nd) {

@@ -75,6 +75,8 @@ struct FuseOptions {
     int diag_kmax = 10;    // diagonal width cap
 };
 std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o);
+// cur <- nx * cur for two diagonal ops when their union has <= diag_kmax qubits (else false).
+bool merge_diagonal(Gate &cur, const Gate &nx, int diag_kmax);
 
 // Product-state prefix: if the circuit starts (from |0...0>) with gates on disjoint
 // qubit sets, each a Dense gate acting on qubits untouched before, the state after
@@ -137,6 +139,8 @@ struct CompileOptions {
     int reg_bits = 4;          // qubits held in registers per thread in a tile phase (16 amplitudes)
     int jit = 0;               // 0 auto, 1 always, -1 never (NVRTC-specialised tile passes)
     bool reorder = true;       // commutation-aware op reordering for tile packing (single rank)
+    int diag_merge = 8;        // tile passes: merge consecutive diagonal ops of a register phase into
+                               // one table of <= this many qubits after scheduling (0 = off)
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.
