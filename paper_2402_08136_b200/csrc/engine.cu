@@ -243,23 +243,37 @@ static int index_in(const std::vector<int> &v, int x) {
     return it == v.end() ? -1 : (int)(it - v.begin());
 }
 
-// Product-state init (+ folded leading diagonals): every factor is a table over its own bits;
-// factors are grouped into <= 4 group tables of <= 14 index bits (L2-resident), each entry the
-// product of its members, so the init kernel does <= 4 lookups and 3 complex products per amplitude.
-static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec, double scale) {
+// Product-state init (+ folded leading diagonals): every factor is a table over its own bits.
+// Factors whose entries are all equal (e.g. H|0> on every clock qubit) only scale the state: their
+// value joins the global scale. The rest are grouped into <= 4 group tables of <= 14 index bits
+// (L2-resident), each entry the product of its members, so the init does <= 4 lookups and 3
+// complex products per amplitude; amplitudes with a bit no factor covers set are 0.
+struct ProductPlan {
+    uint64_t zero_mask = 0;
+    std::vector<std::vector<int>> bits;      // per group: physical bits, ascending (table bit j <- bits[j])
+    std::vector<std::vector<cplx>> tabs;
+};
+
+static ProductPlan plan_product(const sv_state *sv, const Step &st, double scale) {
     std::vector<const ProductFactor *> fs;
-    for (auto &f : st.factors)
-        if (!f.diag) fs.push_back(&f);
-    std::sort(fs.begin(), fs.end(), [](const ProductFactor *a, const ProductFactor *b) {
+    uint64_t covered = 0;
+    cplx cscale(scale, 0.0);
+    for (auto &f : st.factors) {
+        if (!f.diag)
+            for (int q : f.qubits) covered |= 1ull << q;
+        bool uniform = true;
+        for (auto &z : f.vec) uniform &= z == f.vec[0];
+        if (uniform) {
+            cscale *= f.vec[0];
+            continue;
+        }
+        fs.push_back(&f);
+    }
+    std::stable_sort(fs.begin(), fs.end(), [](const ProductFactor *a, const ProductFactor *b) {
+        if (a->diag != b->diag) return !a->diag;
         return *std::min_element(a->qubits.begin(), a->qubits.end()) <
                *std::min_element(b->qubits.begin(), b->qubits.end());
     });
-    for (auto &f : st.factors)
-        if (f.diag) fs.push_back(&f);
-    uint64_t covered = 0;
-    for (auto *f : fs)
-        if (!f->diag)
-            for (int q : f->qubits) covered |= 1ull << q;
     struct Group {
         std::vector<int> bits;
         std::vector<const ProductFactor *> mem;
@@ -292,13 +306,10 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
                 groups[best].bits.push_back(q);
         groups[best].mem.push_back(f);
     }
-    dev::ProductArgs &a = rec.prod;
-    a.psi = sv->psi;
-    a.n_amps = sv->local_amps();
-    a.rank_base = (uint64_t)sv->rank << sv->nloc;
+    if (groups.empty()) groups.push_back({});     // a single scale entry
+    ProductPlan pp;
     const uint64_t all = sv->n >= 64 ? ~0ull : ((1ull << sv->n) - 1ull);
-    a.zero_mask = all & ~covered;
-    a.ngroups = (int)groups.size();
+    pp.zero_mask = all & ~covered;
     for (size_t gi = 0; gi < groups.size(); gi++) {
         Group &G = groups[gi];
         std::sort(G.bits.begin(), G.bits.end());
@@ -316,20 +327,37 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
                     if ((x >> pos[m][j]) & 1) idx |= (size_t)1 << j;
                 v *= G.mem[m]->vec[idx];
             }
-            tab[x] = gi == 0 ? v * scale : v;
+            tab[x] = gi == 0 ? v * cscale : v;
         }
+        pp.bits.push_back(G.bits);
+        pp.tabs.push_back(std::move(tab));
+    }
+    return pp;
+}
+
+static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec &rec, double scale) {
+    ProductPlan pp = plan_product(sv, st, scale);
+    dev::ProductArgs &a = rec.prod;
+    a.psi = sv->psi;
+    a.n_amps = sv->local_amps();
+    a.rank_base = (uint64_t)sv->rank << sv->nloc;
+    a.zero_mask = pp.zero_mask;
+    a.ngroups = (int)pp.tabs.size();
+    for (size_t gi = 0; gi < pp.tabs.size(); gi++) {
+        const std::vector<int> &bits = pp.bits[gi];
         int nr = 0;   // runs of consecutive bits
-        for (size_t j = 0; j < nb; j++) {
-            if (nr > 0 && G.bits[j] == a.rsrc[gi][nr - 1] + a.rlen[gi][nr - 1]) {
+        for (size_t j = 0; j < bits.size(); j++) {
+            if (nr > 0 && bits[j] == a.rsrc[gi][nr - 1] + a.rlen[gi][nr - 1]) {
                 a.rlen[gi][nr - 1]++;
                 continue;
             }
-            a.rsrc[gi][nr] = (uint8_t)G.bits[j];
+            a.rsrc[gi][nr] = (uint8_t)bits[j];
             a.rdst[gi][nr] = (uint8_t)j;
             a.rlen[gi][nr] = 1;
             nr++;
         }
         a.nruns[gi] = nr;
+        const auto &tab = pp.tabs[gi];
         double2 *d = nullptr;
         cuda_check(cudaMalloc(&d, sizeof(double2) * tab.size()), "cudaMalloc(init table)");
         cuda_check(cudaMemcpy(d, tab.data(), sizeof(double2) * tab.size(), cudaMemcpyHostToDevice), "upload init table");
@@ -585,13 +613,38 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     std::vector<Pending> tiles;
     std::vector<size_t> blob_fix;     // recs whose pointer must be rebased (streaming data)
 
-    for (const Step &st : p->sched.steps) {
+    // The product-state init fuses into the first tile pass when that pass comes right after it
+    // (JIT only): the pass computes its tiles' amplitudes instead of reading them, and the init's
+    // own full-state write disappears.
+    const auto &steps = p->sched.steps;
+    const bool fuse_init = use_jit && !getenv("HHLSV_NO_INIT_FUSE") && steps.size() >= 2 &&
+                           steps[0].kind == StepKind::InitProduct && steps[1].kind == StepKind::Tile;
+    InitSpec init_spec;
+    if (fuse_init) {
+        ProductPlan pp = plan_product(sv, steps[0], bscale);
+        init_spec.zero_mask = pp.zero_mask;
+        for (size_t g = 0; g < pp.tabs.size(); g++) {
+            init_spec.off.push_back(push_data(pp.tabs[g]));
+            init_spec.bits.push_back(pp.bits[g]);
+        }
+        p->sched.n_passes--;
+        p->sched.pass_bytes -= steps[0].bytes;
+    }
+    for (size_t si = 0; si < steps.size(); si++) {
+        const Step &st = steps[si];
         LaunchRec rec;
         rec.kind = st.kind;
         rec.bytes = st.bytes;
         switch (st.kind) {
             case StepKind::InitZero: break;
-            case StepKind::InitProduct: build_product(sv, p.get(), st, rec, bscale); break;
+            case StepKind::InitProduct:
+                if (fuse_init) {
+                    rec.skip = true;
+                    rec.bytes = 0.0;
+                } else {
+                    build_product(sv, p.get(), st, rec, bscale);
+                }
+                break;
             case StepKind::Exchange:
                 rec.gbit = st.gbit;
                 rec.lbit = st.lbit;
@@ -698,7 +751,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
                     JitPass jp;
                     jp.name = "hhlsv_tile";
-                    jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra);
+                    jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
+                                             (fuse_init && si == 1) ? &init_spec : nullptr);
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
                 }

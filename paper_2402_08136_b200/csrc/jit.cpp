@@ -184,7 +184,7 @@ bool jit_available(std::string *why) {
 
 // ---------------------------------------------------------------- codegen ----
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
-                            const std::vector<dev::RegOp> &ops, size_t *smem_extra) {
+                            const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init) {
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
@@ -247,6 +247,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
     int nbuf = 1;
     if (const char *e = getenv("HHLSV_JIT_NBUF")) nbuf = atoi(e) == 2 ? 2 : 1;
+    if (init) nbuf = 1;
     const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
                             dsub_max * 16;
     if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
@@ -301,8 +302,31 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
         k << "    const SArr cur = buf0;\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-        k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]);\n";
-        k << "    cp_async_commit();\n    cp_async_wait0();\n    bar();\n";
+        if (init) {      // fused product-state init: compute the tile instead of reading it
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") {\n      const u64 gi = gbase | addr(0ull, u);\n";
+            k << "      double2 amp = mk(0.0, 0.0);\n      if (!(gi & " << u64s(init->zero_mask) << ")) {\n";
+            for (size_t g = 0; g < init->off.size(); g++) {
+                // runs of consecutive bits: table bit j <- physical bit bits[j]
+                const auto &B = init->bits[g];
+                std::vector<uint8_t> src, len, dst;
+                for (size_t j = 0; j < B.size(); j++) {
+                    if (!src.empty() && B[j] == src.back() + len.back()) {
+                        len.back()++;
+                        continue;
+                    }
+                    src.push_back((uint8_t)B[j]);
+                    dst.push_back((uint8_t)j);
+                    len.push_back(1);
+                }
+                k << "        const double2 t" << g << " = __ldg(blob + " << init->off[g] << "ull + ("
+                  << runs_expr("gi", (int)src.size(), src.data(), len.data(), dst.data()) << "));\n";
+                k << "        amp = " << (g == 0 ? std::string("t0") : "cmul(amp, t" + std::to_string(g) + ")") << ";\n";
+            }
+            k << "      }\n      cur[swz(u)] = amp;\n    }\n    bar();\n";
+        } else {
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]);\n";
+            k << "    cp_async_commit();\n    cp_async_wait0();\n    bar();\n";
+        }
     }
     for (size_t p = 0; p < ph.size(); p++) {
         const dev::RegPhase &P = ph[p];

@@ -16,9 +16,18 @@ struct JitPass {
     size_t smem_extra = 0;     // total dynamic shared memory of the generated kernel (bytes)
 };
 
+// Product-state init fused into the first tile pass: the pass computes its tile's amplitudes
+// (prod_g table_g[gather_g(global index)], 0 where a zero_mask bit is set) instead of reading them.
+struct InitSpec {
+    uint64_t zero_mask = 0;
+    std::vector<size_t> off;                 // per group: blob offset of its table
+    std::vector<std::vector<int>> bits;      // per group: physical bits, table bit j <- bits[j]
+};
+
 bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
-                            const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr);
+                            const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr,
+                            const InitSpec *init = nullptr);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.

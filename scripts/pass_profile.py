@@ -34,7 +34,7 @@ for q, k, T, J, DK, FO in itertools.product(a.qpe, a.kmax, a.tile, a.jit, a.dk, 
             prog.run()
             t = prog.timings(with_flops=True)
         dump = prog.dump().splitlines()
-        heads = [ln for ln in dump if not ln.startswith("  ")]
+        heads = [ln for ln in dump if not ln.startswith(("  ", " |"))]
         total = sum(x[0] for x in t)
         import time as _t
         print(f"== {a.config} qpe={q} kmax={k} tile={T} jit={J} dk={DK} fold={FO}: {len(t)} steps, {prog.report['n_fused']} fused ops, "
