@@ -209,7 +209,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // shared sub-table over the run's varying tile bits V; each amplitude then does ONE lookup
     // and ONE complex multiply for the whole run. Used when 2^|V| is small.
     struct DRun { int p, a, b; std::vector<int> V; size_t off; };
-    std::vector<DRun> druns;
+    std::vector<DRun> druns, rtabs;
+    static const bool no_rtab = getenv("HHLSV_JIT_NORTAB") != nullptr;
     size_t dsub_max = 0;
     auto op_vary = [&](const dev::RegOp &op, const dev::RegPhase &P) {
         std::vector<int> v;
@@ -240,6 +241,17 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             oi = oj;
         }
+        // reciprocal rotation: its (s_m, c_m) pairs over the tile's clock bits precomputed per tile
+        // (one division + square root per table entry instead of one per clock value per thread)
+        for (int oi = ph[p].op0; oi < ph[p].op1; oi++) {
+            if (ops[oi].kind != 2 || no_rtab) continue;
+            std::vector<int> V = op_vary(ops[oi], ph[p]);
+            std::sort(V.begin(), V.end());
+            if (V.size() <= 9 && (1u << V.size()) <= 2u * (1u << (T - dev::kRegBits))) {
+                rtabs.push_back({(int)p, oi, oi + 1, V, used});
+                used += (size_t)1 << V.size();
+            }
+        }
         dsub_max = std::max(dsub_max, used);
     }
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
@@ -252,6 +264,27 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             dsub_max * 16;
     if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
     int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 512 / NTHR));
+    // Direct global I/O: when a phase's thread bits start with the tile's positions 0..2 and those are
+    // the physical bits 0..2 (8 lanes cover 128 contiguous bytes), the first phase loads its 16
+    // register amplitudes straight from HBM and the last phase stores them straight back; the tile
+    // never passes through shared memory on the way in/out (saves 2 of the pass's smem sweeps
+    // each way and the cp.async / store-loop address arithmetic).
+    bool low3 = T >= 4 && a.tbits[0] == 0 && a.tbits[1] == 1 && a.tbits[2] == 2;
+    if (const char *e = getenv("HHLSV_JIT_DIRECT")) low3 = low3 && atoi(e) != 0;
+    const bool din = nbuf == 1 && low3 && ph.front().R[0] >= 3;
+    const bool dout = nbuf == 1 && low3 && ph.back().R[0] >= 3;
+    auto tb_expr = [&](const dev::RegPhase &P) {
+        std::ostringstream o;
+        o << "0u";
+        for (int i = 0; i < T - dev::kRegBits; i++) o << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
+        return o.str();
+    };
+    auto phys_slot = [&](const dev::RegPhase &P, int j) {      // physical offset of register slot j
+        uint64_t c = 0;
+        for (int i = 0; i < dev::kRegBits; i++)
+            if ((j >> i) & 1) c |= 1ull << a.tbits[P.R[i]];
+        return c;
+    };
     if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
     std::ostringstream k;
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
@@ -285,6 +318,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
       << "]; };\n";
     k << "  bar();\n";
+    if (din) k << "  const u64 pd_in = addr(0ull, " << tb_expr(ph.front()) << ");\n";
+    if (dout) k << "  const u64 pd_out = addr(0ull, " << tb_expr(ph.back()) << ");\n";
     k << "  u64 tile = blockIdx.x;\n";
     if (nbuf == 2) {
         k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
@@ -302,7 +337,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
         k << "    const SArr cur = buf0;\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
-        if (init) {      // fused product-state init: compute the tile instead of reading it
+        if (din) {
+            // phase 0 reads (or, fused init, computes) its registers directly
+        } else if (init) {      // fused product-state init: compute the tile instead of reading it
             k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") {\n      const u64 gi = gbase | addr(0ull, u);\n";
             k << "      double2 amp = mk(0.0, 0.0);\n      if (!(gi & " << u64s(init->zero_mask) << ")) {\n";
             for (size_t g = 0; g < init->off.size(); g++) {
@@ -361,31 +398,56 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
         }
-        if (any_run) k << "      bar();\n";
-        for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
-        for (int oi = P.op0; oi < P.op1; oi++) {
-            const DRun *run = nullptr;
-            for (auto &dr : druns)
-                if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;
-            if (run) {
-                if (oi == run->a) {      // the whole run: one shared lookup + one complex multiply per slot
-                    const int nv = (int)run->V.size();
-                    k << "      { const u32 bt = 0u";
-                    for (int i = 0; i < nv; i++)
-                        if (std::find(P.R, P.R + 4, run->V[i]) == P.R + 4)
-                            k << " | (((tb >> " << run->V[i] << ") & 1u) << " << i << ")";
-                    k << "; // diagonal run of " << (run->b - run->a) << " ops\n";
-                    for (int j = 0; j < 16; j++) {
-                        int cj = 0;
-                        for (int i = 0; i < nv; i++)
-                            for (int r = 0; r < 4; r++)
-                                if (P.R[r] == run->V[i] && ((j >> r) & 1)) cj |= 1 << i;
-                        k << "        v" << j << " = cmul(dsub[" << run->off << " + (bt | " << cj << "u)], v" << j << ");\n";
-                    }
-                    k << "      }\n";
+        for (auto &rt : rtabs) {
+            if (rt.p != (int)p) continue;
+            any_run = true;
+            const dev::RegOp &op = ops[rt.a];
+            const int nv = (int)rt.V.size();
+            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
+            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << rt.V[i] << ")";
+            k << ";\n        const u64 m = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
+              << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
+            for (int i = 0; i < 4; i++)
+                if (op.ridx[1 << i]) {
+                    int ob = 0;
+                    while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
+                    k << " | ((u64)((loc >> " << P.R[i] << ") & 1u) << " << ob << ")";
                 }
-                continue;
+            k << ";\n        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n        const double s = recip_s(m, "
+              << op.n_c << ", pr.x, " << op.is_signed << ", pr.y);\n        dsub[" << rt.off
+              << " + c] = mk(s, sqrt(fma(-s, s, 1.0)));\n      }\n";
+        }
+        if (any_run) k << "      bar();\n";
+        if (p == 0 && din && init) {
+            for (int j = 0; j < 16; j++) {
+                k << "      double2 v" << j << " = mk(0.0, 0.0);\n      { const u64 gi = gbase | pd_in | " << u64s(phys_slot(P, j))
+                  << ";\n        if (!(gi & " << u64s(init->zero_mask) << ")) {\n";
+                for (size_t g = 0; g < init->off.size(); g++) {
+                    const auto &B = init->bits[g];
+                    std::vector<uint8_t> src, len, dst;
+                    for (size_t q = 0; q < B.size(); q++) {
+                        if (!src.empty() && B[q] == src.back() + len.back()) {
+                            len.back()++;
+                            continue;
+                        }
+                        src.push_back((uint8_t)B[q]);
+                        dst.push_back((uint8_t)q);
+                        len.push_back(1);
+                    }
+                    k << "          const double2 t" << g << " = __ldg(blob + " << init->off[g] << "ull + ("
+                      << runs_expr("gi", (int)src.size(), src.data(), len.data(), dst.data()) << "));\n";
+                    k << "          v" << j << " = " << (g == 0 ? std::string("t0") : "cmul(v" + std::to_string(j) + ", t" + std::to_string(g) + ")")
+                      << ";\n";
+                }
+                k << "        }\n      }\n";
             }
+        } else if (p == 0 && din) {
+            k << "      const double2 *gin = psi + (base | pd_in);\n";
+            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = __ldcs(gin + " << u64s(phys_slot(P, j)) << ");\n";
+        } else {
+            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+        }
+        auto emit_single = [&](int oi) {
             const dev::RegOp &op = ops[oi];
             std::ostringstream cond;
             if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
@@ -517,18 +579,38 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 } else {
                     int A = 0;
                     while (!((op.mask >> A) & 1)) A++;
-                    k << "        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n";
+                    const DRun *rt = nullptr;
+                    for (auto &r : rtabs)
+                        if (r.a == oi) rt = &r;
+                    if (!rt) k << "        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n";
+                    else {
+                        k << "        const u32 bt = 0u";
+                        for (size_t i = 0; i < rt->V.size(); i++)
+                            if (std::find(P.R, P.R + 4, rt->V[i]) == P.R + 4)
+                                k << " | (((tb >> " << rt->V[i] << ") & 1u) << " << i << ")";
+                        k << ";\n";
+                    }
                     // one division + square root per distinct clock value among the slot pairs
-                    // (once per thread when no clock bit is a register bit)
+                    // (once per thread when no clock bit is a register bit), or one lookup in the
+                    // tile's precomputed (s, c) table
                     std::map<uint32_t, int> sc;
                     for (int j = 0; j < 16; j++) {
                         if ((j >> A) & 1) continue;
                         if (sc.count(op.ridx[j])) continue;
                         const int id = (int)sc.size();
                         sc[op.ridx[j]] = id;
-                        k << "        const double s" << id << " = recip_s(ib | " << op.ridx[j] << "u, " << op.n_c
-                          << ", pr.x, " << op.is_signed << ", pr.y); const double c" << id << " = sqrt(fma(-s" << id
-                          << ", s" << id << ", 1.0));\n";
+                        if (rt) {
+                            int cj = 0;
+                            for (size_t i = 0; i < rt->V.size(); i++)
+                                for (int r = 0; r < 4; r++)
+                                    if (P.R[r] == rt->V[i] && ((j >> r) & 1)) cj |= 1 << i;
+                            k << "        const double2 sc" << id << " = dsub[" << rt->off << " + (bt | " << cj
+                              << "u)]; const double s" << id << " = sc" << id << ".x, c" << id << " = sc" << id << ".y;\n";
+                        } else {
+                            k << "        const double s" << id << " = recip_s(ib | " << op.ridx[j] << "u, " << op.n_c
+                              << ", pr.x, " << op.is_signed << ", pr.y); const double c" << id << " = sqrt(fma(-s" << id
+                              << ", s" << id << ", 1.0));\n";
+                        }
                     }
                     for (int j = 0; j < 16; j++) {
                         if ((j >> A) & 1) continue;
@@ -543,11 +625,141 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 }
             }
             k << "      }\n";
+        };
+        // Consecutive diagonal ops (not precomposed in a run) whose only conditions are register-slot
+        // controls are applied as ONE group: ops whose table value is the same on every slot they
+        // touch (e.g. CP-ladder chunks over thread / out-of-tile bits) are multiplied into one scalar
+        // per distinct slot set, and each slot then takes one complex multiply per distinct factor
+        // list (shared across slots) instead of one per op.
+        auto emit_group = [&](const std::vector<int> &G) {
+            k << "      { // diagonal group of " << G.size() << " ops\n";
+            std::vector<std::vector<std::string>> fac(16);
+            std::map<uint32_t, std::vector<int>> uni;
+            std::vector<int> var;
+            for (int oi : G) {
+                const dev::RegOp &op = ops[oi];
+                k << "        const u64 ib" << oi << " = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst)
+                  << ") | (" << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
+                uint32_t m = 0;
+                std::vector<uint32_t> rs;
+                for (int j = 0; j < 16; j++)
+                    if ((j & op.rcm) == op.rcv) {
+                        m |= 1u << j;
+                        if (std::find(rs.begin(), rs.end(), op.ridx[j]) == rs.end()) rs.push_back(op.ridx[j]);
+                    }
+                if (rs.size() == 1) uni[m].push_back(oi);
+                else var.push_back(oi);
+            }
+            int nu = 0;
+            for (auto &kv : uni) {
+                const std::string U = "U" + std::to_string(nu++);
+                bool first = true;
+                for (int oi : kv.second) {
+                    const dev::RegOp &op = ops[oi];
+                    int j0 = 0;
+                    while (!((kv.first >> j0) & 1u)) j0++;
+                    const std::string ld = "__ldg(blob + " + std::to_string(op.data_off) + "ull + (ib" + std::to_string(oi) +
+                                           " | " + std::to_string(op.ridx[j0]) + "u))";
+                    if (first) k << "        double2 " << U << " = " << ld << ";\n";
+                    else k << "        " << U << " = cmul(" << U << ", " << ld << ");\n";
+                    first = false;
+                }
+                for (int j = 0; j < 16; j++)
+                    if ((kv.first >> j) & 1u) fac[j].push_back(U);
+            }
+            for (int oi : var) {
+                const dev::RegOp &op = ops[oi];
+                std::map<uint32_t, std::string> sym;
+                for (int j = 0; j < 16; j++) {
+                    if ((j & op.rcm) != op.rcv) continue;
+                    auto it = sym.find(op.ridx[j]);
+                    if (it == sym.end()) {
+                        const std::string L = "L" + std::to_string(oi) + "_" + std::to_string(op.ridx[j]);
+                        k << "        const double2 " << L << " = __ldg(blob + " << op.data_off << "ull + (ib" << oi << " | "
+                          << op.ridx[j] << "u));\n";
+                        it = sym.emplace(op.ridx[j], L).first;
+                    }
+                    fac[j].push_back(it->second);
+                }
+            }
+            std::map<std::vector<std::string>, std::string> prod;
+            int nf = 0;
+            for (int j = 0; j < 16; j++) {
+                if (fac[j].empty()) continue;
+                std::string f = fac[j][0];
+                for (size_t q = 1; q < fac[j].size(); q++) {
+                    std::vector<std::string> key(fac[j].begin(), fac[j].begin() + q + 1);
+                    auto it = prod.find(key);
+                    if (it == prod.end()) {
+                        const std::string F = "F" + std::to_string(nf++);
+                        k << "        const double2 " << F << " = cmul(" << f << ", " << fac[j][q] << ");\n";
+                        it = prod.emplace(key, F).first;
+                    }
+                    f = it->second;
+                }
+                k << "        v" << j << " = cmul(" << f << ", v" << j << ");\n";
+            }
+            k << "      }\n";
+        };
+        static const bool group_on = !getenv("HHLSV_JIT_NOGROUP");
+        for (int oi = P.op0; oi < P.op1; oi++) {
+            const DRun *run = nullptr;
+            for (auto &dr : druns)
+                if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;
+            if (run) {
+                if (oi == run->a) {      // the whole run: one shared lookup + one complex multiply per slot
+                    const int nv = (int)run->V.size();
+                    k << "      { const u32 bt = 0u";
+                    for (int i = 0; i < nv; i++)
+                        if (std::find(P.R, P.R + 4, run->V[i]) == P.R + 4)
+                            k << " | (((tb >> " << run->V[i] << ") & 1u) << " << i << ")";
+                    k << "; // diagonal run of " << (run->b - run->a) << " ops\n";
+                    for (int j = 0; j < 16; j++) {
+                        bool touched = false;      // slots outside every op's register controls keep factor 1
+                        for (int q = run->a; q < run->b; q++)
+                            if ((j & ops[q].rcm) == ops[q].rcv) touched = true;
+                        if (!touched) continue;
+                        int cj = 0;
+                        for (int i = 0; i < nv; i++)
+                            for (int r = 0; r < 4; r++)
+                                if (P.R[r] == run->V[i] && ((j >> r) & 1)) cj |= 1 << i;
+                        k << "        v" << j << " = cmul(dsub[" << run->off << " + (bt | " << cj << "u)], v" << j << ");\n";
+                    }
+                    k << "      }\n";
+                }
+                continue;
+            }
+            if (group_on && ops[oi].kind == 1) {
+                auto in_run = [&](int q) {
+                    for (auto &dr : druns)
+                        if (dr.p == (int)p && q >= dr.a && q < dr.b) return true;
+                    return false;
+                };
+                int oj = oi;
+                while (oj < P.op1 && ops[oj].kind == 1 && !in_run(oj)) oj++;
+                std::vector<int> G, C;
+                for (int q = oi; q < oj; q++) (ops[q].gcm || ops[q].tcm ? C : G).push_back(q);
+                if (G.size() >= 2) {
+                    emit_group(G);
+                    for (int q : C) emit_single(q);
+                    oi = oj - 1;
+                    continue;
+                }
+            }
+            emit_single(oi);
         }
-        for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
-        k << "      bar();\n    }\n";
+        if (p + 1 == ph.size() && dout) {
+            k << "      double2 *gout = psi + (base | pd_out);\n";
+            for (int j = 0; j < 16; j++) k << "      __stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+            k << "    }\n";
+        } else {
+            for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
+            k << "      bar();\n    }\n";
+        }
     }
-    k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+    if (!dout) k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+    // one barrier per tile: the next tile's first shared-memory write (cp.async, phase-0 stores,
+    // diagonal sub-tables) must not overtake a slower warp still reading this tile's last phase
     k << "    bar();\n  }\n  cp_async_wait0();\n}\n";
     return k.str();
 }

@@ -6,5 +6,5 @@ from workloads import configs  # noqa: E402
 A, b, nc = configs.get("S30")
 for i in range(3):
     t = time.perf_counter()
-    x, rep = pkg.hhl_solve(A, b, clock_qubits=nc, qpe_mode=1, fusion_kmax=1, tile_qubits=11)
+    x, rep = pkg.hhl_solve(A, b, clock_qubits=nc, qpe_mode=1, fusion_kmax=1, tile_qubits=12)
     print(f"solve {i}: {time.perf_counter() - t:.3f} s  frontend {rep['t_frontend_s']*1e3:.1f} ms  sim {rep['t_sim_s']*1e3:.1f} ms", flush=True)
