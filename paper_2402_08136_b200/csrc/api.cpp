@@ -244,7 +244,8 @@ static std::string jit_check_schedule(const Schedule &s) {
         std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
         std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
         std::string err;
-        auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops), err);
+        std::vector<std::pair<uint64_t, uint64_t>> cwide;
+        auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops, nullptr, nullptr, &cwide), err);
         if (cubin.empty()) fail(SV_E_CUDA, err);
         jitlog += "JIT_PASS phases=" + std::to_string(lph.size()) + " regops=" + std::to_string(lops.size()) +
                   " cubin_bytes=" + std::to_string(cubin.size()) + "\n";

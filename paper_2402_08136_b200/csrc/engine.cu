@@ -752,7 +752,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     JitPass jp;
                     jp.name = "hhlsv_tile";
                     jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
-                                             (fuse_init && si == 1) ? &init_spec : nullptr);
+                                             (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide);
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
                 }

@@ -107,6 +107,7 @@ __device__ __forceinline__ u64 lds64(u32 a) {
     return v;
 }
 __device__ __forceinline__ void sts64(u32 a, u64 v) { asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v)); }
+__device__ __forceinline__ void stsd(u32 a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
 __device__ __forceinline__ void bar() { asm volatile("bar.sync 0;" ::: "memory"); }
 struct SRef {
     u32 a;
@@ -184,7 +185,8 @@ bool jit_available(std::string *why) {
 
 // ---------------------------------------------------------------- codegen ----
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
-                            const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init) {
+                            const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init,
+                            std::vector<std::pair<uint64_t, uint64_t>> *cwide) {
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
@@ -193,9 +195,34 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         if (op.kind == 0 && ((op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1)) >= 3)
             wide_ops++;
     // wide-op matrices staged once per (persistent) CTA in shared memory when few (<= 4 x 4 KB)
+    // Wide-op matrices as constant-bank operands (DFMA reads them straight from the constant cache:
+    // no shared-memory or L1 traffic for the matrix), up to 64 KB per pass module.
+    std::map<int, size_t> cstage;      // op index -> offset (double2 units) in cw[]
+    size_t ctot = 0;
+    static const bool no_cw = getenv("HHLSV_JIT_NOCW") != nullptr;
+    if (cwide && !no_cw) {
+        for (size_t i = 0; i < ops.size(); i++) {
+            const auto &op = ops[i];
+            const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            if (op.kind == 0 && Kk >= 3) {
+                cstage[(int)i] = ctot;
+                ctot += (size_t)1 << (2 * Kk);
+            }
+        }
+        if (ctot > 4096) {
+            cstage.clear();
+            ctot = 0;
+        }
+        cwide->clear();
+        for (auto &kv : cstage) {
+            const auto &op = ops[kv.first];
+            const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            cwide->push_back({op.data_off, (uint64_t)1 << (2 * Kk)});
+        }
+    }
     std::map<int, size_t> wstage;      // op index -> offset (double2 units) in the staging region
     size_t wtot = 0;
-    if (wide_ops <= 4)
+    if (wide_ops <= 4 && cstage.empty())
         for (size_t i = 0; i < ops.size(); i++) {
             const auto &op = ops[i];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
@@ -272,6 +299,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     bool low3 = T >= 4 && a.tbits[0] == 0 && a.tbits[1] == 1 && a.tbits[2] == 2;
     if (const char *e = getenv("HHLSV_JIT_DIRECT")) low3 = low3 && atoi(e) != 0;
     const bool din = nbuf == 1 && low3 && ph.front().R[0] >= 3;
+    static const bool pf_on = !getenv("HHLSV_JIT_NOPF");
     const bool dout = nbuf == 1 && low3 && ph.back().R[0] >= 3;
     auto tb_expr = [&](const dev::RegPhase &P) {
         std::ostringstream o;
@@ -287,6 +315,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     };
     if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
     std::ostringstream k;
+    if (ctot) k << "__constant__ double2 cw[" << ctot << "];\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
@@ -306,8 +335,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         for (auto &kv : wstage) {
             const auto &op = ops[kv.first];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
-            k << "  for (int i = threadIdx.x; i < " << (1 << (2 * Kk)) << "; i += " << NTHR << ") wm[" << kv.second
-              << " + i] = blob[" << op.data_off << "ull + i];\n";
+            if (op.is_signed)      // real matrix: column-major plain doubles
+                k << "  for (int i = threadIdx.x; i < " << (1 << (2 * Kk)) << "; i += " << NTHR << ") stsd(wm.b + "
+                  << kv.second * 16 << "u + (u32)(((i % " << (1 << Kk) << ") * " << (1 << Kk) << ") + i / " << (1 << Kk)
+                  << ") * 8u, blob[" << op.data_off << "ull + i].x);\n";
+            else
+                k << "  for (int i = threadIdx.x; i < " << (1 << (2 * Kk)) << "; i += " << NTHR << ") wm[" << kv.second
+                  << " + i] = blob[" << op.data_off << "ull + i];\n";
         }
     }
     if (dsub_max)
@@ -337,6 +371,21 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
         k << "    const SArr cur = buf0;\n";
         k << "    const u64 base = tile_base(tile);\n    const u64 gbase = rank_base | base;\n    (void)gbase;\n";
+        // L2 prefetch of this CTA's next tile: its HBM reads overlap this tile's compute, and the
+        // next tile's loads then hit L2 (296 CTAs x 64 KB in flight << 126 MB L2)
+        if (pf_on && !init) {
+            k << "    if (tile + gridDim.x < n_tiles) {\n      const u64 nb = tile_base(tile + gridDim.x);\n";
+            if (din) {
+                k << "      if ((threadIdx.x & 7u) == 0u) { const char *g = (const char *)(psi + (nb | pd_in));";
+                for (int j = 0; j < 16; j++)
+                    k << " asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(g + " << u64s(16 * phys_slot(ph.front(), j)) << "));";
+                k << " }\n";
+            } else {
+                k << "      for (u32 u = threadIdx.x * 8u; u < NT; u += " << 8 * NTHR
+                  << "u) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(psi + addr(nb, u)));\n";
+            }
+            k << "    }\n";
+        }
         if (din) {
             // phase 0 reads (or, fused init, computes) its registers directly
         } else if (init) {      // fused product-state init: compute the tile instead of reading it
@@ -518,7 +567,65 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         };
                         k << "        {\n";
                         auto ws0 = wstage.find(oi);
-                        if (true) {   // rolled row loop: bounded registers (inputs stay in v) and code size
+                        auto cs0 = cstage.find(oi);
+                        if (cs0 != cstage.end()) {
+                            // fully unrolled blocks of RU rows, matrix entries as constant-bank operands
+                            const int RU = real ? 4 : 2;
+                            for (int r0 = 0; r0 < D; r0 += RU) {
+                                k << "          {";
+                                for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
+                                k << "\n";
+                                for (int cc = 0; cc < D; cc++) {
+                                    const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
+                                    k << "           ";
+                                    for (int q = 0; q < RU; q++) {
+                                        const std::string w = "cw[" + std::to_string(cs0->second + (size_t)(r0 + q) * D + cc) + "]";
+                                        if (real)
+                                            k << " ax" << q << " = fma(" << w << ".x, " << in << ".x, ax" << q << "); ay" << q << " = fma(" << w
+                                              << ".x, " << in << ".y, ay" << q << ");";
+                                        else
+                                            k << " ax" << q << " = fma(" << w << ".x, " << in << ".x, ax" << q << "); ax" << q << " = fma(-" << w
+                                              << ".y, " << in << ".y, ax" << q << "); ay" << q << " = fma(" << w << ".x, " << in << ".y, ay" << q
+                                              << "); ay" << q << " = fma(" << w << ".y, " << in << ".x, ay" << q << ");";
+                                    }
+                                    k << "\n";
+                                }
+                                for (int q = 0; q < RU; q++)
+                                    k << "            cur[swz(tb | " << rd[g | dep_slot(r0 + q, M)] << "u)] = mk(ax" << q << ", ay" << q << ");\n";
+                                k << "          }\n";
+                            }
+                        } else if (ws0 != wstage.end()) {
+                            // rolled loop over blocks of RU rows with RU independent accumulator pairs
+                            // (ILP for the FMA chains); a real matrix is staged column-major as plain
+                            // doubles so one 16-byte shared load feeds two rows
+                            const int RU = real ? 4 : 2;
+                            const std::string wb = "wm.b + " + std::to_string(ws0->second * 16) + "u";
+                            k << "          #pragma unroll 1\n          for (int r = 0; r < " << D << "; r += " << RU << ") {";
+                            for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
+                            k << "\n";
+                            for (int cc = 0; cc < D; cc++) {
+                                const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
+                                if (real) {
+                                    k << "            { const u32 wa = " << wb << " + (u32)(" << cc * D << " + r) * 8u; const double2 w01 = lds(wa), w23 = lds(wa + 16u);"
+                                      << " ax0 = fma(w01.x, " << in << ".x, ax0); ay0 = fma(w01.x, " << in << ".y, ay0);"
+                                      << " ax1 = fma(w01.y, " << in << ".x, ax1); ay1 = fma(w01.y, " << in << ".y, ay1);"
+                                      << " ax2 = fma(w23.x, " << in << ".x, ax2); ay2 = fma(w23.x, " << in << ".y, ay2);"
+                                      << " ax3 = fma(w23.y, " << in << ".x, ax3); ay3 = fma(w23.y, " << in << ".y, ay3); }\n";
+                                } else {
+                                    for (int q = 0; q < RU; q++)
+                                        k << "            { const double2 w = lds(" << wb << " + (u32)((r + " << q << ") * " << D << " + " << cc
+                                          << ") * 16u); ax" << q << " = fma(w.x, " << in << ".x, ax" << q << "); ax" << q << " = fma(-w.y, "
+                                          << in << ".y, ax" << q << "); ay" << q << " = fma(w.x, " << in << ".y, ay" << q << "); ay" << q
+                                          << " = fma(w.y, " << in << ".x, ay" << q << "); }\n";
+                                }
+                            }
+                            for (int q = 0; q < RU; q++) {
+                                k << "            { const u32 rr = (u32)r + " << q << "u; const u32 slot = " << rd[g] << "u";
+                                for (int i = 0; i < K; i++) k << " | ((rr >> " << i << ") & 1u) << " << Rpos[i];
+                                k << "; cur[swz(tb | slot)] = mk(ax" << q << ", ay" << q << "); }\n";
+                            }
+                            k << "          }\n";
+                        } else if (true) {   // rolled row loop: bounded registers (inputs stay in v) and code size
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
                               << "; r++) { double ax = 0.0, ay = 0.0; const auto Ur = "
                               << (ws0 != wstage.end() ? "wm + " + std::to_string(ws0->second) + "u" : std::string("U"))
@@ -873,6 +980,7 @@ void jit_build(std::vector<JitPass> &passes) {
             fail(SV_E_CUDA, "tile JIT failed: " + ents[i]->err);
         }
         passes[i].kern = ents[i]->kern;
+        passes[i].lib = ents[i]->lib;
     }
 }
 
@@ -894,6 +1002,18 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)148 * per_sm;
     if (grid > n_tiles) grid = n_tiles;
+    if (!p.cwide.empty()) {
+        void *cw = nullptr;
+        size_t cbytes = 0;
+        e = cudaLibraryGetGlobal(&cw, &cbytes, p.lib, "cw");
+        if (e != cudaSuccess) return e;
+        size_t off = 0;
+        for (auto &c : p.cwide) {
+            e = cudaMemcpyAsync((char *)cw + off * 16, blob + c.first, c.second * 16, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return e;
+            off += c.second;
+        }
+    }
     void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base};
     return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }

@@ -14,6 +14,10 @@ struct JitPass {
     std::string src;
     cudaKernel_t kern = nullptr;
     size_t smem_extra = 0;     // total dynamic shared memory of the generated kernel (bytes)
+    // wide (>= 3-target) dense matrices read as constant-bank operands: (blob offset, entries) copied
+    // in order into the pass module's __constant__ cw[] on the launch stream before every launch
+    std::vector<std::pair<uint64_t, uint64_t>> cwide;
+    cudaLibrary_t lib = nullptr;
 };
 
 // Product-state init fused into the first tile pass: the pass computes its tile's amplitudes
@@ -27,7 +31,8 @@ struct InitSpec {
 bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr,
-                            const InitSpec *init = nullptr);
+                            const InitSpec *init = nullptr,
+                            std::vector<std::pair<uint64_t, uint64_t>> *cwide = nullptr);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.
