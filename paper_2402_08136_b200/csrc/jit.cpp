@@ -239,6 +239,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     std::vector<DRun> druns, rtabs;
     static const bool no_rtab = getenv("HHLSV_JIT_NORTAB") != nullptr;
     size_t dsub_max = 0;
+    std::vector<size_t> used_ph;
     auto op_vary = [&](const dev::RegOp &op, const dev::RegPhase &P) {
         std::vector<int> v;
         for (int i = 0; i < 4; i++)
@@ -280,6 +281,28 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
         }
         dsub_max = std::max(dsub_max, used);
+        used_ph.push_back(used);
+    }
+    // Hoisted sub-tables (default): phase p+1's tables are built at the end of phase p (the next
+    // tile's phase-0 tables at the end of the last phase) into a region phase p-1 no longer reads,
+    // so the barrier that ends phase p also publishes them: no separate barrier per sub-table build.
+    // Regions alternate 0/1 by phase; with an odd phase count the last phase takes region 2.
+    const size_t nph = ph.size();
+    bool hoist = nph >= 2 && !getenv("HHLSV_JIT_NOHOIST");
+    auto region = [&](size_t q) { return (nph % 2 == 1 && q + 1 == nph) ? 2 : (int)(q % 2); };
+    if (hoist) {
+        size_t R[3] = {0, 0, 0};
+        for (size_t q = 0; q < nph; q++) R[region(q)] = std::max(R[region(q)], used_ph[q]);
+        const size_t B[3] = {0, R[0], R[0] + R[1]};
+        const size_t tot = R[0] + R[1] + R[2];
+        // keep two CTAs per SM: (tile + dep tables + staging + sub-tables) <= 113 KB
+        if (16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 + tot * 16 > 113 * 1024)
+            hoist = false;
+        else {
+            for (auto &d : druns) d.off += B[region(d.p)];
+            for (auto &d : rtabs) d.off += B[region(d.p)];
+            dsub_max = tot;
+        }
     }
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
     // compute phases (default; measured faster than double buffering at half the occupancy),
@@ -354,7 +377,59 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     k << "  bar();\n";
     if (din) k << "  const u64 pd_in = addr(0ull, " << tb_expr(ph.front()) << ");\n";
     if (dout) k << "  const u64 pd_out = addr(0ull, " << tb_expr(ph.back()) << ");\n";
+    auto emit_pre = [&](size_t pp, const std::string &gb) {     // per-tile sub-tables of phase pp
+            const dev::RegPhase &Q = ph[pp];
+            bool any_run = false;
+            k << "      { const u64 gpre = " << gb << "; (void)gpre;\n";
+        for (auto &dr : druns) {
+            if (dr.p != (int)pp) continue;
+            any_run = true;
+            const int nv = (int)dr.V.size();
+            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
+            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << dr.V[i] << ")";
+            k << ";\n        double2 acc = mk(1.0, 0.0);\n";
+            for (int oi = dr.a; oi < dr.b; oi++) {
+                const dev::RegOp &op = ops[oi];
+                k << "        { const u64 ib = (" << runs_expr("gpre", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
+                  << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
+                for (int i = 0; i < 4; i++)
+                    if (op.ridx[1 << i]) {
+                        int ob = 0;
+                        while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
+                        k << " | ((u64)((loc >> " << Q.R[i] << ") & 1u) << " << ob << ")";
+                    }
+                k << "; acc = cmul(acc, __ldg(blob + " << op.data_off << "ull + ib)); }\n";
+            }
+            k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
+        }
+        for (auto &rt : rtabs) {
+            if (rt.p != (int)pp) continue;
+            any_run = true;
+            const dev::RegOp &op = ops[rt.a];
+            const int nv = (int)rt.V.size();
+            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
+            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << rt.V[i] << ")";
+            k << ";\n        const u64 m = (" << runs_expr("gpre", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
+              << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
+            for (int i = 0; i < 4; i++)
+                if (op.ridx[1 << i]) {
+                    int ob = 0;
+                    while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
+                    k << " | ((u64)((loc >> " << Q.R[i] << ") & 1u) << " << ob << ")";
+                }
+            k << ";\n        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n        const double s = recip_s(m, "
+              << op.n_c << ", pr.x, " << op.is_signed << ", pr.y);\n        dsub[" << rt.off
+              << " + c] = mk(s, sqrt(fma(-s, s, 1.0)));\n      }\n";
+        }
+            k << "      }\n";
+            return any_run;
+        };
     k << "  u64 tile = blockIdx.x;\n";
+    if (hoist) {
+        k << "  if (tile < n_tiles) {\n";
+        emit_pre(0, "rank_base | tile_base(tile)");
+        k << "  }\n  bar();\n";
+    }
     if (nbuf == 2) {
         k << "  if (tile < n_tiles) { const u64 b0 = tile_base(tile); for (u32 u = threadIdx.x; u < NT; u += " << NTHR
           << ") cp_async16s(buf0.at(swz(u)), &psi[addr(b0, u)]); }\n";
@@ -425,48 +500,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (int i = 0; i < 4; i++)
                 if ((j >> i) & 1) rd[j] |= 1 << P.R[i];
         }
-        bool any_run = false;
-        for (auto &dr : druns) {
-            if (dr.p != (int)p) continue;
-            any_run = true;
-            const int nv = (int)dr.V.size();
-            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
-            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << dr.V[i] << ")";
-            k << ";\n        double2 acc = mk(1.0, 0.0);\n";
-            for (int oi = dr.a; oi < dr.b; oi++) {
-                const dev::RegOp &op = ops[oi];
-                k << "        { const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
-                  << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
-                for (int i = 0; i < 4; i++)
-                    if (op.ridx[1 << i]) {
-                        int ob = 0;
-                        while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
-                        k << " | ((u64)((loc >> " << P.R[i] << ") & 1u) << " << ob << ")";
-                    }
-                k << "; acc = cmul(acc, __ldg(blob + " << op.data_off << "ull + ib)); }\n";
-            }
-            k << "        dsub[" << dr.off << " + c] = acc;\n      }\n";
+        if (!hoist) {
+            if (emit_pre(p, "gbase")) k << "      bar();\n";
         }
-        for (auto &rt : rtabs) {
-            if (rt.p != (int)p) continue;
-            any_run = true;
-            const dev::RegOp &op = ops[rt.a];
-            const int nv = (int)rt.V.size();
-            k << "      for (u32 c = threadIdx.x; c < " << (1u << nv) << "u; c += " << NTHR << ") {\n        const u32 loc = 0u";
-            for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << rt.V[i] << ")";
-            k << ";\n        const u64 m = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
-              << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
-            for (int i = 0; i < 4; i++)
-                if (op.ridx[1 << i]) {
-                    int ob = 0;
-                    while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
-                    k << " | ((u64)((loc >> " << P.R[i] << ") & 1u) << " << ob << ")";
-                }
-            k << ";\n        const double2 pr = __ldg(blob + " << op.data_off << "ull);\n        const double s = recip_s(m, "
-              << op.n_c << ", pr.x, " << op.is_signed << ", pr.y);\n        dsub[" << rt.off
-              << " + c] = mk(s, sqrt(fma(-s, s, 1.0)));\n      }\n";
-        }
-        if (any_run) k << "      bar();\n";
+
         if (p == 0 && din && init) {
             for (int j = 0; j < 16; j++) {
                 k << "      double2 v" << j << " = mk(0.0, 0.0);\n      { const u64 gi = gbase | pd_in | " << u64s(phys_slot(P, j))
@@ -855,12 +892,25 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             emit_single(oi);
         }
+        // hoisted sub-table build for the next phase (or the next tile's phase 0) after this phase's
+        // registers are stored (they are dead: no extra register pressure), before the barrier
+        auto hoisted = [&] {
+            if (!hoist) return;
+            if (p + 1 < nph) emit_pre(p + 1, "gbase");
+            else {
+                k << "      if (tile + gridDim.x < n_tiles) {\n";
+                emit_pre(0, "rank_base | tile_base(tile + gridDim.x)");
+                k << "      }\n";
+            }
+        };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
             for (int j = 0; j < 16; j++) k << "      __stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+            hoisted();
             k << "    }\n";
         } else {
             for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
+            hoisted();
             k << "      bar();\n    }\n";
         }
     }
