@@ -41,6 +41,17 @@ static void state_free(void *p, cudaStream_t s) {
     else cudaFreeAsync(p, s);
 }
 
+// Small per-state / per-program device buffers also come from the stream-ordered pool: a plain
+// cudaFree is device-synchronising and (measured) can stall for ~0.2 s when the driver trims
+// memory after a 16 GiB state was released; pool frees are stream-ordered and cheap.
+static cudaError_t pool_malloc(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    return state_alloc(p, bytes, s, dev);
+}
+static void pool_free(void *p, cudaStream_t s) { state_free(p, s); }
+
 sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zero_init) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
@@ -90,8 +101,8 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
             v->phys = sv->phys;
             cuda_check(state_alloc((void **)&v->psi, bytes, stream, device), "alloc(virtual shard)");
             v->red_len = dev::kRedBlocks;
-            cuda_check(cudaMalloc(&v->d_red, sizeof(double) * v->red_len), "cudaMalloc(red)");
-            cuda_check(cudaMalloc(&v->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
+            cuda_check(pool_malloc((void **)&v->d_red, sizeof(double) * v->red_len, stream), "cudaMalloc(red)");
+            cuda_check(pool_malloc((void **)&v->d_scalar, sizeof(double) * 8, stream), "cudaMalloc(scalar)");
             sv->views.push_back(v.release());
         }
         sv->psi = sv->views[0]->psi;
@@ -99,8 +110,8 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
         cuda_check(state_alloc((void **)&sv->psi, bytes, stream, device), "alloc(state)");
     }
     sv->red_len = dev::kRedBlocks;
-    cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * sv->red_len), "cudaMalloc(red)");
-    cuda_check(cudaMalloc(&sv->d_scalar, sizeof(double) * 8), "cudaMalloc(scalar)");
+    cuda_check(pool_malloc((void **)&sv->d_red, sizeof(double) * sv->red_len, stream), "cudaMalloc(red)");
+    cuda_check(pool_malloc((void **)&sv->d_scalar, sizeof(double) * 8, stream), "cudaMalloc(scalar)");
     if (world > 1 && !virt) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
     if (zero_init) state_reset(sv.get());
     return sv.release();
@@ -115,11 +126,11 @@ void state_destroy(sv_state *sv) {
         sv->psi = nullptr;
     }
     state_free(sv->psi, sv->stream);
-    cudaFree(sv->d_red);
-    cudaFree(sv->d_scalar);
-    cudaFree(sv->d_io);
-    cudaFree(sv->d_xsend);
-    cudaFree(sv->d_xrecv);
+    pool_free(sv->d_red, sv->stream);
+    pool_free(sv->d_scalar, sv->stream);
+    pool_free(sv->d_io, sv->stream);
+    pool_free(sv->d_xsend, sv->stream);
+    pool_free(sv->d_xrecv, sv->stream);
     nccl_destroy(sv->comm);
     delete sv;
 }
@@ -135,18 +146,18 @@ void state_reset(sv_state *sv) {
 
 static void ensure_io(sv_state *sv, size_t n2) {
     if (sv->io_len >= n2) return;
-    cudaFree(sv->d_io);
+    pool_free(sv->d_io, sv->stream);
     sv->d_io = nullptr;
     sv->io_len = 0;
-    cuda_check(cudaMalloc(&sv->d_io, sizeof(double2) * n2), "cudaMalloc(io)");
+    cuda_check(pool_malloc((void **)&sv->d_io, sizeof(double2) * n2, sv->stream), "cudaMalloc(io)");
     sv->io_len = n2;
 }
 
 static void ensure_red(sv_state *sv, size_t n) {
     if (sv->red_len >= n) return;
-    cudaFree(sv->d_red);
+    pool_free(sv->d_red, sv->stream);
     sv->d_red = nullptr;
-    cuda_check(cudaMalloc(&sv->d_red, sizeof(double) * n), "cudaMalloc(red)");
+    cuda_check(pool_malloc((void **)&sv->d_red, sizeof(double) * n, sv->stream), "cudaMalloc(red)");
     sv->red_len = n;
 }
 
@@ -162,11 +173,11 @@ static void exchange(sv_state *sv, int gbit, int lbit) {
     const uint64_t half = sv->local_amps() >> 1;
     const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);   // 1 GiB
     if (sv->x_len < chunk) {
-        cudaFree(sv->d_xsend);
-        cudaFree(sv->d_xrecv);
+        pool_free(sv->d_xsend, sv->stream);
+        pool_free(sv->d_xrecv, sv->stream);
         sv->d_xsend = sv->d_xrecv = nullptr;
-        cuda_check(cudaMalloc(&sv->d_xsend, sizeof(double2) * chunk), "cudaMalloc(xsend)");
-        cuda_check(cudaMalloc(&sv->d_xrecv, sizeof(double2) * chunk), "cudaMalloc(xrecv)");
+        cuda_check(pool_malloc((void **)&sv->d_xsend, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xsend)");
+        cuda_check(pool_malloc((void **)&sv->d_xrecv, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xrecv)");
         sv->x_len = chunk;
     }
     const bool top = lbit == sv->nloc - 1;
@@ -197,11 +208,11 @@ static void virtual_exchange(sv_state *sv, int gbit, int lbit) {
     const uint64_t half = sv->local_amps() >> 1;
     const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);
     if (sv->x_len < chunk) {
-        cudaFree(sv->d_xsend);
-        cudaFree(sv->d_xrecv);
+        pool_free(sv->d_xsend, sv->stream);
+        pool_free(sv->d_xrecv, sv->stream);
         sv->d_xsend = sv->d_xrecv = nullptr;
-        cuda_check(cudaMalloc(&sv->d_xsend, sizeof(double2) * chunk), "cudaMalloc(xsend)");
-        cuda_check(cudaMalloc(&sv->d_xrecv, sizeof(double2) * chunk), "cudaMalloc(xrecv)");
+        cuda_check(pool_malloc((void **)&sv->d_xsend, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xsend)");
+        cuda_check(pool_malloc((void **)&sv->d_xrecv, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xrecv)");
         sv->x_len = chunk;
     }
     for (int r = 0; r < sv->vworld; r++) {
@@ -359,7 +370,7 @@ static void build_product(sv_state *sv, sv_program *p, const Step &st, LaunchRec
         a.nruns[gi] = nr;
         const auto &tab = pp.tabs[gi];
         double2 *d = nullptr;
-        cuda_check(cudaMalloc(&d, sizeof(double2) * tab.size()), "cudaMalloc(init table)");
+        cuda_check(pool_malloc((void **)&d, sizeof(double2) * tab.size(), p->sv->stream), "cudaMalloc(init table)");
         cuda_check(cudaMemcpy(d, tab.data(), sizeof(double2) * tab.size(), cudaMemcpyHostToDevice), "upload init table");
         p->d_tabs.push_back(d);
         p->h2d_bytes += sizeof(double2) * tab.size();
@@ -753,6 +764,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     jp.name = "hhlsv_tile";
                     jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
                                              (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide);
+                    for (auto &c : jp.cwide)
+                        jp.cwvals.insert(jp.cwvals.end(), blob.begin() + c.first, blob.begin() + c.first + c.second);
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
                 }
@@ -765,17 +778,17 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     }
     // upload blob and tile ops, then rebase pointers
     if (!blob.empty()) {
-        cuda_check(cudaMalloc(&p->d_blob, sizeof(double2) * blob.size()), "cudaMalloc(blob)");
+        cuda_check(pool_malloc((void **)&p->d_blob, sizeof(double2) * blob.size(), p->sv->stream), "cudaMalloc(blob)");
         cuda_check(cudaMemcpy(p->d_blob, blob.data(), sizeof(double2) * blob.size(), cudaMemcpyHostToDevice),
                    "upload blob");
     }
     if (!rops.empty()) {
-        cuda_check(cudaMalloc(&p->d_ops, sizeof(dev::RegOp) * rops.size()), "cudaMalloc(tile ops)");
+        cuda_check(pool_malloc((void **)&p->d_ops, sizeof(dev::RegOp) * rops.size(), p->sv->stream), "cudaMalloc(tile ops)");
         cuda_check(cudaMemcpy(p->d_ops, rops.data(), sizeof(dev::RegOp) * rops.size(), cudaMemcpyHostToDevice),
                    "upload tile ops");
     }
     if (!phases.empty()) {
-        cuda_check(cudaMalloc(&p->d_phases, sizeof(dev::RegPhase) * phases.size()), "cudaMalloc(phases)");
+        cuda_check(pool_malloc((void **)&p->d_phases, sizeof(dev::RegPhase) * phases.size(), p->sv->stream), "cudaMalloc(phases)");
         cuda_check(cudaMemcpy(p->d_phases, phases.data(), sizeof(dev::RegPhase) * phases.size(),
                               cudaMemcpyHostToDevice),
                    "upload phases");
@@ -794,11 +807,16 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         }
         if (FILE *f = fopen((std::string(dir) + "/program.txt").c_str(), "w")) {
             for (const LaunchRec &r : p->recs) {
-                if (r.kind == StepKind::Tile && r.jit >= 0)
-                    fprintf(f, "TILE %s %llu %d %llu %zu\n", jit_source_tag(p->jit[r.jit].src).c_str(),
+                if (r.kind == StepKind::Tile && r.jit >= 0) {
+                    const auto &cw = p->jit[r.jit].cwvals;
+                    fprintf(f, "TILE %s %llu %d %llu %zu %d\n", jit_source_tag(p->jit[r.jit].src).c_str(),
                             (unsigned long long)r.tile.n_tiles, r.tile.T, (unsigned long long)r.tile.rank_base,
-                            p->jit[r.jit].smem_extra);
-                else
+                            p->jit[r.jit].smem_extra, r.jit);
+                    if (FILE *g = fopen((std::string(dir) + "/cw_" + std::to_string(r.jit) + ".bin").c_str(), "wb")) {
+                        fwrite(cw.data(), sizeof(double2), cw.size(), g);
+                        fclose(g);
+                    }
+                } else
                     fprintf(f, "OTHER %d %d\n", (int)r.kind, (int)r.skip);
             }
             fclose(f);
@@ -923,10 +941,10 @@ void program_destroy(sv_program *p) {
     if (!p) return;
     if (p->sv) cudaStreamSynchronize(p->sv->stream);
     for (auto *q : p->subs) program_destroy(q);
-    cudaFree(p->d_blob);
-    cudaFree(p->d_ops);
-    cudaFree(p->d_phases);
-    for (auto *d : p->d_tabs) cudaFree(d);
+    pool_free(p->d_blob, p->sv ? p->sv->stream : nullptr);
+    pool_free(p->d_ops, p->sv ? p->sv->stream : nullptr);
+    pool_free(p->d_phases, p->sv ? p->sv->stream : nullptr);
+    for (auto *d : p->d_tabs) pool_free(d, p->sv ? p->sv->stream : nullptr);
     for (auto e : p->ev) cudaEventDestroy(e);
     delete p;
 }

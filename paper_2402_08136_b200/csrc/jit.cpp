@@ -200,7 +200,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     std::map<int, size_t> cstage;      // op index -> offset (double2 units) in cw[]
     size_t ctot = 0;
     static const bool no_cw = getenv("HHLSV_JIT_NOCW") != nullptr;
-    if (cwide && !no_cw) {
+    static std::atomic<int> gen_count{0};
+    const int gen_idx = gen_count++;
+    const bool cw_only_skip = getenv("HHLSV_JIT_CWONLY") && atoi(getenv("HHLSV_JIT_CWONLY")) != gen_idx;   // debug
+    if (cwide && !no_cw && !cw_only_skip) {
         for (size_t i = 0; i < ops.size(); i++) {
             const auto &op = ops[i];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
@@ -209,7 +212,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 ctot += (size_t)1 << (2 * Kk);
             }
         }
-        if (ctot > 4096) {
+        if (ctot > 2040) {      // kernel parameter space: 32764 bytes
             cstage.clear();
             ctot = 0;
         }
@@ -338,9 +341,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     };
     if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
     std::ostringstream k;
-    if (ctot) k << "__constant__ double2 cw[" << ctot << "];\n";
+    if (ctot) k << "struct CWArg { double2 w[" << ctot << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
-      << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base) {\n";
+      << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base"
+      << (ctot ? ", const CWArg cwa" : "") << ") {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
     k << "  const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);\n";
@@ -605,9 +609,40 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         k << "        {\n";
                         auto ws0 = wstage.find(oi);
                         auto cs0 = cstage.find(oi);
-                        if (cs0 != cstage.end()) {
-                            // fully unrolled blocks of RU rows, matrix entries as constant-bank operands
+                        static const int cwru = getenv("HHLSV_JIT_CWRU") ? atoi(getenv("HHLSV_JIT_CWRU")) : 0;
+                        static const bool cw_unroll = getenv("HHLSV_JIT_CWUNROLL") != nullptr;
+                        if (cs0 != cstage.end() && !cw_unroll) {
+                            // rolled loop over blocks of RU rows (the fully unrolled form below gave wrong
+                            // results for some small-tile kernels, source equivalent -- kept behind
+                            // HHLSV_JIT_CWUNROLL for investigation); matrix entries from the by-value
+                            // kernel parameter (constant bank, uniform across the warp)
                             const int RU = real ? 4 : 2;
+                            k << "          #pragma unroll 1\n          for (int r = 0; r < " << D << "; r += " << RU << ") {";
+                            for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
+                            k << "\n";
+                            for (int cc = 0; cc < D; cc++) {
+                                const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
+                                for (int q = 0; q < RU; q++) {
+                                    const std::string w = "cwa.w[" + std::to_string(cs0->second + cc) + " + (r + " + std::to_string(q) +
+                                                          ") * " + std::to_string(D) + "]";
+                                    if (real)
+                                        k << "            { const double w = " << w << ".x; ax" << q << " = fma(w, " << in << ".x, ax" << q
+                                          << "); ay" << q << " = fma(w, " << in << ".y, ay" << q << "); }\n";
+                                    else
+                                        k << "            { const double2 w = " << w << "; ax" << q << " = fma(w.x, " << in << ".x, ax" << q
+                                          << "); ax" << q << " = fma(-w.y, " << in << ".y, ax" << q << "); ay" << q << " = fma(w.x, " << in
+                                          << ".y, ay" << q << "); ay" << q << " = fma(w.y, " << in << ".x, ay" << q << "); }\n";
+                                }
+                            }
+                            for (int q = 0; q < RU; q++) {
+                                k << "            { const u32 rr = (u32)r + " << q << "u; const u32 slot = " << rd[g] << "u";
+                                for (int i = 0; i < K; i++) k << " | ((rr >> " << i << ") & 1u) << " << Rpos[i];
+                                k << "; cur[swz(tb | slot)] = mk(ax" << q << ", ay" << q << "); }\n";
+                            }
+                            k << "          }\n";
+                        } else if (cs0 != cstage.end()) {
+                            // fully unrolled blocks of RU rows, matrix entries as constant-bank operands
+                            const int RU = cwru > 0 ? cwru : (real ? 4 : 2);
                             for (int r0 = 0; r0 < D; r0 += RU) {
                                 k << "          {";
                                 for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
@@ -616,7 +651,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                     const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
                                     k << "           ";
                                     for (int q = 0; q < RU; q++) {
-                                        const std::string w = "cw[" + std::to_string(cs0->second + (size_t)(r0 + q) * D + cc) + "]";
+                                        static const bool cwdbg = getenv("HHLSV_JIT_CWDBG") != nullptr;
+                                        const std::string w = cwdbg ? "__ldg(U + " + std::to_string((size_t)(r0 + q) * D + cc) + ")"
+                                                                    : "cwa.w[" + std::to_string(cs0->second + (size_t)(r0 + q) * D + cc) + "]";
                                         if (real)
                                             k << " ax" << q << " = fma(" << w << ".x, " << in << ".x, ax" << q << "); ay" << q << " = fma(" << w
                                               << ".x, " << in << ".y, ay" << q << ");";
@@ -1030,7 +1067,6 @@ void jit_build(std::vector<JitPass> &passes) {
             fail(SV_E_CUDA, "tile JIT failed: " + ents[i]->err);
         }
         passes[i].kern = ents[i]->kern;
-        passes[i].lib = ents[i]->lib;
     }
 }
 
@@ -1052,19 +1088,7 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)148 * per_sm;
     if (grid > n_tiles) grid = n_tiles;
-    if (!p.cwide.empty()) {
-        void *cw = nullptr;
-        size_t cbytes = 0;
-        e = cudaLibraryGetGlobal(&cw, &cbytes, p.lib, "cw");
-        if (e != cudaSuccess) return e;
-        size_t off = 0;
-        for (auto &c : p.cwide) {
-            e = cudaMemcpyAsync((char *)cw + off * 16, blob + c.first, c.second * 16, cudaMemcpyDeviceToDevice, s);
-            if (e != cudaSuccess) return e;
-            off += c.second;
-        }
-    }
-    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base};
+    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base, (void *)p.cwvals.data()};
     return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 

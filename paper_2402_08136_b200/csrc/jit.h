@@ -14,10 +14,12 @@ struct JitPass {
     std::string src;
     cudaKernel_t kern = nullptr;
     size_t smem_extra = 0;     // total dynamic shared memory of the generated kernel (bytes)
-    // wide (>= 3-target) dense matrices read as constant-bank operands: (blob offset, entries) copied
-    // in order into the pass module's __constant__ cw[] on the launch stream before every launch
+    // wide (>= 3-target) dense matrices read as constant-bank operands: (blob offset, entries) in
+    // the order of the kernel's by-value parameter cwa (<= 32 KB of kernel parameters: per-launch,
+    // hence coherent even when passes with identical structure share one cached module), and the
+    // host copy of those values passed at every launch
     std::vector<std::pair<uint64_t, uint64_t>> cwide;
-    cudaLibrary_t lib = nullptr;
+    std::vector<double2> cwvals;
 };
 
 // Product-state init fused into the first tile pass: the pass computes its tile's amplitudes

@@ -41,6 +41,8 @@ static unsigned char *g_smem;
 #define smem_raw g_smem
 static inline unsigned long long __cvta_generic_to_shared(void *p) { return (unsigned long long)p; }
 static inline double __ddiv_rn(double a, double b) { return a / b; }
+template <class T> static inline T __ldcs(const T *p) { return *p; }
+template <class T> static inline void __stcs(T *p, T v) { *p = v; }
 '''
 
 MAIN = r'''
@@ -76,7 +78,29 @@ def host_source(src: str) -> str:
                s, flags=re.S)
     s = re.sub(r"void cp_async_(commit|wait1|wait0)\(\) \{[^}]*\}", r"void cp_async_\1() {}", s)
     s = s.replace("#pragma unroll 1", "")
-    return SHIM + s + MAIN
+    # prelude: explicit shared-window asm accessors -> byte offsets into the emulated smem
+    s = s.replace("__cvta_generic_to_shared(smem_raw)", "0")
+    acc = {
+        "double2 lds(u32 a)": "{ double2 v; memcpy(&v, g_smem + a, 16); return v; }",
+        "void sts(u32 a, double2 v)": "{ memcpy(g_smem + a, &v, 16); }",
+        "u64 lds64(u32 a)": "{ u64 v; memcpy(&v, g_smem + a, 8); return v; }",
+        "void sts64(u32 a, u64 v)": "{ memcpy(g_smem + a, &v, 8); }",
+        "void stsd(u32 a, double v)": "{ memcpy(g_smem + a, &v, 8); }",
+        "void bar()": "{ __syncthreads(); }",
+        "void cp_async16s(u32 s, const void *gmem)": "{ memcpy(g_smem + s, gmem, 16); }",
+    }
+    for sig, body in acc.items():
+        s = re.sub(r"(__device__ __forceinline__ " + re.escape(sig) + r") \{.*?\n?\}\n", lambda m: m.group(1) + " " + body + "\n",
+                   s, count=1, flags=re.S)
+    s = re.sub(r'asm volatile\("prefetch\.global\.L2 \[%0\];" ::"l"\(.*?\)\);', ";", s)
+    main = MAIN
+    if "struct CWArg" in s:
+        main = main.replace("hhlsv_tile(psi.data(), blob.data(), n_tiles, rank_base);",
+                            "hhlsv_tile(psi.data(), blob.data(), n_tiles, rank_base, g_cw);")
+        main = main.replace("int main(int argc, char **argv) {",
+                            "static CWArg g_cw;\nint main(int argc, char **argv) {\n    { FILE *c = fopen(argv[7], \"rb\"); "
+                            "fread(&g_cw, 1, sizeof g_cw, c); fclose(c); }")
+    return SHIM + s + main
 
 
 def main():
@@ -91,6 +115,7 @@ def main():
         if t[0] != "TILE":
             raise SystemExit(f"non-tile step in the program: {ln.strip()}")
         tag, n_tiles, T, rb, smem = t[1], int(t[2]), int(t[3]), int(t[4]), int(t[5])
+        cwf = os.path.join(d, f"cw_{t[6]}.bin") if len(t) > 6 else "/dev/null"
         exe = os.path.join(work, tag)
         if not os.path.exists(exe):
             src = open(os.path.join(d, tag + ".cu")).read()
@@ -99,7 +124,7 @@ def main():
             subprocess.run(["g++", "-O1", "-g", "-std=c++20", "-pthread", "-w", "-fsanitize=address", "-o", exe, cpp],
                            check=True)
         subprocess.run([exe, state, os.path.join(d, "blob.bin"), str(n_tiles), str(rb), str(1 << (T - 4)),
-                        str(smem)], check=True)
+                        str(smem), cwf], check=True)
         print(f"ran {tag} n_tiles={n_tiles}", flush=True)
     np.save(out, np.fromfile(state, dtype=np.complex128))
 
