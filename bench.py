@@ -226,7 +226,7 @@ def run_ours(args):
                 d = per_kind.setdefault(kind, [0.0, 0, 0.0, 0.0, 0.0])
                 d[0] += ms
                 d[1] += 1
-                d[2] = by
+                d[2] += by
                 d[3] += fl
                 # per-launch roofline time: the slower of the HBM and the FP64 bound
                 d[4] += max(by / (peak_gbs * 1e9), fl / FP64_PEAK) * 1e3
@@ -249,6 +249,7 @@ def run_ours(args):
     dom = max(((k, v) for k, v in per_kind.items() if k != kind_exchange), key=lambda kv: kv[1][0])
     dom_kind, (dom_ms, dom_n, dom_bytes, dom_flops, dom_roof_ms) = dom
     dom_avg = dom_ms / max(1, dom_n)
+    dom_bytes = dom_bytes / max(1, dom_n)          # mean algorithmic bytes per launch (pass 1 writes only)
     achieved = dom_bytes / (dom_avg * 1e-3) / 1e9
     kind_names = pkg.sv.STEP_KINDS
     traffic = None
@@ -273,6 +274,7 @@ def run_ours(args):
     nvlink = None
     if kind_exchange in per_kind:      # global-qubit swaps: bytes each rank sends + receives per exchange
         xms, xn, xby = per_kind[kind_exchange][:3]
+        xby = xby / max(1, xn)                      # mean bytes per exchange
         nvlink = {"exchanges_per_step": xn // max(1, args.steps), "ms_per_exchange": xms / max(1, xn),
                   "bytes_per_exchange": xby, "gbs": xby / (xms / max(1, xn) * 1e-3) / 1e9 if xms > 0 else None,
                   "share_of_step": xms / args.steps / ms_step}

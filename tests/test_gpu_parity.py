@@ -333,3 +333,17 @@ def test_table1_30bus_on_gpu():
     x, rep = pkg.hhl_solve(A, b)
     assert (rep["n_data"], rep["n_clock"], rep["n_total"]) == (5, 10, 16)
     assert abs(np.linalg.norm(x - np.linalg.solve(A, b)) - 1.18e-3) < 0.005e-3
+
+
+@pytest.mark.parametrize("kinds", [("controlled", "diagonal"), ("dense", "controlled"), ("dense", "diagonal", "swap")])
+@pytest.mark.parametrize("T", [7, 8, 9, 12])
+def test_jit_small_tiles_wide_ops(kinds, T):
+    """NVRTC tile passes at small tiles with 3-qubit (wide) dense/controlled ops: single-phase passes,
+    direct HBM<->register phases, thread/tile-controlled wide ops, kernel-parameter matrices
+    (regression: an unrolled form of the wide-op row loop miscomputed T=8 controlled kernels)."""
+    n = 12
+    for seed in range(6):
+        gates = synthetic.random_circuit(n, 40, seed=700 + seed, kinds=kinds, kmax=3)
+        psi0 = synthetic.random_state(n, seed)
+        got, ref, _ = run_both(n, gates, psi0, fusion_kmax=2, tile_qubits=T, tile_jit=1)
+        assert np.abs(got - ref).max() < 1e-10, (seed, np.abs(got - ref).max())
