@@ -326,6 +326,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     if (const char *e = getenv("HHLSV_JIT_DIRECT")) low3 = low3 && atoi(e) != 0;
     const bool din = nbuf == 1 && low3 && ph.front().R[0] >= 3;
     static const bool pf_on = !getenv("HHLSV_JIT_NOPF");
+    // cross-tile register prefetch: the next tile's phase-0 loads are issued right after this tile's
+    // last stores, so their latency overlaps the tile-end barrier and the next sub-table builds
+    const bool xpf = din && !init && !getenv("HHLSV_JIT_NOXPF");
     const bool dout = nbuf == 1 && low3 && ph.back().R[0] >= 3;
     auto tb_expr = [&](const dev::RegPhase &P) {
         std::ostringstream o;
@@ -429,6 +432,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             return any_run;
         };
     k << "  u64 tile = blockIdx.x;\n";
+    if (xpf) {
+        k << "  double2 x0";
+        for (int j = 1; j < 16; j++) k << ", x" << j;
+        k << ";\n  { const double2 *gnx = psi + (tile_base(tile < n_tiles ? tile : n_tiles - 1) | pd_in);";
+        for (int j = 0; j < 16; j++) k << " x" << j << " = __ldcs(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
+        k << " }\n";
+    }
     if (hoist) {
         k << "  if (tile < n_tiles) {\n";
         emit_pre(0, "rank_base | tile_base(tile)");
@@ -531,6 +541,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 }
                 k << "        }\n      }\n";
             }
+        } else if (p == 0 && din && xpf) {
+            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = x" << j << ";\n";
         } else if (p == 0 && din) {
             k << "      const double2 *gin = psi + (base | pd_in);\n";
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = __ldcs(gin + " << u64s(phys_slot(P, j)) << ");\n";
@@ -932,6 +944,12 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // hoisted sub-table build for the next phase (or the next tile's phase 0) after this phase's
         // registers are stored (they are dead: no extra register pressure), before the barrier
         auto hoisted = [&] {
+            if (xpf && p + 1 == nph) {      // next tile's phase-0 registers (this tile's are stored: dead)
+                // unconditional (clamped to the last tile) so x is dead between phase 0 and here
+                k << "      { const u64 nt = tile + gridDim.x < n_tiles ? tile + gridDim.x : n_tiles - 1; const double2 *gnx = psi + (tile_base(nt) | pd_in);";
+                for (int j = 0; j < 16; j++) k << " x" << j << " = __ldcs(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
+                k << " }\n";
+            }
             if (!hoist) return;
             if (p + 1 < nph) emit_pre(p + 1, "gbase");
             else {
