@@ -341,10 +341,37 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     return fuse(rest, fo);
 }
 
-static CompileOptions hhl_compile_opts(const hhl_options *opt) {
+// Optional initial physical layout of a single-rank eigenbasis HHL program: the three lowest
+// clock qubits take the three lowest physical bits -- every tile holds those (128-byte segments) and
+// their QFT/IQFT gates all fall in the middle pass anyway -- and the system register follows at
+// physical 3..3+n_b-1, so the final 4-qubit V runs in a last phase whose thread bits start with the
+// coalesced low bits (direct register->HBM stores instead of a shared-memory round trip).
+static std::vector<int> hhl_layout(const HHLPlanHost &p, const hhl_options *opt, int world) {
+    // Measured on S30: mode 1 makes the V pass 11.7 -> 8.1 ms but the greedy packer then
+    // loads the middle pass with 79 ops (12.2 -> 17.4 ms): net slower, so the default stays identity;
+    // HHLSV_LAYOUT=1|2 selects a variant for experiments.
+    static const int mode = getenv("HHLSV_LAYOUT") ? atoi(getenv("HHLSV_LAYOUT")) : 0;
+    if (mode == 0 || world != 1 || !opt || opt->qpe_mode != 1 || opt->tile_qubits < 0 || p.n_c < 4) return {};
+    std::vector<int> phys(p.n, -1);
+    std::vector<int> low;                                          // logical qubits at physical 0..2
+    if (mode == 2)
+        for (int j = p.n_c - 3; j < p.n_c; j++) low.push_back(p.n_b + j);   // top clock qubits
+    else
+        for (int j = 0; j < 3; j++) low.push_back(p.n_b + j);               // bottom clock qubits
+    int next = 0;
+    for (int q : low) phys[q] = next++;
+    for (int s = 0; s < p.n_b; s++) phys[s] = next++;              // system
+    for (int j = 0; j < p.n_c; j++)
+        if (phys[p.n_b + j] < 0) phys[p.n_b + j] = next++;        // remaining clock qubits
+    phys[p.n - 1] = next++;                                        // ancilla
+    return phys;
+}
+
+static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost *p = nullptr, int world = 1) {
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
     if (opt) co.jit = opt->tile_jit;
+    if (p) co.phys_init = hhl_layout(*p, opt, world);
     return co;
 }
 
@@ -359,7 +386,8 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     size_t n_logical = 0;
     std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
     prof_mark("fold + fuse");
-    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt), n_logical);
+    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt, &p, sv->nloc == sv->n ? 1 : 2),
+                                      n_logical);
     prof_mark("program_create");
     if (rep) {
         std::memset(rep, 0, sizeof(*rep));
@@ -428,7 +456,9 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
         std::vector<int> phys(p.n);
         for (int q = 0; q < p.n; q++) phys[q] = q;
-        Schedule s = compile(fused, nullptr, p.n, p.n - g, phys, hhl_compile_opts(opt));
+        const CompileOptions hco = hhl_compile_opts(opt, &p, world);
+        if (!hco.phys_init.empty()) phys = hco.phys_init;
+        Schedule s = compile(fused, nullptr, p.n, p.n - g, phys, hco);
         if (rep) {
             std::memset(rep, 0, sizeof(*rep));
             rep->lambda_min = p.lam_min;

@@ -587,6 +587,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     if (p->resets) {
         p->phys_in.resize(sv->n);
         std::iota(p->phys_in.begin(), p->phys_in.end(), 0);
+        if ((int)co.phys_init.size() == sv->n && sv->nloc == sv->n) p->phys_in = co.phys_init;
     } else {
         p->phys_in = sv->phys;
     }

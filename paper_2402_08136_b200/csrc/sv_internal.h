@@ -141,6 +141,8 @@ struct CompileOptions {
     bool reorder = true;       // commutation-aware op reordering for tile packing (single rank)
     int diag_merge = 8;        // tile passes: merge consecutive diagonal ops of a register phase into
                                // one table of <= this many qubits after scheduling (0 = off)
+    std::vector<int> phys_init;  // programs that start with their own initialisation: logical->physical
+                                 // map at program start (empty = identity)
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.
