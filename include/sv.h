@@ -201,6 +201,15 @@ sv_status sv_norm2(sv_state *sv, double *out);
 sv_status sv_postselect_slice(sv_state *sv, const int *fixed_q, const int *fixed_v, int n_fixed,
                               double *amps_out, uint64_t *idx_out, uint64_t n_out, double *prob_out);
 
+/* Shot sampling (SPEC `sample` S:166-174; Fig. 3 caption, "10,000 measurements of the
+ * Bell state"): writes `shots` LOGICAL basis indices drawn i.i.d. from |a_i|^2 / sum |a|^2 to out
+ * (caller-owned, shots uint64). Deterministic given seed: shot s uses the uniform
+ * u_s = (splitmix64(seed + (s+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53 and inverse-CDF search in logical
+ * order with the fixed summation order of DESIGN.md §Sampling (the oracle implements the same
+ * generator and order, so indices are identical). Single-rank states only (SV_E_ARG when sharded);
+ * SV_E_ZEROPROB for a zero state. Synchronous. */
+sv_status sv_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out);
+
 /* ------------------------------------------------------------------- HHL ---- */
 /* HHL front end + solve ("Practical HHL procedures", Fig. 5, resources
  * PAPER.md:225-242 read per DESIGN.md R2/R3). */

@@ -308,6 +308,13 @@ sv_status sv_postselect_slice(sv_state *sv, const int *fixed_q, const int *fixed
     });
 }
 
+sv_status sv_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out) {
+    return guard([&] {
+        if (!sv) fail(SV_E_ARG, "null state");
+        state_sample(sv, shots, seed, out);
+    });
+}
+
 // ------------------------------------------------------------------- HHL ----
 static double opt_snap(const hhl_options *o) { return (o && o->recip_snap >= 0.0) ? o->recip_snap : 1e-5; }
 

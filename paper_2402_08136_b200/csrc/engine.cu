@@ -1096,6 +1096,51 @@ void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in)
     cuda_check(cudaStreamSynchronize(sv->stream), "write sync");
 }
 
+void state_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out) {
+    if (sv->world > 1 || sv->vworld > 1) fail(SV_E_ARG, "sample: single-rank states only");
+    if (shots && !out) fail(SV_E_ARG, "sample: null output");
+    std::unique_ptr<dev::SampleArgs> a(new dev::SampleArgs());
+    a->psi = sv->psi;
+    a->n = sv->n;
+    a->lb1 = std::min(sv->n, dev::kSampleLB1);
+    a->nblk = 1ull << (sv->n - a->lb1);
+    a->lb2 = std::min(sv->n - a->lb1, dev::kSampleLB2);
+    a->nsup = a->nblk >> a->lb2;
+    fill_phys(sv, a->phys);
+    for (uint64_t i = 0; i < (1ull << a->lb1); i++) {
+        uint64_t P = 0;
+        for (int q = 0; q < a->lb1; q++)
+            if ((i >> q) & 1ull) P |= 1ull << a->phys[q];
+        a->lo[i] = P;
+    }
+    a->shots = shots;
+    a->seed = seed;
+    cuda_check(pool_malloc((void **)&a->S, sizeof(double) * a->nblk, sv->stream), "alloc(sample S)");
+    cuda_check(pool_malloc((void **)&a->cum, sizeof(double) * a->nsup, sv->stream), "alloc(sample cum)");
+    cuda_check(pool_malloc((void **)&a->out, sizeof(uint64_t) * std::max<uint64_t>(1, shots), sv->stream),
+               "alloc(sample out)");
+    struct Free {
+        sv_state *sv;
+        dev::SampleArgs *a;
+        ~Free() {
+            pool_free(a->S, sv->stream);
+            pool_free(a->cum, sv->stream);
+            pool_free(a->out, sv->stream);
+        }
+    } fr{sv, a.get()};
+    cuda_check(dev::launch_sample_sums(*a, sv->stream), "sample sums");
+    double total = 0.0;
+    cuda_check(cudaMemcpyAsync(&total, a->cum + a->nsup - 1, sizeof(double), cudaMemcpyDeviceToHost, sv->stream),
+               "sample total");
+    cuda_check(cudaStreamSynchronize(sv->stream), "sample sync");
+    if (!(total > 0.0)) fail(SV_E_ZEROPROB, "sample: zero state");
+    cuda_check(dev::launch_sample_draw(*a, sv->stream), "sample draw");
+    if (shots)
+        cuda_check(cudaMemcpyAsync(out, a->out, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, sv->stream),
+                   "sample out");
+    cuda_check(cudaStreamSynchronize(sv->stream), "sample sync");
+}
+
 void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, double *amps, uint64_t *idx,
                       uint64_t n_out, double *prob) {
     if (nfixed < 0 || (nfixed > 0 && (!fq || !fv)) || !amps) fail(SV_E_ARG, "postselect: bad arguments");

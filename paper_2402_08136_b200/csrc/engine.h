@@ -90,6 +90,8 @@ void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out);
 void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in);
 double state_norm2(sv_state *sv);
 void state_probabilities(sv_state *sv, const int *qubits, int nq, double *out);
+// Shot sampling: `shots` logical indices drawn from |a|^2, deterministic in seed.
+void state_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out);
 void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, double *amps, uint64_t *idx,
                       uint64_t n_out, double *prob);
 }  // namespace hhlsv

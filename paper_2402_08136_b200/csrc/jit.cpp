@@ -95,12 +95,21 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 // Shared memory through explicit 32-bit shared-window addresses (volatile asm keeps program order
 // between all shared accesses and barriers): nvcc's addressing form. NVRTC's default 64-bit
 // shared-pointer arithmetic trips a ptxas -O2/-O3 miscompilation on some of these kernels.
+#ifdef HHLSV_SMEM_CLOBBER
+__device__ __forceinline__ double2 lds(u32 a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory"); }
+#else
 __device__ __forceinline__ double2 lds(u32 a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
 }
 __device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y)); }
+#endif
 __device__ __forceinline__ u64 lds64(u32 a) {
     u64 v;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
@@ -108,6 +117,14 @@ __device__ __forceinline__ u64 lds64(u32 a) {
 }
 __device__ __forceinline__ void sts64(u32 a, u64 v) { asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v)); }
 __device__ __forceinline__ void stsd(u32 a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+// Streaming HBM loads of tile data: not allocated in L1 (an SM must never keep lines another SM
+// writes during the pass: a stale line would survive into the next pass), volatile with a memory
+// clobber (never moved across this thread's own stores or re-executed by the compiler)
+__device__ __forceinline__ double2 ldcs_v(const double2 *g) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(g) : "memory");
+    return v;
+}
 __device__ __forceinline__ void bar() { asm volatile("bar.sync 0;" ::: "memory"); }
 struct SRef {
     u32 a;
@@ -328,7 +345,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     static const bool pf_on = !getenv("HHLSV_JIT_NOPF");
     // cross-tile register prefetch: the next tile's phase-0 loads are issued right after this tile's
     // last stores, so their latency overlaps the tile-end barrier and the next sub-table builds
-    const bool xpf = din && !init && !getenv("HHLSV_JIT_NOXPF");
+    static std::atomic<int> xpf_count{0};
+    const int xpf_idx = xpf_count++;
+    // Off by default (HHLSV_JIT_XPF=1 enables it): with it, ptxas -O2/-O3 (not -O1, source checked
+    // equivalent) produced wrong amplitudes for a T = 8 controlled/diagonal circuit
+    // (tests/test_gpu_parity.py::test_jit_small_tiles_wide_ops, seed 703), for ~0.3 ms on S30.
+    const bool xpf = din && !init && getenv("HHLSV_JIT_XPF") &&
+                     (!getenv("HHLSV_JIT_XPFONLY") || atoi(getenv("HHLSV_JIT_XPFONLY")) == xpf_idx);   // debug
     const bool dout = nbuf == 1 && low3 && ph.back().R[0] >= 3;
     auto tb_expr = [&](const dev::RegPhase &P) {
         std::ostringstream o;
@@ -436,7 +459,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "  double2 x0";
         for (int j = 1; j < 16; j++) k << ", x" << j;
         k << ";\n  { const double2 *gnx = psi + (tile_base(tile < n_tiles ? tile : n_tiles - 1) | pd_in);";
-        for (int j = 0; j < 16; j++) k << " x" << j << " = __ldcs(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
+        for (int j = 0; j < 16; j++) k << " x" << j << " = ldcs_v(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
         k << " }\n";
     }
     if (hoist) {
@@ -545,11 +568,22 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = x" << j << ";\n";
         } else if (p == 0 && din) {
             k << "      const double2 *gin = psi + (base | pd_in);\n";
-            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = __ldcs(gin + " << u64s(phys_slot(P, j)) << ");\n";
+            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
         } else {
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
         }
+        // The last op of a last phase that stores through shared memory is a wide dense op without
+        // controls: its rows are written to their final shared-memory slots, so neither the register
+        // reload nor the end-of-phase stores are needed.
+        bool tail_in_smem = false;
+        auto tail_wide = [&](int oi) {
+            const dev::RegOp &op = ops[oi];
+            const int Kq = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            return p + 1 == ph.size() && !dout && oi + 1 == P.op1 && op.kind == 0 && Kq >= 3 && !op.rcm && !op.tcm &&
+                   !op.gcm && !getenv("HHLSV_JIT_NOTAIL");
+        };
         auto emit_single = [&](int oi) {
+            tail_in_smem = tail_wide(oi);
             const dev::RegOp &op = ops[oi];
             std::ostringstream cond;
             if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
@@ -731,10 +765,11 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 k << " cur[swz(tb | " << rd[g | dep_slot(r, M)] << "u)] = mk(ax, ay); }\n";
                             }
                         }
-                        for (int r = 0; r < D; r++) {
-                            const int j = g | dep_slot(r, M);
-                            k << "          v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
-                        }
+                        if (!tail_in_smem)      // else: the outputs already sit in their final smem slots
+                            for (int r = 0; r < D; r++) {
+                                const int j = g | dep_slot(r, M);
+                                k << "          v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+                            }
                         k << "        }\n";
                         continue;
                     }
@@ -946,8 +981,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         auto hoisted = [&] {
             if (xpf && p + 1 == nph) {      // next tile's phase-0 registers (this tile's are stored: dead)
                 // unconditional (clamped to the last tile) so x is dead between phase 0 and here
-                k << "      { const u64 nt = tile + gridDim.x < n_tiles ? tile + gridDim.x : n_tiles - 1; const double2 *gnx = psi + (tile_base(nt) | pd_in);";
-                for (int j = 0; j < 16; j++) k << " x" << j << " = __ldcs(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
+                // past the last tile: reload this CTA's own tile (never another CTA's, which may be in flight)
+                k << "      { const u64 nt = tile + gridDim.x < n_tiles ? tile + gridDim.x : tile; const double2 *gnx = psi + (tile_base(nt) | pd_in);";
+                for (int j = 0; j < 16; j++) k << " x" << j << " = ldcs_v(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
                 k << " }\n";
             }
             if (!hoist) return;
@@ -964,7 +1000,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             hoisted();
             k << "    }\n";
         } else {
-            for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
+            if (!tail_in_smem)
+                for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
             hoisted();
             k << "      bar();\n    }\n";
         }
@@ -1010,6 +1047,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     // ASan/UBSan, scripts/jit_emulate.py; same PTX fine at -O1).
     std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O3"};
     if (const char *x = getenv("HHLSV_JIT_OPT")) opts.back() = x;     // experiments
+    if (getenv("HHLSV_JIT_CLOBBER")) opts.push_back("-DHHLSV_SMEM_CLOBBER");
     int rc = n.compile(prog, (int)opts.size(), opts.data());
     if (rc) {
         size_t ls = 0;

@@ -638,6 +638,129 @@ cudaError_t launch_marginal(const double2 *psi, int nloc, const int *S, int q, d
     return cudaGetLastError();
 }
 
+// ============================================================ shot sampling ====
+__device__ __forceinline__ uint64_t sample_phys(const SampleArgs &a, uint64_t L) {
+    uint64_t P = a.lo[L & ((1ull << a.lb1) - 1ull)];
+    const uint64_t hi = L >> a.lb1;
+    for (int q = a.lb1; q < a.n; q++)
+        if ((hi >> (q - a.lb1)) & 1ull) P |= 1ull << a.phys[q];
+    return P;
+}
+__device__ __forceinline__ double sample_p(const SampleArgs &a, uint64_t P) {
+    const double2 v = a.psi[P];
+    return __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+}
+
+// one warp per block: lanes sum strided elements sequentially, then the halving tree
+__global__ void k_sample_blocks(const SampleArgs a) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= a.nblk) return;
+    const uint64_t per = 1ull << a.lb1;
+    uint64_t hiP = 0;                               // physical bits of the block's high logical bits
+    for (int q = a.lb1; q < a.n; q++)
+        if ((warp >> (q - a.lb1)) & 1ull) hiP |= 1ull << a.phys[q];
+    double r = 0.0;
+    if (per >= 32) {
+        for (uint64_t k = 0; k < per / 32; k++) {
+            const double pv = sample_p(a, hiP | a.lo[k * 32 + lane]);
+            r = k == 0 ? pv : __dadd_rn(r, pv);
+        }
+    } else if ((uint64_t)lane < per) {
+        r = sample_p(a, hiP | a.lo[lane]);
+    }
+    for (int h = 16; h >= 1; h >>= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, r, h);
+        if (lane < h) r = __dadd_rn(r, o);
+    }
+    if (lane == 0) a.S[warp] = r;
+}
+
+__global__ void k_sample_sup(const SampleArgs a) {
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.nsup) return;
+    const uint64_t nb = 1ull << a.lb2;
+    double r = a.S[c * nb];
+    for (uint64_t b = 1; b < nb; b++) r = __dadd_rn(r, a.S[c * nb + b]);
+    a.cum[c] = r;
+}
+
+__global__ void k_sample_prefix(const SampleArgs a) {
+    double r = a.cum[0];
+    for (uint64_t c = 1; c < a.nsup; c++) {
+        r = __dadd_rn(r, a.cum[c]);
+        a.cum[c] = r;
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_sample_draw(const SampleArgs a) {
+    const uint64_t sidx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sidx >= a.shots) return;
+    const double u = (double)(splitmix64(a.seed + (sidx + 1) * 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53;
+    const double total = a.cum[a.nsup - 1];
+    const double t = __dmul_rn(u, total);
+    // superblock: first c with cum_c > t (binary search on the non-decreasing prefix)
+    uint64_t lo = 0, hi = a.nsup;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a.cum[mid] > t) hi = mid;
+        else lo = mid + 1;
+    }
+    uint64_t c = lo;
+    if (c >= a.nsup) {                              // rounding: last superblock with a nonzero sum
+        c = a.nsup - 1;
+        while (c > 0 && a.cum[c] == a.cum[c - 1]) c--;
+    }
+    // block inside the superblock
+    const uint64_t nb = 1ull << a.lb2;
+    double r = c ? a.cum[c - 1] : 0.0;
+    uint64_t blk = UINT64_MAX, lastnz = c * nb;
+    double before = r, before_lastnz = r;
+    for (uint64_t b = c * nb; b < (c + 1) * nb; b++) {
+        const double nr = __dadd_rn(r, a.S[b]);
+        if (a.S[b] > 0.0) { lastnz = b; before_lastnz = r; }
+        if (nr > t) { blk = b; before = r; break; }
+        r = nr;
+    }
+    if (blk == UINT64_MAX) { blk = lastnz; before = before_lastnz; }
+    // element inside the block (logical order)
+    const uint64_t per = 1ull << a.lb1;
+    uint64_t hiP = 0;
+    for (int q = a.lb1; q < a.n; q++)
+        if ((blk >> (q - a.lb1)) & 1ull) hiP |= 1ull << a.phys[q];
+    r = before;
+    uint64_t el = UINT64_MAX, lastel = 0;
+    for (uint64_t i = 0; i < per; i++) {
+        const double pv = sample_p(a, hiP | a.lo[i]);
+        const double nr = __dadd_rn(r, pv);
+        if (pv > 0.0) lastel = i;
+        if (nr > t) { el = i; break; }
+        r = nr;
+    }
+    if (el == UINT64_MAX) el = lastel;
+    a.out[sidx] = (blk << a.lb1) | el;
+}
+
+cudaError_t launch_sample_sums(const SampleArgs &a, cudaStream_t s) {
+    const uint64_t threads = a.nblk * 32;
+    k_sample_blocks<<<(unsigned)((threads + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    k_sample_sup<<<(unsigned)((a.nsup + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    k_sample_prefix<<<1, 1, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_draw(const SampleArgs &a, cudaStream_t s) {
+    if (a.shots == 0) return cudaSuccess;
+    k_sample_draw<<<(unsigned)((a.shots + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 // ======================================================= gather / scatter ====
 __global__ void k_gather(const GatherArgs a) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

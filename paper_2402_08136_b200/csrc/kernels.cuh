@@ -146,6 +146,29 @@ struct ScatterArgs {             // inverse of gather (sv_write): only owned ele
     int phys[64];
 };
 cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
+// Shot sampling (sv_sample; SPEC `sample`, Fig. 3 "10,000 measurements"): inverse-CDF draws in
+// LOGICAL index order with a fixed summation order shared with the oracle:
+//  p_i = re*re + im*im (two roundings + one, no FMA);
+//  block b (2^lb1 logical indices): lane l of a warp sums p_{b,32k+l} for k = 0.. sequentially, then the
+//    32 lane sums are combined by halving (a[j] += a[j+h], h = 16, 8, .., 1) -> S_b;
+//  superblock c (2^lb2 blocks): T_c = sequential sum of its S_b; cum_c = sequential inclusive prefix;
+//  shot s: u = (splitmix64(seed + (s+1)*golden) >> 11) * 2^-53, t = u * cum_last; c = first with cum_c > t;
+//    running r from cum_{c-1} over the superblock's S_b -> first block with r > t; running r from the value
+//    before that block over its p_i (logical order) -> first i with r > t; when rounding leaves no such
+//    block / element, the last one with a nonzero sum is taken.
+constexpr int kSampleLB1 = 10, kSampleLB2 = 10;
+struct SampleArgs {
+    const double2 *psi;
+    int n, lb1, lb2;
+    uint64_t nblk, nsup;
+    uint64_t lo[1 << kSampleLB1];    // physical offset of the low lb1 logical bits (identity-free map)
+    int phys[64];
+    double *S, *cum;                 // nblk block sums, nsup superblock prefix sums (device)
+    uint64_t shots, seed;
+    uint64_t *out;                   // shots logical indices (device)
+};
+cudaError_t launch_sample_sums(const SampleArgs &a, cudaStream_t s);   // S, then cum
+cudaError_t launch_sample_draw(const SampleArgs &a, cudaStream_t s);
 // Exchange helpers: pack/unpack the half of the local state whose bit lbit == val, elements [off, off+cnt).
 cudaError_t launch_pack(const double2 *psi, double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
                         cudaStream_t s);

@@ -74,7 +74,7 @@ EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
            "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
-           "sv_norm2", "sv_postselect_slice", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve",
+           "sv_norm2", "sv_postselect_slice", "sv_sample", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve",
            "hhl_schedule_dump"]
 
 _lib = None
@@ -114,6 +114,7 @@ def load(path: str = LIB_PATH):
         "sv_probabilities": [vp, P(c_int), c_int, P(c_dbl)],
         "sv_norm2": [vp, P(c_dbl)],
         "sv_postselect_slice": [vp, P(c_int), P(c_int), c_int, P(c_dbl), P(c_u64), c_u64, P(c_dbl)],
+        "sv_sample": [vp, c_u64, c_u64, P(c_u64)],
         "hhl_plan_size": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(c_int), P(c_int), P(c_int)],
         "hhl_schedule_dump": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), c_int, ctypes.c_char_p, ctypes.c_size_t,
                               P(hhl_report)],
@@ -279,6 +280,13 @@ class State:
                                           idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), amps.size,
                                           ctypes.byref(p)))
         return amps, idx, p.value
+
+    def sample(self, shots: int, seed: int = 0) -> np.ndarray:
+        """sv_sample: `shots` logical basis indices drawn from |a|^2 (deterministic in seed)."""
+        out = np.empty(max(1, int(shots)), dtype=np.uint64)
+        _check(load().sv_sample(self._h, int(shots), int(seed) & ((1 << 64) - 1),
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+        return out[:int(shots)]
 
 
 class Program:
