@@ -279,6 +279,20 @@ def run_ours(args):
                   "bytes_per_exchange": xby, "gbs": xby / (xms / max(1, xn) * 1e-3) / 1e9 if xms > 0 else None,
                   "share_of_step": xms / args.steps / ms_step}
 
+    # shot-sampling readout on the final S30 state: 10^5 shots (N=1; sv_sample is single-rank)
+    sample = None
+    if world == 1:
+        try:
+            st.sample(1000, seed=1)                       # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st.sample(100000, seed=2402)
+            ts = time.perf_counter() - t0
+            nb = 16.0 * (1 << configs.n_qubits(cfg))      # one read of the state for the block sums
+            sample = {"shots": 100000, "ms": ts * 1e3, "state_read_gbs": nb / ts / 1e9}
+        except Exception as exc:                          # reported, never fatal for the bench line
+            sample = {"error": str(exc)[:200]}
+
     # e2e through the public API with host buffers (N=1 only: hhl_solve owns its state)
     e2e = None
     if not args.no_e2e:
@@ -332,6 +346,8 @@ def run_ours(args):
                 "gpu_launches": int(stats["launches"] + 1), "clocks": clocks.summary()}
         if nvlink:
             line["nvlink"] = nvlink
+        if sample:
+            line["sample"] = sample
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -640,13 +640,16 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             init_spec.bits.push_back(pp.bits[g]);
         }
         p->sched.n_passes--;
-        p->sched.pass_bytes -= steps[0].bytes;
+        p->sched.pass_bytes -= steps[0].bytes;                       // no separate init pass
+        p->sched.pass_bytes -= 16.0 * (double)sv->local_amps();       // and the first pass reads nothing
     }
     for (size_t si = 0; si < steps.size(); si++) {
         const Step &st = steps[si];
         LaunchRec rec;
         rec.kind = st.kind;
         rec.bytes = st.bytes;
+        // the pass that computes the product-state init reads nothing: its HBM bytes are the write
+        if (fuse_init && si == 1 && st.kind == StepKind::Tile) rec.bytes = 16.0 * (double)sv->local_amps();
         switch (st.kind) {
             case StepKind::InitZero: break;
             case StepKind::InitProduct:
