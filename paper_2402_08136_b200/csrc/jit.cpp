@@ -486,7 +486,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // L2 prefetch of this CTA's next tile: its HBM reads overlap this tile's compute, and the
         // next tile's loads then hit L2 (296 CTAs x 64 KB in flight << 126 MB L2)
         if (pf_on && !init) {
-            k << "    if (tile + gridDim.x < n_tiles) {\n      const u64 nb = tile_base(tile + gridDim.x);\n";
+            static const int pfd = getenv("HHLSV_JIT_PFDIST") ? std::max(1, atoi(getenv("HHLSV_JIT_PFDIST"))) : 1;
+            k << "    if (tile + " << pfd << "ull * gridDim.x < n_tiles) {\n      const u64 nb = tile_base(tile + " << pfd
+              << "ull * gridDim.x);\n";
             if (din) {
                 k << "      if ((threadIdx.x & 7u) == 0u) { const char *g = (const char *)(psi + (nb | pd_in));";
                 for (int j = 0; j < 16; j++)
