@@ -653,6 +653,11 @@ __device__ __forceinline__ double sample_p(const SampleArgs &a, uint64_t P) {
 
 // one warp per block: lanes sum strided elements sequentially, then the halving tree
 __global__ void k_sample_blocks(const SampleArgs a) {
+    // the low-bit offset table in shared memory: lanes index it at 32 different entries per load
+    // (a by-value parameter indexed per lane would serialise in the constant cache)
+    __shared__ uint64_t lo_s[1 << kSampleLB1];
+    for (uint64_t i = threadIdx.x; i < (1ull << a.lb1); i += blockDim.x) lo_s[i] = a.lo[i];
+    __syncthreads();
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= a.nblk) return;
@@ -663,11 +668,11 @@ __global__ void k_sample_blocks(const SampleArgs a) {
     double r = 0.0;
     if (per >= 32) {
         for (uint64_t k = 0; k < per / 32; k++) {
-            const double pv = sample_p(a, hiP | a.lo[k * 32 + lane]);
+            const double pv = sample_p(a, hiP | lo_s[k * 32 + lane]);
             r = k == 0 ? pv : __dadd_rn(r, pv);
         }
     } else if ((uint64_t)lane < per) {
-        r = sample_p(a, hiP | a.lo[lane]);
+        r = sample_p(a, hiP | lo_s[lane]);
     }
     for (int h = 16; h >= 1; h >>= 1) {
         const double o = __shfl_down_sync(0xffffffffu, r, h);
