@@ -861,6 +861,15 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // touch (e.g. CP-ladder chunks over thread / out-of-tile bits) are multiplied into one scalar
         // per distinct slot set, and each slot then takes one complex multiply per distinct factor
         // list (shared across slots) instead of one per op.
+        auto op_cond = [&](const dev::RegOp &op) {     // thread / tile guard of a diagonal op ("" = none)
+            std::ostringstream c;
+            if (op.gcm) c << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
+            if (op.tcm) {
+                if (op.gcm) c << " && ";
+                c << "((tb & " << op.tcm << "u) == " << op.tcv << "u)";
+            }
+            return c.str();
+        };
         auto emit_group = [&](const std::vector<int> &G) {
             k << "      { // diagonal group of " << G.size() << " ops\n";
             std::vector<std::vector<std::string>> fac(16);
@@ -888,8 +897,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     const dev::RegOp &op = ops[oi];
                     int j0 = 0;
                     while (!((kv.first >> j0) & 1u)) j0++;
-                    const std::string ld = "__ldg(blob + " + std::to_string(op.data_off) + "ull + (ib" + std::to_string(oi) +
-                                           " | " + std::to_string(op.ridx[j0]) + "u))";
+                    std::string ld = "__ldg(blob + " + std::to_string(op.data_off) + "ull + (ib" + std::to_string(oi) +
+                                     " | " + std::to_string(op.ridx[j0]) + "u))";
+                    const std::string cnd = op_cond(op);      // guarded op: factor 1 where the guard fails
+                    if (!cnd.empty()) ld = "((" + cnd + ") ? " + ld + " : mk(1.0, 0.0))";
                     if (first) k << "        double2 " << U << " = " << ld << ";\n";
                     else k << "        " << U << " = cmul(" << U << ", " << ld << ");\n";
                     first = false;
@@ -905,8 +916,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     auto it = sym.find(op.ridx[j]);
                     if (it == sym.end()) {
                         const std::string L = "L" + std::to_string(oi) + "_" + std::to_string(op.ridx[j]);
-                        k << "        const double2 " << L << " = __ldg(blob + " << op.data_off << "ull + (ib" << oi << " | "
-                          << op.ridx[j] << "u));\n";
+                        const std::string cnd = op_cond(op);
+                        k << "        const double2 " << L << " = " << (cnd.empty() ? "" : "(" + cnd + ") ? ") << "__ldg(blob + "
+                          << op.data_off << "ull + (ib" << oi << " | " << op.ridx[j] << "u))" << (cnd.empty() ? "" : " : mk(1.0, 0.0)")
+                          << ";\n";
                         it = sym.emplace(op.ridx[j], L).first;
                     }
                     fac[j].push_back(it->second);
@@ -968,7 +981,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 int oj = oi;
                 while (oj < P.op1 && ops[oj].kind == 1 && !in_run(oj)) oj++;
                 std::vector<int> G, C;
-                for (int q = oi; q < oj; q++) (ops[q].gcm || ops[q].tcm ? C : G).push_back(q);
+                static const bool guard_sep = getenv("HHLSV_JIT_GUARDSEP") != nullptr;   // old form: guarded ops apart
+                for (int q = oi; q < oj; q++) ((guard_sep && (ops[q].gcm || ops[q].tcm)) ? C : G).push_back(q);
                 if (G.size() >= 2) {
                     emit_group(G);
                     for (int q : C) emit_single(q);
