@@ -315,7 +315,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             if i > 0:
                 times.append(time.perf_counter() - t0)
-        te = float(np.mean(times))
+        te = float(np.median(times))               # median: robust to one-off driver stalls
         if world > 1:
             t = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -365,7 +365,7 @@ def main():
     ap.add_argument("--tile", type=int, default=12)
     ap.add_argument("--qpe", type=int, default=1, help="0 textbook c-U chain, 1 eigenbasis rewrite (SURVEY f2)")
     ap.add_argument("--jit", type=int, default=0, help="tile pass specialisation: 0 auto, 1 on, -1 off")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
