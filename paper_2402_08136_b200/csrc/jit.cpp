@@ -1154,6 +1154,12 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     const void *f = reinterpret_cast<const void *>(p.kern);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // shared-memory carveout: experiments (HHLSV_JIT_CARVEOUT = percent of the maximum shared memory;
+    // the rest of the 256 KB SM data memory stays L1 for the diagonal tables)
+    if (const char *cv = getenv("HHLSV_JIT_CARVEOUT")) {
+        e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+        if (e != cudaSuccess) return e;
+    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem);
     if (e != cudaSuccess) return e;
