@@ -172,3 +172,21 @@ def test_hhl_schedule_dump_host_only(lib):
     assert "EXCHANGE" in txt2
     with pytest.raises(pkg.SVError):
         pkg.hhl_schedule_dump(A, b, world=3)
+
+
+def _jit_lines(txt):
+    return [ln for ln in txt.splitlines() if ln.startswith("JIT_PASS")]
+
+
+def test_jit_codegen_s30_and_small_tiles(lib):
+    """The NVRTC tile-pass generator (csrc/jit.cpp) emits sources that compile for sm_100a without a
+    GPU: the 5 passes of the S30 bench program (direct HBM phases, diagonal groups, reciprocal tables,
+    wide-op kernel parameters) and a small-tile circuit with 3-qubit controlled ops."""
+    A, b, nc = configs.get("S30")
+    txt, rep = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, fusion_kmax=1, tile_qubits=12, qpe_mode=1, tile_jit=1)
+    passes = _jit_lines(txt)
+    assert len(passes) == rep["n_passes"] == 5
+    assert all(int(p.split("cubin_bytes=")[1]) > 0 for p in passes)
+    gates = synthetic.random_circuit(12, 40, seed=703, kinds=("controlled", "diagonal"), kmax=3)
+    txt2, rep2 = pkg.schedule_dump(12, gates, fusion_kmax=2, tile_qubits=8, tile_jit=1)
+    assert len(_jit_lines(txt2)) == rep2["n_passes"] >= 1

@@ -104,3 +104,13 @@ def test_gpu_sample_permuted_map_and_errors():
     st.write(np.zeros(1 << n, dtype=complex))
     with pytest.raises(pkg.SVError):
         st.sample(10, seed=1)
+
+
+@pytest.mark.gpu
+def test_gpu_sample_sharded_state_refused():
+    """sv_sample is single-rank (DESIGN.md §6 Sampling): a sharded state reports SV_E_ARG, no fallback."""
+    import paper_2402_08136_b200 as pkg
+    st = pkg.State(10, world=2)
+    st.write(synthetic.random_state(10, 1))
+    with pytest.raises(pkg.SVError):
+        st.sample(10, seed=1)
