@@ -664,7 +664,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             // results for some small-tile kernels, source equivalent -- kept behind
                             // HHLSV_JIT_CWUNROLL for investigation); matrix entries from the by-value
                             // kernel parameter (constant bank, uniform across the warp)
-                            const int RU = real ? 4 : 2;
+                            static const int ru_env = getenv("HHLSV_JIT_RU") ? atoi(getenv("HHLSV_JIT_RU")) : 0;
+                            const int RU = std::min(D, ru_env > 0 ? ru_env : (real ? 16 : 2));   // measured: real 16 best
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D << "; r += " << RU << ") {";
                             for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
                             k << "\n";
