@@ -767,7 +767,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     JitPass jp;
                     jp.name = "hhlsv_tile";
                     jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
-                                             (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide);
+                                             (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide, &blob);
                     for (auto &c : jp.cwide)
                         jp.cwvals.insert(jp.cwvals.end(), blob.begin() + c.first, blob.begin() + c.first + c.second);
                     rec.jit = (int)p->jit.size();

@@ -203,7 +203,8 @@ bool jit_available(std::string *why) {
 // ---------------------------------------------------------------- codegen ----
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init,
-                            std::vector<std::pair<uint64_t, uint64_t>> *cwide) {
+                            std::vector<std::pair<uint64_t, uint64_t>> *cwide, const std::vector<double2> *hblob) {
+    static const bool no_sparse = getenv("HHLSV_JIT_NOSPARSE") != nullptr;
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
@@ -672,6 +673,12 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             for (int cc = 0; cc < D; cc++) {
                                 const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
                                 for (int q = 0; q < RU; q++) {
+                                    // one row block (RU == D): exact structural zeros of the matrix (e.g. the
+                                    // identity padding of the system register in V) are skipped at codegen
+                                    if (hblob && RU == D && !no_sparse) {
+                                        const double2 e = (*hblob)[op.data_off + (size_t)q * D + cc];
+                                        if (e.x == 0.0 && e.y == 0.0) continue;
+                                    }
                                     const std::string w = "cwa.w[" + std::to_string(cs0->second + cc) + " + (r + " + std::to_string(q) +
                                                           ") * " + std::to_string(D) + "]";
                                     if (real)

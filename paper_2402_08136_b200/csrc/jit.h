@@ -34,7 +34,8 @@ bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr,
                             const InitSpec *init = nullptr,
-                            std::vector<std::pair<uint64_t, uint64_t>> *cwide = nullptr);
+                            std::vector<std::pair<uint64_t, uint64_t>> *cwide = nullptr,
+                            const std::vector<double2> *hblob = nullptr);   // host blob: structural zeros
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.
