@@ -155,6 +155,19 @@ __device__ __forceinline__ double2 mk(double x, double y) { double2 r; r.x = x; 
 __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
     return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+#ifdef HHLSV_LDT   // experiment: read-only tables kept in L1 (evict_last)
+__device__ __forceinline__ double2 ldt(const double2 *p) {
+    double2 v;
+    asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldt(const double *p) {
+    double v;
+    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+#define __ldg ldt
+#endif
 __device__ __forceinline__ double recip_s(u64 m, int n_c, double dL, int sg, double snap) {
     if (m == 0) return 0.0;
     double sign = 1.0;
@@ -1072,6 +1085,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O3"};
     if (const char *x = getenv("HHLSV_JIT_OPT")) opts.back() = x;     // experiments
     if (getenv("HHLSV_JIT_CLOBBER")) opts.push_back("-DHHLSV_SMEM_CLOBBER");
+    if (getenv("HHLSV_JIT_LDT")) opts.push_back("-DHHLSV_LDT");
     int rc = n.compile(prog, (int)opts.size(), opts.data());
     if (rc) {
         size_t ls = 0;
