@@ -179,6 +179,8 @@ __device__ __forceinline__ double recip_s(u64 m, int n_c, double dL, int sg, dou
 }
 )";
 
+uint32_t swz_host(uint32_t u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12)) & 7u); }
+
 int dep_slot(int c, int M) {   // deposit bits of c into the set bits of M (4-bit register masks)
     int out = 0, bit = 0;
     for (int i = 0; i < 4; i++)
@@ -357,6 +359,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     if (const char *e = getenv("HHLSV_JIT_DIRECT")) low3 = low3 && atoi(e) != 0;
     const bool din = nbuf == 1 && low3 && ph.front().R[0] >= 3;
     static const bool pf_on = !getenv("HHLSV_JIT_NOPF");
+    static const bool lin_swz = !getenv("HHLSV_JIT_NOLINSWZ");
+    auto sref = [&](int c) {       // shared-memory slot of register slot c (tile-local bits) in this phase
+        std::ostringstream o;
+        if (lin_swz) o << "cur[stb ^ " << swz_host((uint32_t)c) << "u]";
+        else o << "cur[swz(tb | " << c << "u)]";
+        return o.str();
+    };
     // cross-tile register prefetch: the next tile's phase-0 loads are issued right after this tile's
     // last stores, so their latency overlaps the tile-end barrier and the next sub-table builds
     static std::atomic<int> xpf_count{0};
@@ -547,6 +556,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << "    { // phase " << p << "\n      const u32 tb = 0u";
         for (int i = 0; i < T - dev::kRegBits; i++) k << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
         k << ";\n";
+        // the swizzle is XOR-linear and tb / slot bits are disjoint: swz(tb | c) = swz(tb) ^ swz(c), so a
+        // register slot's shared-memory index is one XOR with a codegen constant
+        if (lin_swz) k << "      const u32 stb = swz(tb);\n";
         int rd[16];
         for (int j = 0; j < 16; j++) {
             rd[j] = 0;
@@ -586,7 +598,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      const double2 *gin = psi + (base | pd_in);\n";
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
         } else {
-            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = " << sref(rd[j]) << ";\n";
         }
         // The last op of a last phase that stores through shared memory is a wide dense op without
         // controls: its rows are written to their final shared-memory slots, so neither the register
@@ -734,7 +746,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                     k << "\n";
                                 }
                                 for (int q = 0; q < RU; q++)
-                                    k << "            cur[swz(tb | " << rd[g | dep_slot(r0 + q, M)] << "u)] = mk(ax" << q << ", ay" << q << ");\n";
+                                    k << "            " << sref(rd[g | dep_slot(r0 + q, M)]) << " = mk(ax" << q << ", ay" << q << ");\n";
                                 k << "          }\n";
                             }
                         } else if (ws0 != wstage.end()) {
@@ -785,13 +797,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 else
                                     k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
                                       << row("Ur");
-                                k << " cur[swz(tb | " << rd[g | dep_slot(r, M)] << "u)] = mk(ax, ay); }\n";
+                                k << " " << sref(rd[g | dep_slot(r, M)]) << " = mk(ax, ay); }\n";
                             }
                         }
                         if (!tail_in_smem)      // else: the outputs already sit in their final smem slots
                             for (int r = 0; r < D; r++) {
                                 const int j = g | dep_slot(r, M);
-                                k << "          v" << j << " = cur[swz(tb | " << rd[j] << "u)];\n";
+                                k << "          v" << j << " = " << sref(rd[j]) << ";\n";
                             }
                         k << "        }\n";
                         continue;
@@ -1038,7 +1050,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "    }\n";
         } else {
             if (!tail_in_smem)
-                for (int j = 0; j < 16; j++) k << "      cur[swz(tb | " << rd[j] << "u)] = v" << j << ";\n";
+                for (int j = 0; j < 16; j++) k << "      " << sref(rd[j]) << " = v" << j << ";\n";
             hoisted();
             k << "      bar();\n    }\n";
         }
