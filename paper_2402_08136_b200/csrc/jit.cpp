@@ -1045,7 +1045,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
-            for (int j = 0; j < 16; j++) k << "      __stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+            static const bool plain_st = getenv("HHLSV_JIT_PLAINST") != nullptr;     // experiment: st.global.wb
+            for (int j = 0; j < 16; j++)
+                k << "      " << (plain_st ? "gout[" : "__stcs(gout + ") << u64s(phys_slot(P, j)) << (plain_st ? "] = v" : ", v") << j
+                  << (plain_st ? ";\n" : ");\n");
             hoisted();
             k << "    }\n";
         } else {
