@@ -114,3 +114,28 @@ def test_gpu_sample_sharded_state_refused():
     st.write(synthetic.random_state(10, 1))
     with pytest.raises(pkg.SVError):
         st.sample(10, seed=1)
+
+
+@pytest.mark.gpu
+def test_gpu_sample_s30_postselection_rate():
+    """Full bench size (S30, 2^30 amplitudes, the bench's launch configuration): 10^5 shots from the
+    final HHL state; the fraction with ancilla = 1 and clock = 0 (R7) matches P_succ
+    within 5 sigma, and every post-selected shot's system index lies in the 16-state data register."""
+    import paper_2402_08136_b200 as pkg
+    from workloads import configs
+    A, b, nc = configs.get("S30")
+    n = configs.n_qubits("S30")
+    st = pkg.State(n)
+    prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, fusion_kmax=1, tile_qubits=12, qpe_mode=1)
+    prog.run()
+    _, p_succ = prog.readout()
+    shots = 100000
+    s = st.sample(shots, seed=2402).astype(np.uint64)
+    anc = (s >> np.uint64(n - 1)) & np.uint64(1)
+    clock = (s >> np.uint64(4)) & np.uint64((1 << nc) - 1)
+    hit = (anc == 1) & (clock == 0)
+    frac = hit.mean()
+    sigma = np.sqrt(p_succ * (1 - p_succ) / shots)
+    assert abs(frac - p_succ) < 5 * sigma, (frac, p_succ)
+    # the post-selected shots are the slice's logical indices: 2^(n-1) + s_sys, s_sys < 16
+    assert ((s[hit] - np.uint64(1 << (n - 1))) < np.uint64(16)).all()
