@@ -228,6 +228,16 @@ typedef struct {
                            c-U_j = V diag(e^{2 pi i frac(2^j phi_s)}) V^T, so the controlled chain becomes
                            V^T, one diagonal phase factor per clock bit over (system, clock bit), V — the
                            same unitary (parity is checked against the textbook oracle) */
+    /* Optional caller-supplied eigendecomposition of the PADDED (and, for a non-symmetric A,
+     * Hermitian-embedded) N_p x N_p system matrix (N_p = 2^n_data), used instead of the library's
+     * Jacobi eigensolver (step 2 of PAPER.md:156-199): eig_lambda[s] (N_p doubles) and eig_vectors
+     * (N_p x N_p, row-major, column s = unit eigenvector of eig_lambda[s]: the numpy.linalg.eigh
+     * layout). Both NULL (default) -> the library computes them. Checked: SV_E_ARG when
+     * max|A v_s - lambda_s v_s| > 1e-8 max(1, max|lambda|) or V is not orthogonal to 1e-10.
+     * Use: reproducing another eigensolver's phases bit for bit (the HHL state is sensitive to
+     * phi_s with gain ~2 pi 2^n_c). */
+    const double *eig_lambda;
+    const double *eig_vectors;
 } hhl_options;
 
 typedef struct {
@@ -240,12 +250,19 @@ typedef struct {
     double t_frontend_s, t_sim_s;
     double h2d_bytes, d2h_bytes;   /* host<->device bytes of one solve (program upload, slice read) */
     int x_offset;                  /* Hermitian embedding of a non-symmetric A: x = lower half of the slice */
+    int n_orig;                    /* N of the caller's system (before padding / embedding) */
+    double b_norm;                 /* ||b||_2 of the caller's b (set by hhl_build_program / hhl_solve):
+                                      the scale of step 4's recovery, PAPER.md:193-198 */
+    double p_anc1;                 /* P(ancilla = 1) summed over every clock value (hhl_solve only;
+                                      the paper's "measure ancilla and get 1", before
+                                      the clock = 0 post-selection of R7) */
 } hhl_report;
 
-/* Build the HHL circuit for A (N×N, row-major, real; a non-symmetric A is embedded as
- * [[0, A], [A^T, 0]] [0; x] = [b; 0]) and b (N) and return it as a
- * program for `sv` (which must have n_b + n_c + 1 qubits; call hhl_plan_size first).
- * On return *b_norm, *lambda_min are what hhl_recover needs. */
+/* hhl_plan_size: the register sizes (n_data, n_clock, n_total) hhl_build_program needs for (A, b).
+ * hhl_build_program: build the HHL circuit for A (N×N, row-major, real; a non-symmetric A is embedded
+ * as [[0, A], [A^T, 0]] [0; x] = [b; 0]) and b (N) and return it as a program for
+ * `sv` (which must have n_total qubits). rep (optional) receives the plan (lambda_min, b_norm, sizes,
+ * schedule figures): it is what hhl_readout needs. */
 sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_options *opt, int *n_data,
                         int *n_clock, int *n_total);
 sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
@@ -256,10 +273,12 @@ sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int 
  * rep (may be NULL) receives the plan and schedule sizes; its timing fields are zero. */
 sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_options *opt, int world, char *buf,
                             size_t buf_len, hhl_report *rep);
-/* Read out and recover x (PAPER.md:193-198 read per F3/R8): x = ||b|| sqrt(P)/lambda_min |x>,
- * |x> = slice / sqrt(P), padding stripped; x_out has N doubles (real part). */
-sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out,
-                      double *p_success);
+/* Read out and recover x after the program ran (PAPER.md:193-198 step 4, read per F3/R8):
+ * post-select ancilla = 1, clock = 0 (R7), P = the slice's squared norm, |x> = slice / sqrt(P),
+ * x = rep->b_norm * sqrt(P) / rep->lambda_min * |x> (real part, padding / embedding stripped).
+ * rep = the report hhl_build_program filled. x_out has N doubles; N must equal rep->n_orig
+ * (SV_E_ARG otherwise). SV_E_ZEROPROB when P < 1e-12. p_success (optional) receives P. */
+sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double *x_out, double *p_success);
 /* Everything at once: create the state, build, run, read out, recover, destroy.
  * A, b, x_out are HOST buffers. dist = NULL for 1 GPU. */
 sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, const hhl_options *opt,

@@ -317,11 +317,30 @@ sv_status sv_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out) 
 
 // ------------------------------------------------------------------- HHL ----
 static double opt_snap(const hhl_options *o) { return (o && o->recip_snap >= 0.0) ? o->recip_snap : 1e-5; }
+static HHLPlanHost plan_of(const double *A, const double *b, int N, const hhl_options *o) {
+    return hhl_plan(A, b, N, o ? o->clock_qubits : 0, opt_snap(o), o ? o->eig_lambda : nullptr,
+                    o ? o->eig_vectors : nullptr);
+}
+// the plan fields of hhl_report (sizes, spectrum, delta/t, b_norm)
+static void report_plan(hhl_report *rep, const HHLPlanHost &p) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->lambda_min = p.lam_min;
+    rep->lambda_max = p.lam_max;
+    rep->kappa = p.kappa;
+    rep->delta = p.delta;
+    rep->t_evol = p.t;
+    rep->n_data = p.n_b;
+    rep->n_clock = p.n_c;
+    rep->n_total = p.n;
+    rep->x_offset = p.x_offset;
+    rep->n_orig = p.n_orig;
+    rep->b_norm = p.b_norm;
+}
 
 sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_options *opt, int *n_data, int *n_clock,
                         int *n_total) {
     return guard([&] {
-        HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+        HHLPlanHost p = plan_of(A, b, N, opt);
         if (n_data) *n_data = p.n_b;
         if (n_clock) *n_clock = p.n_c;
         if (n_total) *n_total = p.n;
@@ -355,9 +374,8 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
 // coalesced low bits (direct register->HBM stores instead of a shared-memory round trip).
 static std::vector<int> hhl_layout(const HHLPlanHost &p, const hhl_options *opt, int world) {
     // Measured on S30: mode 1 makes the V pass 11.7 -> 8.1 ms but the greedy packer then
-    // loads the middle pass with 79 ops (12.2 -> 17.4 ms): net slower, so the default stays identity;
-    // HHLSV_LAYOUT=1|2 selects a variant for experiments.
-    static const int mode = getenv("HHLSV_LAYOUT") ? atoi(getenv("HHLSV_LAYOUT")) : 0;
+    // loads the middle pass with 79 ops (12.2 -> 17.4 ms): net slower, so the default stays identity.
+    const int mode = 0;
     if (mode == 0 || world != 1 || !opt || opt->qpe_mode != 1 || opt->tile_qubits < 0 || p.n_c < 4) return {};
     std::vector<int> phys(p.n, -1);
     std::vector<int> low;                                          // logical qubits at physical 0..2
@@ -383,10 +401,10 @@ static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost
 }
 
 static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
-                             hhl_report *rep, double *b_norm_out) {
+                             hhl_report *rep) {
     const double t0 = now_s();
     prof_mark("build_hhl start");
-    HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+    HHLPlanHost p = plan_of(A, b, N, opt);
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
     prof_mark("hhl_plan");
     std::vector<ProductFactor> factors;
@@ -397,15 +415,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
                                       n_logical);
     prof_mark("program_create");
     if (rep) {
-        std::memset(rep, 0, sizeof(*rep));
-        rep->lambda_min = p.lam_min;
-        rep->lambda_max = p.lam_max;
-        rep->kappa = p.kappa;
-        rep->delta = p.delta;
-        rep->t_evol = p.t;
-        rep->n_data = p.n_b;
-        rep->n_clock = p.n_c;
-        rep->n_total = p.n;
+        report_plan(rep, p);
         rep->n_logical = n_logical;
         rep->n_fused = prog->sched.n_fused;
         rep->n_passes = prog->sched.n_passes;
@@ -413,10 +423,8 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
         rep->pass_bytes = prog->sched.pass_bytes;
         rep->h2d_bytes = prog->h2d_bytes;
         rep->d2h_bytes = 16.0 * (double)(1ull << p.n_b) + 8.0;
-        rep->x_offset = p.x_offset;
         rep->t_frontend_s = now_s() - t0;
     }
-    if (b_norm_out) *b_norm_out = p.b_norm;
     return prog;
 }
 
@@ -425,13 +433,16 @@ sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int 
     return guard([&] {
         if (!sv || !out) fail(SV_E_ARG, "null argument");
         *out = nullptr;
-        *out = build_hhl(sv, A, b, N, opt, rep, nullptr);
+        *out = build_hhl(sv, A, b, N, opt, rep);
     });
 }
 
-static void readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_out) {
+static void readout(sv_state *sv, const hhl_report *rep, int N, double *x_out, double *p_out) {
     const int nb = rep->n_data, nc = rep->n_clock, n = rep->n_total;
-    if (n != sv->n) fail(SV_E_ARG, "report does not match the state");
+    if (n != sv->n || nb < 1 || nc < 1 || nb + nc + 1 != n) fail(SV_E_ARG, "report does not match the state");
+    if (N != rep->n_orig || N < 1 || rep->x_offset < 0 || (uint64_t)rep->x_offset + (uint64_t)N > (1ull << nb))
+        fail(SV_E_ARG, "N does not match the report (N must equal rep->n_orig)");
+    if (!(rep->lambda_min > 0.0) || !(rep->b_norm > 0.0)) fail(SV_E_ARG, "report lacks lambda_min / b_norm");
     std::vector<int> fq, fv;
     for (int j = 0; j < nc; j++) {
         fq.push_back(nb + j);
@@ -447,7 +458,7 @@ static void readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, d
     if (P < 1e-12) fail(SV_E_ZEROPROB, "post-selection probability below 1e-12");
     // x = ||b|| sqrt(P)/lambda_min * slice/sqrt(P)   (PAPER.md:193-198 read per F3/R8)
     if (x_out)
-        for (int i = 0; i < N; i++) x_out[i] = b_norm * amps[2 * (rep->x_offset + i)] / rep->lambda_min;
+        for (int i = 0; i < N; i++) x_out[i] = rep->b_norm * amps[2 * (rep->x_offset + i)] / rep->lambda_min;
 }
 
 sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_options *opt, int world, char *buf,
@@ -456,7 +467,7 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         if (world < 1 || (world & (world - 1))) fail(SV_E_ARG, "world must be a power of two");
         int g = 0;
         while ((1 << g) < world) g++;
-        HHLPlanHost p = hhl_plan(A, b, N, opt ? opt->clock_qubits : 0, opt_snap(opt));
+        HHLPlanHost p = plan_of(A, b, N, opt);
         if (p.n - g < 1) fail(SV_E_ARG, "too many ranks for this system");
         std::vector<ProductFactor> factors;
         size_t n_logical = 0;
@@ -467,21 +478,12 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         if (!hco.phys_init.empty()) phys = hco.phys_init;
         Schedule s = compile(fused, nullptr, p.n, p.n - g, phys, hco);
         if (rep) {
-            std::memset(rep, 0, sizeof(*rep));
-            rep->lambda_min = p.lam_min;
-            rep->lambda_max = p.lam_max;
-            rep->kappa = p.kappa;
-            rep->delta = p.delta;
-            rep->t_evol = p.t;
-            rep->n_data = p.n_b;
-            rep->n_clock = p.n_c;
-            rep->n_total = p.n;
+            report_plan(rep, p);
             rep->n_logical = n_logical;
             rep->n_fused = s.n_fused;
             rep->n_passes = s.n_passes;
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
-            rep->x_offset = p.x_offset;
         }
         if (buf && buf_len) {
             std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s);
@@ -493,10 +495,10 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
     });
 }
 
-sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double b_norm, double *x_out, double *p_success) {
+sv_status hhl_readout(sv_state *sv, const hhl_report *rep, int N, double *x_out, double *p_success) {
     return guard([&] {
         if (!sv || !rep) fail(SV_E_ARG, "null argument");
-        readout(sv, rep, N, b_norm, x_out, p_success);
+        readout(sv, rep, N, x_out, p_success);
     });
 }
 
@@ -509,19 +511,23 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         if (clock_qubits > 0) o.clock_qubits = clock_qubits;
         if (!opt) o.recip_snap = -1.0;
         prof_mark("hhl_solve start");
-        HHLPlanHost p = hhl_plan(A, b, N, o.clock_qubits, opt_snap(&o));
+        HHLPlanHost p = plan_of(A, b, N, &o);
         // the HHL program starts with its own initialisation step: no |0...0> fill needed
         sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream, false);
         prof_mark("state_create");
         sv_program *prog = nullptr;
         try {
             hhl_report r{};
-            double bn = 0.0;
-            prog = build_hhl(sv, A, b, N, &o, &r, &bn);
+            prog = build_hhl(sv, A, b, N, &o, &r);
             const double t0 = now_s();
             program_run(sv, prog);
-            r.norm2 = state_norm2(sv);
-            readout(sv, &r, N, bn, x_out, &r.p_success);
+            // one reduction gives the norm and P(ancilla = 1) (logical qubit n-1)
+            double pa[2] = {0.0, 0.0};
+            const int anc = p.n - 1;
+            state_probabilities(sv, &anc, 1, pa);
+            r.norm2 = pa[0] + pa[1];
+            r.p_anc1 = pa[1];
+            readout(sv, &r, N, x_out, &r.p_success);
             r.t_sim_s = now_s() - t0;
             prof_mark("run + readout");
             if (rep) *rep = r;

@@ -20,6 +20,7 @@
 #include <set>
 #include <sstream>
 
+#include "jit.h"
 #include "sv_internal.h"
 
 namespace hhlsv {
@@ -291,7 +292,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     const int T = std::min(o.tile_qubits, nloc);
     const bool tiles = o.tile_qubits > 0 && nloc >= o.reg_bits + 3;
     int wmin_opt = o.wmin;   // default 3 (128-byte segments): more tile bits for op targets per pass
-    if (const char *e = getenv("HHLSV_WMIN")) wmin_opt = atoi(e);     // developer experiments
+    if (jit_config().wmin != 3) wmin_opt = jit_config().wmin;     // developer experiments (HHLSV_JIT=wmin=..)
     const int wmin = std::min(wmin_opt, T - o.reg_bits);
     const int R = o.reg_bits;
     // single-rank tile schedules: commutation-aware reordering for packing (multi-rank keeps the
@@ -322,8 +323,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
         tile.tile_bits = set;
         // register phases: each phase's ops have their nd targets inside R (|R| <= reg_bits)
         phase_schedule(tile.tile_ops, R, tile.phase_R, tile.phase_start);
-        static const int dm_env = getenv("HHLSV_DIAG_MERGE") ? atoi(getenv("HHLSV_DIAG_MERGE")) : -1;   // experiments
-        const int dm = dm_env >= 0 ? dm_env : o.diag_merge;
+        const int dm = jit_config().diag_merge >= 0 ? jit_config().diag_merge : o.diag_merge;
         if (dm > 0) merge_phase_diagonals(tile, dm);
         // Fill each phase's register set up to R bits with the highest tile bits (lanes keep the
         // low ones), except bits a reciprocal rotation of the phase reads as clock bits: those would

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <mutex>
+
 #include "engine.h"
 
 namespace hhlsv {
@@ -19,26 +21,49 @@ static void nccl_check(int rc, const char *what) {
 }
 
 // ------------------------------------------------------------------ state ----
-// State buffers come from the device's stream-ordered memory pool with an unbounded release
-// threshold: freeing a 16 GiB state and creating the next one (hhl_solve called repeatedly)
-// reuses the pool instead of unmapping/remapping pages (HHLSV_NO_POOL=1 disables).
+// State buffers come from a stream-ordered memory pool OWNED BY THE LIBRARY (one per device, never
+// the process-wide default pool, so other allocators in the process -- e.g. torch -- are not
+// starved) with an unbounded release threshold: freeing a 16 GiB state and creating the next one
+// (hhl_solve called repeatedly) reuses the pool instead of unmapping/remapping pages. When the last
+// live state of the process is destroyed the pool is trimmed to zero.
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+int g_live_states = 0;
+}  // namespace
+
+static cudaMemPool_t lib_pool(int device) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (device < 0 || device >= 64) fail(SV_E_ARG, "device index out of range");
+    if (!g_pools[device]) {
+        cudaMemPoolProps pr{};
+        pr.allocType = cudaMemAllocationTypePinned;
+        pr.handleTypes = cudaMemHandleTypeNone;
+        pr.location.type = cudaMemLocationTypeDevice;
+        pr.location.id = device;
+        cuda_check(cudaMemPoolCreate(&g_pools[device], &pr), "cudaMemPoolCreate");
+        uint64_t thr = UINT64_MAX;
+        cuda_check(cudaMemPoolSetAttribute(g_pools[device], cudaMemPoolAttrReleaseThreshold, &thr), "pool threshold");
+    }
+    return g_pools[device];
+}
+
+// Bytes the library pool of `device` holds reserved but not in use (reusable by the next state).
+static size_t pool_slack(int device) {
+    cudaMemPool_t pool = lib_pool(device);
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return reserved > used ? (size_t)(reserved - used) : 0;
+}
+
 static cudaError_t state_alloc(void **p, size_t bytes, cudaStream_t s, int device) {
-    static const bool no_pool = getenv("HHLSV_NO_POOL") != nullptr;
-    if (no_pool) return cudaMalloc(p, bytes);
-    cudaMemPool_t pool;
-    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
-    if (e != cudaSuccess) return e;
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    e = cudaMallocAsync(p, bytes, s);
+    cudaError_t e = cudaMallocFromPoolAsync(p, bytes, lib_pool(device), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return e;
 }
 static void state_free(void *p, cudaStream_t s) {
-    static const bool no_pool = getenv("HHLSV_NO_POOL") != nullptr;
-    if (!p) return;
-    if (no_pool) cudaFree(p);
-    else cudaFreeAsync(p, s);
+    if (p) cudaFreeAsync(p, s);
 }
 
 // Small per-state / per-program device buffers also come from the stream-ordered pool: a plain
@@ -85,6 +110,7 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
     const size_t bytes = sizeof(double2) << sv->nloc;
     size_t freeb = 0, totb = 0;
     cuda_check(cudaMemGetInfo(&freeb, &totb), "cudaMemGetInfo");
+    freeb += pool_slack(device);     // reserved by the library pool but free for reuse
     if (bytes * (virt ? world : 1) > freeb) fail(SV_E_OOM, "state does not fit in device memory");
     if (virt) {
         sv->vworld = world;
@@ -114,14 +140,21 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
     cuda_check(pool_malloc((void **)&sv->d_scalar, sizeof(double) * 8, stream), "cudaMalloc(scalar)");
     if (world > 1 && !virt) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
     if (zero_init) state_reset(sv.get());
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_live_states++;
+    }
     return sv.release();
 }
 
-void state_destroy(sv_state *sv) {
+static void destroy_impl(sv_state *sv, bool top);
+void state_destroy(sv_state *sv) { destroy_impl(sv, true); }
+
+static void destroy_impl(sv_state *sv, bool top) {
     if (!sv) return;
     cudaStreamSynchronize(sv->stream);
     if (sv->vworld > 1) {
-        for (auto *v : sv->views) state_destroy(v);
+        for (auto *v : sv->views) destroy_impl(v, false);
         sv->views.clear();
         sv->psi = nullptr;
     }
@@ -132,7 +165,15 @@ void state_destroy(sv_state *sv) {
     pool_free(sv->d_xsend, sv->stream);
     pool_free(sv->d_xrecv, sv->stream);
     nccl_destroy(sv->comm);
+    const int device = sv->device;
+    cudaStreamSynchronize(sv->stream);
     delete sv;
+    if (!top) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (--g_live_states <= 0) {      // last live state: hand the pool's memory back to the device
+        g_live_states = 0;
+        if (device >= 0 && device < 64 && g_pools[device]) cudaMemPoolTrimTo(g_pools[device], 0);
+    }
 }
 
 void state_reset(sv_state *sv) {
@@ -629,7 +670,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     // (JIT only): the pass computes its tiles' amplitudes instead of reading them, and the init's
     // own full-state write disappears.
     const auto &steps = p->sched.steps;
-    const bool fuse_init = use_jit && !getenv("HHLSV_NO_INIT_FUSE") && steps.size() >= 2 &&
+    const bool fuse_init = use_jit && jit_config().init_fuse && steps.size() >= 2 &&
                            steps[0].kind == StepKind::InitProduct && steps[1].kind == StepKind::Tile;
     InitSpec init_spec;
     if (fuse_init) {
@@ -803,28 +844,6 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         LaunchRec &rec = p->recs[r];
         if (rec.kind == StepKind::Dense) rec.dense.U = p->d_blob + (size_t)rec.dense.U;
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
-    }
-    if (const char *dir = getenv("HHLSV_EMU_DUMP")) {      // debug: launch list + blob for host emulation
-        if (FILE *f = fopen((std::string(dir) + "/blob.bin").c_str(), "wb")) {
-            fwrite(blob.data(), sizeof(double2), blob.size(), f);
-            fclose(f);
-        }
-        if (FILE *f = fopen((std::string(dir) + "/program.txt").c_str(), "w")) {
-            for (const LaunchRec &r : p->recs) {
-                if (r.kind == StepKind::Tile && r.jit >= 0) {
-                    const auto &cw = p->jit[r.jit].cwvals;
-                    fprintf(f, "TILE %s %llu %d %llu %zu %d\n", jit_source_tag(p->jit[r.jit].src).c_str(),
-                            (unsigned long long)r.tile.n_tiles, r.tile.T, (unsigned long long)r.tile.rank_base,
-                            p->jit[r.jit].smem_extra, r.jit);
-                    if (FILE *g = fopen((std::string(dir) + "/cw_" + std::to_string(r.jit) + ".bin").c_str(), "wb")) {
-                        fwrite(cw.data(), sizeof(double2), cw.size(), g);
-                        fclose(g);
-                    }
-                } else
-                    fprintf(f, "OTHER %d %d\n", (int)r.kind, (int)r.skip);
-            }
-            fclose(f);
-        }
     }
     prof_mark("  lower + upload");
     if (!p->jit.empty()) jit_build(p->jit);

@@ -20,6 +20,7 @@
 #include <numeric>
 #include <stdexcept>
 
+#include "jit.h"
 #include "sv_internal.h"
 
 namespace hhlsv {
@@ -174,7 +175,8 @@ void jacobi_eigh(int N, std::vector<double> A, std::vector<double> &lam, std::ve
 // Step 1 of the procedure box: normalise b, expand to a power of two
 // (identity padding, R9); eigen-analysis; n_QPE from the resources formula read per
 // F3 (R2/R3: +1 sign qubit always); delta and t per qlsarepo (R4); phi_s per R13.
-HHLPlanHost hhl_plan(const double *A, const double *b, int N0, int clock_qubits, double snap) {
+HHLPlanHost hhl_plan(const double *A, const double *b, int N0, int clock_qubits, double snap, const double *eig_lam,
+                     const double *eig_V) {
     if (!A || !b || N0 < 1) fail(SV_E_ARG, "hhl: null A/b or N < 1");
     HHLPlanHost p;
     p.n_orig = N0;
@@ -216,7 +218,31 @@ HHLPlanHost hhl_plan(const double *A, const double *b, int N0, int clock_qubits,
     p.b_hat.assign(N, 0.0);
     for (int i = 0; i < N0; i++) p.b_hat[i] = b[i] / bn;
     p.b_norm = bn;
-    jacobi_eigh(N, p.A, p.lam, p.V);
+    if (!eig_lam != !eig_V) fail(SV_E_ARG, "hhl: eig_lambda and eig_vectors must be given together");
+    if (eig_lam) {
+        // caller-supplied eigendecomposition (hhl_options.eig_*): row-major V, column s <-> lambda_s
+        p.lam.assign(eig_lam, eig_lam + N);
+        p.V.assign((size_t)N * N, 0.0);
+        double lmax = 1.0;
+        for (int s = 0; s < N; s++) lmax = std::max(lmax, std::fabs(p.lam[s]));
+        for (int i = 0; i < N; i++)
+            for (int s = 0; s < N; s++) p.V[i + (size_t)N * s] = eig_V[(size_t)i * N + s];
+        for (int s = 0; s < N; s++) {
+            for (int i = 0; i < N; i++) {
+                double av = 0.0;
+                for (int j = 0; j < N; j++) av += p.A[(size_t)i * N + j] * p.V[j + (size_t)N * s];
+                if (!(std::fabs(av - p.lam[s] * p.V[i + (size_t)N * s]) <= 1e-8 * lmax))
+                    fail(SV_E_ARG, "hhl: eig_vectors/eig_lambda do not diagonalise the padded A");
+            }
+            for (int r = 0; r < N; r++) {
+                double d = 0.0;
+                for (int i = 0; i < N; i++) d += p.V[i + (size_t)N * s] * p.V[i + (size_t)N * r];
+                if (!(std::fabs(d - (r == s ? 1.0 : 0.0)) <= 1e-10)) fail(SV_E_ARG, "hhl: eig_vectors not orthonormal");
+            }
+        }
+    } else {
+        jacobi_eigh(N, p.A, p.lam, p.V);
+    }
     p.lam_min = INFINITY;
     p.lam_max = 0.0;
     for (double l : p.lam) {
@@ -309,8 +335,7 @@ static void append_eigen_chain(std::vector<Gate> &g, const HHLPlanHost &p, const
     // scheduler can place each factor in whichever pass holds its clock bit's QFT Hadamard; the
     // factors of one register phase are then merged after scheduling (compile.cpp
     // merge_phase_diagonals). Lets the final V join the last QFT pass.
-    int chunk = 1;
-    if (const char *e = getenv("HHLSV_EIGEN_CHUNK")) chunk = std::max(1, atoi(e));   // experiments
+    const int chunk = jit_config().eigen_chunk > 0 ? jit_config().eigen_chunk : 1;   // experiments
     std::vector<Gate> diags;
     for (int j0 = 0; j0 < nc; j0 += chunk) {
         const int cj = std::min(chunk, nc - j0);

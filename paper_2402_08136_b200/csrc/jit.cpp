@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <future>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -92,24 +93,22 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-// Shared memory through explicit 32-bit shared-window addresses (volatile asm keeps program order
-// between all shared accesses and barriers): nvcc's addressing form. NVRTC's default 64-bit
-// shared-pointer arithmetic trips a ptxas -O2/-O3 miscompilation on some of these kernels.
+// Shared memory through explicit 32-bit shared-window addresses (nvcc's addressing form; NVRTC's
+// default 64-bit shared-pointer arithmetic tripped a ptxas -O2/-O3 miscompilation on some of these
+// kernels). Every shared access and barrier is a volatile asm: the compiler keeps their program
+// order (volatile asm statements are never reordered with respect to each other); the
+// "memory" clobber is added when JitConfig::smem_clobber is set.
 #ifdef HHLSV_SMEM_CLOBBER
-__device__ __forceinline__ double2 lds(u32 a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory"); }
+#define HHLSV_CLB : "memory"
 #else
+#define HHLSV_CLB
+#endif
 __device__ __forceinline__ double2 lds(u32 a) {
     double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) HHLSV_CLB);
     return v;
 }
-__device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y)); }
-#endif
+__device__ __forceinline__ void sts(u32 a, double2 v) { asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) HHLSV_CLB); }
 __device__ __forceinline__ u64 lds64(u32 a) {
     u64 v;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
@@ -155,19 +154,6 @@ __device__ __forceinline__ double2 mk(double x, double y) { double2 r; r.x = x; 
 __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
     return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
-#ifdef HHLSV_LDT   // experiment: read-only tables kept in L1 (evict_last)
-__device__ __forceinline__ double2 ldt(const double2 *p) {
-    double2 v;
-    asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ldt(const double *p) {
-    double v;
-    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-#define __ldg ldt
-#endif
 __device__ __forceinline__ double recip_s(u64 m, int n_c, double dL, int sg, double snap) {
     if (m == 0) return 0.0;
     double sign = 1.0;
@@ -209,6 +195,46 @@ std::string runs_expr(const char *src, int n, const uint8_t *s, const uint8_t *l
 }
 }  // namespace
 
+const JitConfig &jit_config() {
+    static const JitConfig c = [] {
+        JitConfig x;
+        const char *e = getenv("HHLSV_JIT");
+        if (!e) return x;
+        std::string all(e);
+        size_t pos = 0;
+        while (pos <= all.size()) {
+            size_t end = all.find(',', pos);
+            if (end == std::string::npos) end = all.size();
+            const std::string kv = all.substr(pos, end - pos);
+            pos = end + 1;
+            const size_t eq = kv.find('=');
+            if (eq == std::string::npos) continue;
+            const std::string key = kv.substr(0, eq), val = kv.substr(eq + 1);
+            const int iv = atoi(val.c_str());
+            if (key == "direct") x.direct = iv != 0;
+            else if (key == "pf") x.prefetch = iv != 0;
+            else if (key == "pfdist") x.pf_dist = std::max(1, iv);
+            else if (key == "group") x.group = iv != 0;
+            else if (key == "rtab") x.rtab = iv != 0;
+            else if (key == "hoist") x.hoist = iv != 0;
+            else if (key == "sparse") x.sparse = iv != 0;
+            else if (key == "tail") x.tail = iv != 0;
+            else if (key == "cw") x.cw = iv != 0;
+            else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
+            else if (key == "minb") x.min_blocks = std::max(0, iv);
+            else if (key == "ru") x.ru = std::max(0, iv);
+            else if (key == "clobber") x.smem_clobber = iv != 0;
+            else if (key == "ptxas") x.ptxas_opt = "-Xptxas=" + val;
+            else if (key == "wmin") x.wmin = std::max(0, iv);
+            else if (key == "dmerge") x.diag_merge = iv;
+            else if (key == "echunk") x.eigen_chunk = std::max(0, iv);
+            else if (key == "initfuse") x.init_fuse = iv != 0;
+        }
+        return x;
+    }();
+    return c;
+}
+
 bool jit_available(std::string *why) {
     Nvrtc &n = nvrtc();
     if (why) *why = n.why;
@@ -219,7 +245,7 @@ bool jit_available(std::string *why) {
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init,
                             std::vector<std::pair<uint64_t, uint64_t>> *cwide, const std::vector<double2> *hblob) {
-    static const bool no_sparse = getenv("HHLSV_JIT_NOSPARSE") != nullptr;
+    const JitConfig &cfg = jit_config();
     const int T = a.T;
     const int NTHR = 1 << (T - dev::kRegBits);
     const int SA = (T + 1) / 2, SB = T - SA;
@@ -232,11 +258,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // no shared-memory or L1 traffic for the matrix), up to 64 KB per pass module.
     std::map<int, size_t> cstage;      // op index -> offset (double2 units) in cw[]
     size_t ctot = 0;
-    static const bool no_cw = getenv("HHLSV_JIT_NOCW") != nullptr;
-    static std::atomic<int> gen_count{0};
-    const int gen_idx = gen_count++;
-    const bool cw_only_skip = getenv("HHLSV_JIT_CWONLY") && atoi(getenv("HHLSV_JIT_CWONLY")) != gen_idx;   // debug
-    if (cwide && !no_cw && !cw_only_skip) {
+    if (cwide && cfg.cw) {
         for (size_t i = 0; i < ops.size(); i++) {
             const auto &op = ops[i];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
@@ -273,7 +295,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // and ONE complex multiply for the whole run. Used when 2^|V| is small.
     struct DRun { int p, a, b; std::vector<int> V; size_t off; };
     std::vector<DRun> druns, rtabs;
-    static const bool no_rtab = getenv("HHLSV_JIT_NORTAB") != nullptr;
     size_t dsub_max = 0;
     std::vector<size_t> used_ph;
     auto op_vary = [&](const dev::RegOp &op, const dev::RegPhase &P) {
@@ -308,7 +329,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // reciprocal rotation: its (s_m, c_m) pairs over the tile's clock bits precomputed per tile
         // (one division + square root per table entry instead of one per clock value per thread)
         for (int oi = ph[p].op0; oi < ph[p].op1; oi++) {
-            if (ops[oi].kind != 2 || no_rtab) continue;
+            if (ops[oi].kind != 2 || !cfg.rtab) continue;
             std::vector<int> V = op_vary(ops[oi], ph[p]);
             std::sort(V.begin(), V.end());
             if (V.size() <= 9 && (1u << V.size()) <= 2u * (1u << (T - dev::kRegBits))) {
@@ -324,7 +345,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // so the barrier that ends phase p also publishes them: no separate barrier per sub-table build.
     // Regions alternate 0/1 by phase; with an odd phase count the last phase takes region 2.
     const size_t nph = ph.size();
-    bool hoist = nph >= 2 && !getenv("HHLSV_JIT_NOHOIST");
+    bool hoist = nph >= 2 && cfg.hoist;
     auto region = [&](size_t q) { return (nph % 2 == 1 && q + 1 == nph) ? 2 : (int)(q % 2); };
     if (hoist) {
         size_t R[3] = {0, 0, 0};
@@ -343,8 +364,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
     // compute phases (default; measured faster than double buffering at half the occupancy),
     // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
-    int nbuf = 1;
-    if (const char *e = getenv("HHLSV_JIT_NBUF")) nbuf = atoi(e) == 2 ? 2 : 1;
+    int nbuf = cfg.nbuf == 2 ? 2 : 1;
     if (init) nbuf = 1;
     const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
                             dsub_max * 16;
@@ -356,25 +376,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // never passes through shared memory on the way in/out (saves 2 of the pass's smem sweeps
     // each way and the cp.async / store-loop address arithmetic).
     bool low3 = T >= 4 && a.tbits[0] == 0 && a.tbits[1] == 1 && a.tbits[2] == 2;
-    if (const char *e = getenv("HHLSV_JIT_DIRECT")) low3 = low3 && atoi(e) != 0;
+    low3 = low3 && cfg.direct;
     const bool din = nbuf == 1 && low3 && ph.front().R[0] >= 3;
-    static const bool pf_on = !getenv("HHLSV_JIT_NOPF");
-    static const bool lin_swz = !getenv("HHLSV_JIT_NOLINSWZ");
+    const bool pf_on = cfg.prefetch;
     auto sref = [&](int c) {       // shared-memory slot of register slot c (tile-local bits) in this phase
         std::ostringstream o;
-        if (lin_swz) o << "cur[stb ^ " << swz_host((uint32_t)c) << "u]";
-        else o << "cur[swz(tb | " << c << "u)]";
+        o << "cur[stb ^ " << swz_host((uint32_t)c) << "u]";
         return o.str();
     };
-    // cross-tile register prefetch: the next tile's phase-0 loads are issued right after this tile's
-    // last stores, so their latency overlaps the tile-end barrier and the next sub-table builds
-    static std::atomic<int> xpf_count{0};
-    const int xpf_idx = xpf_count++;
-    // Off by default (HHLSV_JIT_XPF=1 enables it): with it, ptxas -O2/-O3 (not -O1, source checked
-    // equivalent) produced wrong amplitudes for a T = 8 controlled/diagonal circuit
-    // (tests/test_gpu_parity.py::test_jit_small_tiles_wide_ops, seed 703), for ~0.3 ms on S30.
-    const bool xpf = din && !init && getenv("HHLSV_JIT_XPF") &&
-                     (!getenv("HHLSV_JIT_XPFONLY") || atoi(getenv("HHLSV_JIT_XPFONLY")) == xpf_idx);   // debug
     const bool dout = nbuf == 1 && low3 && ph.back().R[0] >= 3;
     auto tb_expr = [&](const dev::RegPhase &P) {
         std::ostringstream o;
@@ -388,7 +397,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             if ((j >> i) & 1) c |= 1ull << a.tbits[P.R[i]];
         return c;
     };
-    if (const char *e = getenv("HHLSV_JIT_MINB")) min_blocks = std::max(1, atoi(e));
+    if (cfg.min_blocks > 0) min_blocks = cfg.min_blocks;
     std::ostringstream k;
     if (ctot) k << "struct CWArg { double2 w[" << ctot << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
@@ -478,13 +487,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             return any_run;
         };
     k << "  u64 tile = blockIdx.x;\n";
-    if (xpf) {
-        k << "  double2 x0";
-        for (int j = 1; j < 16; j++) k << ", x" << j;
-        k << ";\n  { const double2 *gnx = psi + (tile_base(tile < n_tiles ? tile : n_tiles - 1) | pd_in);";
-        for (int j = 0; j < 16; j++) k << " x" << j << " = ldcs_v(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
-        k << " }\n";
-    }
     if (hoist) {
         k << "  if (tile < n_tiles) {\n";
         emit_pre(0, "rank_base | tile_base(tile)");
@@ -509,7 +511,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // L2 prefetch of this CTA's next tile: its HBM reads overlap this tile's compute, and the
         // next tile's loads then hit L2 (296 CTAs x 64 KB in flight << 126 MB L2)
         if (pf_on && !init) {
-            static const int pfd = getenv("HHLSV_JIT_PFDIST") ? std::max(1, atoi(getenv("HHLSV_JIT_PFDIST"))) : 1;
+            const int pfd = std::max(1, cfg.pf_dist);
             k << "    if (tile + " << pfd << "ull * gridDim.x < n_tiles) {\n      const u64 nb = tile_base(tile + " << pfd
               << "ull * gridDim.x);\n";
             if (din) {
@@ -558,7 +560,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         k << ";\n";
         // the swizzle is XOR-linear and tb / slot bits are disjoint: swz(tb | c) = swz(tb) ^ swz(c), so a
         // register slot's shared-memory index is one XOR with a codegen constant
-        if (lin_swz) k << "      const u32 stb = swz(tb);\n";
+        k << "      const u32 stb = swz(tb);\n";
         int rd[16];
         for (int j = 0; j < 16; j++) {
             rd[j] = 0;
@@ -592,8 +594,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 }
                 k << "        }\n      }\n";
             }
-        } else if (p == 0 && din && xpf) {
-            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = x" << j << ";\n";
         } else if (p == 0 && din) {
             k << "      const double2 *gin = psi + (base | pd_in);\n";
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
@@ -608,7 +608,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             const dev::RegOp &op = ops[oi];
             const int Kq = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
             return p + 1 == ph.size() && !dout && oi + 1 == P.op1 && op.kind == 0 && Kq >= 3 && !op.rcm && !op.tcm &&
-                   !op.gcm && !getenv("HHLSV_JIT_NOTAIL");
+                   !op.gcm && cfg.tail;
         };
         auto emit_single = [&](int oi) {
             tail_in_smem = tail_wide(oi);
@@ -683,15 +683,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         k << "        {\n";
                         auto ws0 = wstage.find(oi);
                         auto cs0 = cstage.find(oi);
-                        static const int cwru = getenv("HHLSV_JIT_CWRU") ? atoi(getenv("HHLSV_JIT_CWRU")) : 0;
-                        static const bool cw_unroll = getenv("HHLSV_JIT_CWUNROLL") != nullptr;
-                        if (cs0 != cstage.end() && !cw_unroll) {
-                            // rolled loop over blocks of RU rows (the fully unrolled form below gave wrong
-                            // results for some small-tile kernels, source equivalent -- kept behind
-                            // HHLSV_JIT_CWUNROLL for investigation); matrix entries from the by-value
-                            // kernel parameter (constant bank, uniform across the warp)
-                            static const int ru_env = getenv("HHLSV_JIT_RU") ? atoi(getenv("HHLSV_JIT_RU")) : 0;
-                            const int RU = std::min(D, ru_env > 0 ? ru_env : (real ? 16 : 2));   // measured: real 16 best
+                        if (cs0 != cstage.end()) {
+                            // rolled loop over blocks of RU rows; matrix entries from the by-value kernel
+                            // parameter (constant bank, uniform across the warp)
+                            const int RU = std::min(D, cfg.ru > 0 ? cfg.ru : (real ? 16 : 2));   // measured: real 16 best
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D << "; r += " << RU << ") {";
                             for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
                             k << "\n";
@@ -700,7 +695,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 for (int q = 0; q < RU; q++) {
                                     // one row block (RU == D): exact structural zeros of the matrix (e.g. the
                                     // identity padding of the system register in V) are skipped at codegen
-                                    if (hblob && RU == D && !no_sparse) {
+                                    if (hblob && RU == D && cfg.sparse) {
                                         const double2 e = (*hblob)[op.data_off + (size_t)q * D + cc];
                                         if (e.x == 0.0 && e.y == 0.0) continue;
                                     }
@@ -721,34 +716,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 k << "; cur[swz(tb | slot)] = mk(ax" << q << ", ay" << q << "); }\n";
                             }
                             k << "          }\n";
-                        } else if (cs0 != cstage.end()) {
-                            // fully unrolled blocks of RU rows, matrix entries as constant-bank operands
-                            const int RU = cwru > 0 ? cwru : (real ? 4 : 2);
-                            for (int r0 = 0; r0 < D; r0 += RU) {
-                                k << "          {";
-                                for (int q = 0; q < RU; q++) k << " double ax" << q << " = 0.0, ay" << q << " = 0.0;";
-                                k << "\n";
-                                for (int cc = 0; cc < D; cc++) {
-                                    const std::string in = "v" + std::to_string(g | dep_slot(cc, M));
-                                    k << "           ";
-                                    for (int q = 0; q < RU; q++) {
-                                        static const bool cwdbg = getenv("HHLSV_JIT_CWDBG") != nullptr;
-                                        const std::string w = cwdbg ? "__ldg(U + " + std::to_string((size_t)(r0 + q) * D + cc) + ")"
-                                                                    : "cwa.w[" + std::to_string(cs0->second + (size_t)(r0 + q) * D + cc) + "]";
-                                        if (real)
-                                            k << " ax" << q << " = fma(" << w << ".x, " << in << ".x, ax" << q << "); ay" << q << " = fma(" << w
-                                              << ".x, " << in << ".y, ay" << q << ");";
-                                        else
-                                            k << " ax" << q << " = fma(" << w << ".x, " << in << ".x, ax" << q << "); ax" << q << " = fma(-" << w
-                                              << ".y, " << in << ".y, ax" << q << "); ay" << q << " = fma(" << w << ".x, " << in << ".y, ay" << q
-                                              << "); ay" << q << " = fma(" << w << ".y, " << in << ".x, ay" << q << ");";
-                                    }
-                                    k << "\n";
-                                }
-                                for (int q = 0; q < RU; q++)
-                                    k << "            " << sref(rd[g | dep_slot(r0 + q, M)]) << " = mk(ax" << q << ", ay" << q << ");\n";
-                                k << "          }\n";
-                            }
                         } else if (ws0 != wstage.end()) {
                             // rolled loop over blocks of RU rows with RU independent accumulator pairs
                             // (ILP for the FMA chains); a real matrix is staged column-major as plain
@@ -780,7 +747,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                                 k << "; cur[swz(tb | slot)] = mk(ax" << q << ", ay" << q << "); }\n";
                             }
                             k << "          }\n";
-                        } else if (true) {   // rolled row loop: bounded registers (inputs stay in v) and code size
+                        } else {   // rolled row loop: bounded registers (inputs stay in v) and code size
                             k << "          #pragma unroll 1\n          for (int r = 0; r < " << D
                               << "; r++) { double ax = 0.0, ay = 0.0; const auto Ur = "
                               << (ws0 != wstage.end() ? "wm + " + std::to_string(ws0->second) + "u" : std::string("U"))
@@ -788,17 +755,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                               << " const u32 slot = " << rd[g] << "u";
                             for (int i = 0; i < K; i++) k << " | (((u32)r >> " << i << ") & 1u) << " << Rpos[i];
                             k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
-                        } else {
-                            auto ws = wstage.find(oi);
-                            for (int r = 0; r < D; r++) {
-                                if (ws != wstage.end())
-                                    k << "          { double ax = 0.0, ay = 0.0; const auto Ur = wm + " << ws->second + r * D
-                                      << "u;" << row_s("Ur");
-                                else
-                                    k << "          { double ax = 0.0, ay = 0.0; const double2 *Ur = U + " << r * D << ";"
-                                      << row("Ur");
-                                k << " " << sref(rd[g | dep_slot(r, M)]) << " = mk(ax, ay); }\n";
-                            }
                         }
                         if (!tail_in_smem)      // else: the outputs already sit in their final smem slots
                             for (int r = 0; r < D; r++) {
@@ -977,7 +933,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "      }\n";
         };
-        static const bool group_on = !getenv("HHLSV_JIT_NOGROUP");
+        const bool group_on = cfg.group;
         for (int oi = P.op0; oi < P.op1; oi++) {
             const DRun *run = nullptr;
             for (auto &dr : druns)
@@ -1014,8 +970,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 int oj = oi;
                 while (oj < P.op1 && ops[oj].kind == 1 && !in_run(oj)) oj++;
                 std::vector<int> G, C;
-                static const bool guard_sep = getenv("HHLSV_JIT_GUARDSEP") != nullptr;   // old form: guarded ops apart
-                for (int q = oi; q < oj; q++) ((guard_sep && (ops[q].gcm || ops[q].tcm)) ? C : G).push_back(q);
+                for (int q = oi; q < oj; q++) G.push_back(q);
                 if (G.size() >= 2) {
                     emit_group(G);
                     for (int q : C) emit_single(q);
@@ -1028,13 +983,6 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // hoisted sub-table build for the next phase (or the next tile's phase 0) after this phase's
         // registers are stored (they are dead: no extra register pressure), before the barrier
         auto hoisted = [&] {
-            if (xpf && p + 1 == nph) {      // next tile's phase-0 registers (this tile's are stored: dead)
-                // unconditional (clamped to the last tile) so x is dead between phase 0 and here
-                // past the last tile: reload this CTA's own tile (never another CTA's, which may be in flight)
-                k << "      { const u64 nt = tile + gridDim.x < n_tiles ? tile + gridDim.x : tile; const double2 *gnx = psi + (tile_base(nt) | pd_in);";
-                for (int j = 0; j < 16; j++) k << " x" << j << " = ldcs_v(gnx + " << u64s(phys_slot(ph.front(), j)) << ");";
-                k << " }\n";
-            }
             if (!hoist) return;
             if (p + 1 < nph) emit_pre(p + 1, "gbase");
             else {
@@ -1045,10 +993,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
-            static const bool plain_st = getenv("HHLSV_JIT_PLAINST") != nullptr;     // experiment: st.global.wb
-            for (int j = 0; j < 16; j++)
-                k << "      " << (plain_st ? "gout[" : "__stcs(gout + ") << u64s(phys_slot(P, j)) << (plain_st ? "] = v" : ", v") << j
-                  << (plain_st ? ";\n" : ");\n");
+            for (int j = 0; j < 16; j++) k << "      __stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
             hoisted();
             k << "    }\n";
         } else {
@@ -1067,10 +1012,17 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
 
 // ---------------------------------------------------------------- compile ----
 namespace {
+// One compiled + loaded tile kernel per distinct source text. The thread that inserts an entry owns
+// its compilation; every other thread that finds it (a concurrent program creation on another
+// thread, or the same source twice in one program) waits on `ready` until the owner has published
+// lib/kern/err. Only the owner erases a failed entry (so a later call can retry).
 struct CacheEntry {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
     std::string err;
+    std::promise<void> done;
+    std::shared_future<void> ready;
+    CacheEntry() : ready(done.get_future().share()) {}
 };
 std::mutex g_mu;
 std::map<std::string, std::shared_ptr<CacheEntry>> g_cache;
@@ -1098,9 +1050,9 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     // some tile kernels into illegal-address faults (source clean under host emulation with
     // ASan/UBSan, scripts/jit_emulate.py; same PTX fine at -O1).
     std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O3"};
-    if (const char *x = getenv("HHLSV_JIT_OPT")) opts.back() = x;     // experiments
-    if (getenv("HHLSV_JIT_CLOBBER")) opts.push_back("-DHHLSV_SMEM_CLOBBER");
-    if (getenv("HHLSV_JIT_LDT")) opts.push_back("-DHHLSV_LDT");
+    const JitConfig &cfg = jit_config();
+    if (!cfg.ptxas_opt.empty()) opts.back() = cfg.ptxas_opt.c_str();
+    if (cfg.smem_clobber) opts.push_back("-DHHLSV_SMEM_CLOBBER");
     int rc = n.compile(prog, (int)opts.size(), opts.data());
     if (rc) {
         size_t ls = 0;
@@ -1144,7 +1096,7 @@ void jit_build(std::vector<JitPass> &passes) {
     if (!nvrtc().ok) fail(SV_E_CUDA, "tile JIT unavailable: " + nvrtc().why);
     // compile the passes not yet in the cache in parallel (NVRTC programs are independent)
     std::vector<std::shared_ptr<CacheEntry>> ents(passes.size());
-    std::vector<size_t> todo;
+    std::vector<size_t> todo;       // entries this call owns
     {
         std::lock_guard<std::mutex> lk(g_mu);
         for (size_t i = 0; i < passes.size(); i++) {
@@ -1164,17 +1116,25 @@ void jit_build(std::vector<JitPass> &passes) {
         th.emplace_back([&, i] { cubins[i] = compile_cubin(passes[i].src, ents[i]->err); });
     for (auto &t : th) t.join();
     for (size_t i : todo) {
-        if (cubins[i].empty()) continue;
-        cudaError_t e = cudaLibraryLoadData(&ents[i]->lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-        if (e == cudaSuccess) e = cudaLibraryGetKernel(&ents[i]->kern, ents[i]->lib, passes[i].name.c_str());
-        if (e != cudaSuccess) ents[i]->err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        CacheEntry &e = *ents[i];
+        if (!cubins[i].empty()) {
+            cudaError_t rc = cudaLibraryLoadData(&e.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+            if (rc == cudaSuccess) rc = cudaLibraryGetKernel(&e.kern, e.lib, passes[i].name.c_str());
+            if (rc != cudaSuccess) {
+                e.kern = nullptr;
+                e.err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(rc);
+            }
+        }
+        if (!e.kern) {               // owner: drop the failed entry so a later build can retry
+            std::lock_guard<std::mutex> lk(g_mu);
+            auto it = g_cache.find(passes[i].src);
+            if (it != g_cache.end() && it->second == ents[i]) g_cache.erase(it);
+        }
+        e.done.set_value();          // publishes lib / kern / err to every waiter
     }
     for (size_t i = 0; i < passes.size(); i++) {
-        if (!ents[i]->kern) {
-            std::lock_guard<std::mutex> lk(g_mu);
-            g_cache.erase(passes[i].src);
-            fail(SV_E_CUDA, "tile JIT failed: " + ents[i]->err);
-        }
+        ents[i]->ready.wait();
+        if (!ents[i]->kern) fail(SV_E_CUDA, "tile JIT failed: " + ents[i]->err);
         passes[i].kern = ents[i]->kern;
     }
 }
@@ -1191,12 +1151,6 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     const void *f = reinterpret_cast<const void *>(p.kern);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    // shared-memory carveout: experiments (HHLSV_JIT_CARVEOUT = percent of the maximum shared memory;
-    // the rest of the 256 KB SM data memory stays L1 for the diagonal tables)
-    if (const char *cv = getenv("HHLSV_JIT_CARVEOUT")) {
-        e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
-        if (e != cudaSuccess) return e;
-    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem);
     if (e != cudaSuccess) return e;

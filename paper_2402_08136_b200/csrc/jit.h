@@ -30,6 +30,31 @@ struct InitSpec {
     std::vector<std::vector<int>> bits;      // per group: physical bits, table bit j <- bits[j]
 };
 
+// Code-generation switches of the tile JIT (all default on / measured best). Developer A/B
+// experiments only: parsed ONCE from HHLSV_JIT="key=value,..." (e.g. HHLSV_JIT=pf=0,group=0).
+struct JitConfig {
+    bool direct = true;       // direct: HBM <-> register first/last phases when the thread bits are coalesced
+    bool prefetch = true;     // pf: L2 prefetch of the CTA's next tile at the top of each tile
+    int pf_dist = 1;          // pfdist: prefetch distance in tiles
+    bool group = true;        // group: consecutive diagonal ops of a phase share per-slot factor products
+    bool rtab = true;         // rtab: per-tile (s_m, c_m) tables of the reciprocal rotation
+    bool hoist = true;        // hoist: phase p+1's sub-tables are built at the end of phase p
+    bool sparse = true;       // sparse: exact structural zeros of wide matrices skipped at codegen
+    bool tail = true;         // tail: a trailing wide dense op writes straight into the store buffer
+    bool cw = true;           // cw: >= 3-target matrices as by-value kernel parameters (constant bank)
+    int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
+    int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
+    int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)
+    bool smem_clobber = false;  // clobber: "memory" clobber on every shared-memory asm access
+    std::string ptxas_opt = "-Xptxas=-O3";   // ptxas: optimisation level passed to NVRTC's ptxas
+    // scheduler / front-end switches (same variable)
+    int wmin = 3;             // wmin: low physical bits every tile holds (3 = 128-byte segments)
+    int diag_merge = -1;      // dmerge: in-phase diagonal merge width (-1 = CompileOptions::diag_merge)
+    int eigen_chunk = 0;      // echunk: clock bits per eigen-phase table (0 = front-end default)
+    bool init_fuse = true;    // initfuse: product-state init computed inside the first tile pass
+};
+const JitConfig &jit_config();
+
 bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr,

@@ -66,7 +66,10 @@ struct HHLPlanHost {
     int x_offset = 0;                // Hermitian embedding: x is the lower half
 };
 
-HHLPlanHost hhl_plan(const double *A, const double *b, int N, int clock_qubits, double snap);
+// eig_lam / eig_V (optional, both or neither): caller-supplied eigendecomposition of the padded
+// matrix (hhl_options.eig_*; V row-major, column s <-> eig_lam[s]) instead of jacobi_eigh.
+HHLPlanHost hhl_plan(const double *A, const double *b, int N, int clock_qubits, double snap,
+                     const double *eig_lam = nullptr, const double *eig_V = nullptr);
 std::vector<Gate> hhl_build(const HHLPlanHost &p, int qpe_mode = 0);
 void jacobi_eigh(int N, std::vector<double> A, std::vector<double> &lam, std::vector<double> &V);
 

@@ -54,7 +54,8 @@ class sv_plan_report(ctypes.Structure):
 class hhl_options(ctypes.Structure):
     _fields_ = [("clock_qubits", ctypes.c_int), ("fusion_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
                 ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("tile_jit", ctypes.c_int),
-                ("diag_kmax", ctypes.c_int), ("qpe_mode", ctypes.c_int)]
+                ("diag_kmax", ctypes.c_int), ("qpe_mode", ctypes.c_int),
+                ("eig_lambda", ctypes.POINTER(ctypes.c_double)), ("eig_vectors", ctypes.POINTER(ctypes.c_double))]
 
 
 class hhl_report(ctypes.Structure):
@@ -64,7 +65,8 @@ class hhl_report(ctypes.Structure):
                 ("n_total", ctypes.c_int), ("n_logical", ctypes.c_uint64), ("n_fused", ctypes.c_uint64),
                 ("n_passes", ctypes.c_uint64), ("alg_bytes", ctypes.c_double), ("pass_bytes", ctypes.c_double),
                 ("t_frontend_s", ctypes.c_double), ("t_sim_s", ctypes.c_double), ("h2d_bytes", ctypes.c_double),
-                ("d2h_bytes", ctypes.c_double), ("x_offset", ctypes.c_int)]
+                ("d2h_bytes", ctypes.c_double), ("x_offset", ctypes.c_int), ("n_orig", ctypes.c_int),
+                ("b_norm", ctypes.c_double), ("p_anc1", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -119,7 +121,7 @@ def load(path: str = LIB_PATH):
         "hhl_schedule_dump": [P(c_dbl), P(c_dbl), c_int, P(hhl_options), c_int, ctypes.c_char_p, ctypes.c_size_t,
                               P(hhl_report)],
         "hhl_build_program": [vp, P(c_dbl), P(c_dbl), c_int, P(hhl_options), P(vp), P(hhl_report)],
-        "hhl_readout": [vp, P(hhl_report), c_int, c_dbl, P(c_dbl), P(c_dbl)],
+        "hhl_readout": [vp, P(hhl_report), c_int, P(c_dbl), P(c_dbl)],
         "hhl_solve": [P(c_dbl), P(c_dbl), c_int, c_int, P(hhl_options), P(sv_dist), vp, P(c_dbl), P(hhl_report)],
     }
     for name, args in sig.items():
@@ -365,10 +367,27 @@ def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax
     return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
 
 
-def _opts(clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0, diag_kmax=0,
-          qpe_mode=0):
-    return hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap), int(init_fold),
-                       int(tile_jit), int(diag_kmax), int(qpe_mode))
+class _Opts:
+    """hhl_options plus the buffers its eig_* pointers reference (kept alive with it)."""
+
+    def __init__(self, clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0,
+                 diag_kmax=0, qpe_mode=0, eig=None):
+        self.o = hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap),
+                             int(init_fold), int(tile_jit), int(diag_kmax), int(qpe_mode))
+        if eig is not None:          # (lambda, V): caller-supplied eigendecomposition of the padded A
+            self.lam = np.ascontiguousarray(eig[0], dtype=np.float64)
+            self.V = np.ascontiguousarray(eig[1], dtype=np.float64)
+            if self.V.shape != (self.lam.size, self.lam.size):
+                raise SVError(1, "eig: V must be N x N with N = len(lambda)")
+            self.o.eig_lambda = _dp(self.lam)
+            self.o.eig_vectors = _dp(self.V)
+
+    def ref(self):
+        return ctypes.byref(self.o)
+
+
+def _opts(**kw):
+    return _Opts(**kw)
 
 
 def hhl_plan_size(A, b, **kw):
@@ -376,7 +395,7 @@ def hhl_plan_size(A, b, **kw):
     b = np.ascontiguousarray(b, dtype=np.float64)
     o = _opts(**kw)
     nd, nc, nt = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    _check(load().hhl_plan_size(_dp(A), _dp(b), b.size, ctypes.byref(o), ctypes.byref(nd), ctypes.byref(nc),
+    _check(load().hhl_plan_size(_dp(A), _dp(b), b.size, o.ref(), ctypes.byref(nd), ctypes.byref(nc),
                                 ctypes.byref(nt)))
     return nd.value, nc.value, nt.value
 
@@ -389,7 +408,7 @@ def hhl_schedule_dump(A, b, world: int = 1, **kw):
     o = _opts(**kw)
     buf = ctypes.create_string_buffer(1 << 22)
     rep = hhl_report()
-    _check(load().hhl_schedule_dump(_dp(A), _dp(b), b.size, ctypes.byref(o), int(world), buf, len(buf),
+    _check(load().hhl_schedule_dump(_dp(A), _dp(b), b.size, o.ref(), int(world), buf, len(buf),
                                     ctypes.byref(rep)))
     return buf.value.decode(), {f: getattr(rep, f) for f, _ in rep._fields_}
 
@@ -404,18 +423,16 @@ class HHLProgram(Program):
         o = _opts(**kw)
         h = ctypes.c_void_p()
         rep = hhl_report()
-        _check(load().hhl_build_program(state.handle, _dp(A), _dp(b), b.size, ctypes.byref(o), ctypes.byref(h),
+        _check(load().hhl_build_program(state.handle, _dp(A), _dp(b), b.size, o.ref(), ctypes.byref(h),
                                         ctypes.byref(rep)))
         p = cls(state, h, rep.as_dict())
         p._rep = rep
-        p.N = b.size
-        p.b_norm = float(np.linalg.norm(b))
         return p
 
     def readout(self):
-        x = np.empty(self.N)
+        x = np.empty(self._rep.n_orig)
         ps = ctypes.c_double()
-        _check(load().hhl_readout(self.state.handle, ctypes.byref(self._rep), self.N, self.b_norm, _dp(x),
+        _check(load().hhl_readout(self.state.handle, ctypes.byref(self._rep), self._rep.n_orig, _dp(x),
                                   ctypes.byref(ps)))
         return x, ps.value
 
@@ -432,7 +449,7 @@ def hhl_solve(A, b, clock_qubits=0, world=1, rank=0, device=-1, nccl_id=None, st
     if world > 1 or device >= 0:
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         dist = sv_dist(world, rank, device, ctypes.cast(idbuf, ctypes.c_char_p) if idbuf else None)
-    _check(load().hhl_solve(_dp(A), _dp(b), b.size, int(clock_qubits), ctypes.byref(o),
+    _check(load().hhl_solve(_dp(A), _dp(b), b.size, int(clock_qubits), o.ref(),
                             ctypes.byref(dist) if dist else None, stream if stream is not None else _current_stream(),
                             _dp(x), ctypes.byref(rep)))
     return x, rep.as_dict()
