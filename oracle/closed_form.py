@@ -182,3 +182,44 @@ def sampled_amplitudes(p, indices) -> np.ndarray:
         y = yk[a_i[t], kpos[int(k_i[t])]]
         out[t] = np.sum(beta * y * p.V[sys_i[t], :])
     return out
+
+
+def block_amplitudes(p, k_highs, b: int) -> np.ndarray:
+    """psi over whole clock blocks: for each k_high in k_highs, every clock value
+    k = k_high·2^b + k_low (k_low < 2^b), every system index and both ancilla values.
+    Returns psi_blk[a, j, k_low, sys] = psi[sys + 2^n_b·(k_high_j·2^b + k_low) + 2^(n-1)·a].
+
+    Same eq. CF as full_state; the final H^{⊗n_c} row of k is split as
+    (-1)^{k·m} = (-1)^{k_high·m_high} (-1)^{k_low·m_low}: the high bits are contracted with one
+    matrix-vector product per block (O(2^n_c)), the low bits by a 2^b-point Walsh transform.
+    Cost per eigen-component: the two 2^n_c-point transforms of _y_vectors plus one pass per block."""
+    nb, nc = p.n_b, p.n_c
+    Nc = 1 << nc
+    N = 1 << nb
+    if not 0 <= b <= nc:
+        raise ValueError("block bits out of range")
+    nh = nc - b
+    s_tab = recip_table(nc, p.delta, 1, p.snap)
+    beta = p.V.T @ p.b_hat
+    out = np.zeros((2, len(k_highs), 1 << b, N), dtype=np.complex128)
+    # Walsh rows of the high bits: sign[j, m_high] = (-1)^{popcount(k_high_j & m_high)}
+    mh = np.arange(1 << nh, dtype=np.int64)
+    signs = np.empty((len(k_highs), 1 << nh))
+    for j, kh in enumerate(k_highs):
+        x = np.bitwise_and(mh, int(kh))
+        par = np.zeros(mh.size, dtype=np.int64)
+        while np.any(x):
+            par ^= x & 1
+            x >>= 1
+        signs[j] = 1.0 - 2.0 * par
+    for s in range(beta.size):
+        if beta[s] == 0.0:
+            continue
+        ws = _y_vectors(p.phi[s], nc, s_tab)
+        for a in (0, 1):
+            W = ws[a].reshape(1 << nh, 1 << b)          # m = m_low + 2^b m_high
+            U = signs @ W                               # (blocks, 2^b): high bits contracted
+            for j in range(len(k_highs)):
+                y = fwht(U[j]) * np.sqrt(1 << b) / np.sqrt(Nc)   # unnormalised low-bit Walsh, / sqrt(N_c)
+                out[a, j] += beta[s] * np.outer(y, p.V[:, s])
+    return out

@@ -190,3 +190,24 @@ def test_jit_codegen_s30_and_small_tiles(lib):
     gates = synthetic.random_circuit(12, 40, seed=703, kinds=("controlled", "diagonal"), kmax=3)
     txt2, rep2 = pkg.schedule_dump(12, gates, fusion_kmax=2, tile_qubits=8, tile_jit=1)
     assert len(_jit_lines(txt2)) == rep2["n_passes"] >= 1
+
+
+def test_eig_option_host_checks_and_same_kernels():
+    """hhl_options.eig_*: a wrong eigendecomposition is rejected (host-only path, no GPU); the
+    oracle's numpy eigendecomposition gives the SAME schedule and the same NVRTC tile passes as the
+    product's Jacobi eigensolver for the bench workload (so tests/test_bench_program.py's 1e-10 check
+    with eig=oracle runs the bench's kernels)."""
+    from oracle import hhl as ohhl
+    from workloads import configs
+    A, b, nc = configs.get("S30")
+    p = ohhl.plan(A, b, nc)
+    V = p.V.copy()
+    V[:, [0, 1]] = V[:, [1, 0]]
+    with pytest.raises(pkg.SVError):
+        pkg.hhl_schedule_dump(A, b, clock_qubits=nc, eig=(p.lam, V))
+    with pytest.raises(pkg.SVError):
+        pkg.hhl_schedule_dump(A, b, clock_qubits=nc, eig=(p.lam * 1.001, p.V))
+    t1, r1 = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, **configs.BENCH_OPTS)
+    t2, r2 = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, eig=(p.lam, p.V), **configs.BENCH_OPTS)
+    assert t1 == t2 and "JIT_PASS" in t1
+    assert abs(r1["b_norm"] - float(np.linalg.norm(b))) < 1e-12 * r1["b_norm"] and r1["n_orig"] == 13

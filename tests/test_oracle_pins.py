@@ -253,6 +253,19 @@ def test_closed_form_sampled_matches_full():
     assert np.abs(cf.sampled_amplitudes(p, idx) - full[idx]).max() < 1e-13
 
 
+def test_closed_form_block_amplitudes_match_full():
+    """block_amplitudes (high clock bits contracted by a matrix-vector product, low bits by a
+    Walsh transform) = full_state on whole clock blocks, incl. block 0 (the post-selected slice)."""
+    for name, b in (("C3", 8), ("C3", 0), ("C2", 6), ("C3p", 3)):
+        A, bb, nc = configs.get(name)
+        p = hhl.plan(A, bb, nc)
+        full = cf.full_state(p).reshape(2, 1 << p.n_c, 1 << p.n_b)
+        khs = [0, (1 << (p.n_c - b)) - 1, (1 << (p.n_c - b)) // 3]
+        blk = cf.block_amplitudes(p, khs, b)
+        for j, kh in enumerate(khs):
+            assert np.abs(blk[:, j] - full[:, kh << b:(kh + 1) << b]).max() < 1e-13
+
+
 def test_recip_table_matches_c_definition():
     """numpy s_m (closed_form) = C s_m (sv_oracle.c) incl. sign half, clipping and snapping."""
     for nc, delta, snap in [(3, 0.25, 0.0), (6, 1 / 32, 1e-5), (10, 1 / 128, 1e-5), (12, 0.3, 0.01)]:

@@ -75,6 +75,23 @@ def test_multi_level_consistent_with_block_cdf():
     assert ((lo - 1e-12 <= t) & (t < cdf[s] + 1e-12)).all()
 
 
+@pytest.mark.parametrize("n", [12, 21, 22])
+def test_multi_level_equals_plain_inverse_cdf_dyadic(n):
+    """Several blocks / superblocks (n > 10): on a state whose probabilities are dyadic with few
+    significant bits (a_i = d_i 2^-8, d_i in -3..3) every partial sum is exact in fp64 whatever the
+    summation order, so the multi-level procedure must equal textbook inverse-CDF sampling index for
+    index (ties cannot be broken differently: all CDF values are exact)."""
+    g = synthetic.rng(1000 + n)
+    d = g.integers(-3, 4, size=(1 << n, 2)).astype(np.float64)
+    d[g.random(1 << n) < 0.3] = 0.0                      # zero runs: empty blocks/elements are skipped
+    psi = (d[:, 0] + 1j * d[:, 1]) * 2.0 ** -8
+    shots = 3000
+    p = psi.real * psi.real + psi.imag * psi.imag
+    cdf = np.cumsum(p)
+    plain = np.searchsorted(cdf, osample.uniforms(11, shots) * cdf[-1], side="right")
+    assert (osample.sample(psi, shots, seed=11) == plain).all()
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,shots", [(3, 1000), (12, 5000), (22, 2000)])
 def test_gpu_sample_matches_oracle(n, shots):
