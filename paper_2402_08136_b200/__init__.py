@@ -5,7 +5,7 @@ sm_100a; `sv` is its thin ctypes binding with the same names. Nothing here impor
 the test oracle (oracle/), and there is no CPU fallback.
 """
 from .sv import (EXPORTS, HHLProgram, Program, State, SVError, hhl_plan_size,  # noqa: F401
-                 hhl_schedule_dump, hhl_solve, load, nccl_unique_id, schedule_dump)
+                 hhl_schedule_dump, hhl_solve, load, nccl_unique_id, schedule_dump, trim_memory)
 
 __all__ = ["State", "Program", "HHLProgram", "SVError", "hhl_solve", "hhl_plan_size", "hhl_schedule_dump", "load", "nccl_unique_id",
-           "EXPORTS"]
+           "trim_memory", "EXPORTS"]

@@ -95,6 +95,18 @@ sv_status sv_destroy(sv_state *sv) {
     return guard([&] { state_destroy(sv); });
 }
 
+sv_status sv_trim_memory(int device) {
+    return guard([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+            cudaGetLastError();
+            fail(SV_E_CUDA, "no CUDA device: this library has no CPU fallback");
+        }
+        cuda_check(cudaDeviceSynchronize(), "sync before trim");
+        pool_trim(device, 0);
+    });
+}
+
 sv_status sv_reset(sv_state *sv) {
     return guard([&] {
         if (!sv) fail(SV_E_ARG, "null state");
@@ -472,11 +484,31 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         std::vector<ProductFactor> factors;
         size_t n_logical = 0;
         std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
-        std::vector<int> phys(p.n);
-        for (int q = 0; q < p.n; q++) phys[q] = q;
-        const CompileOptions hco = hhl_compile_opts(opt, &p, world);
-        if (!hco.phys_init.empty()) phys = hco.phys_init;
-        Schedule s = compile(fused, nullptr, p.n, p.n - g, phys, hco);
+        // rank 0's program exactly as hhl_build_program creates it, on a host-only stand-in state
+        // (no device memory): same schedule, same lowering, same generated tile passes
+        sv_state host{};
+        host.n = p.n;
+        host.g = g;
+        host.nloc = p.n - g;
+        host.world = world;
+        host.rank = 0;
+        host.phys.resize(p.n);
+        for (int q = 0; q < p.n; q++) host.phys[q] = q;
+        CompileOptions hco = hhl_compile_opts(opt, &p, world);
+        std::string jitlog;
+        hco.dry_run = opt && opt->tile_jit > 0;
+        hco.dry_log = &jitlog;
+        Schedule s;
+        if (hco.dry_run) {
+            std::unique_ptr<sv_program> prog(program_create(&host, fused, factors.empty() ? nullptr : &factors, hco,
+                                                            n_logical));
+            s = prog->sched;
+        } else {
+            std::vector<int> phys(p.n);
+            for (int q = 0; q < p.n; q++) phys[q] = q;
+            if (!hco.phys_init.empty()) phys = hco.phys_init;
+            s = compile(fused, factors.empty() ? nullptr : &factors, p.n, p.n - g, phys, hco);
+        }
         if (rep) {
             report_plan(rep, p);
             rep->n_logical = n_logical;
@@ -486,8 +518,7 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
             rep->pass_bytes = s.pass_bytes;
         }
         if (buf && buf_len) {
-            std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s);
-            if (opt && opt->tile_jit > 0) t += jit_check_schedule(s);
+            std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s) + jitlog;
             size_t n = std::min(buf_len - 1, t.size());
             std::memcpy(buf, t.data(), n);
             buf[n] = 0;

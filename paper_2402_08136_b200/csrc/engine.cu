@@ -24,13 +24,22 @@ static void nccl_check(int rc, const char *what) {
 // State buffers come from a stream-ordered memory pool OWNED BY THE LIBRARY (one per device, never
 // the process-wide default pool, so other allocators in the process -- e.g. torch -- are not
 // starved) with an unbounded release threshold: freeing a 16 GiB state and creating the next one
-// (hhl_solve called repeatedly) reuses the pool instead of unmapping/remapping pages. When the last
-// live state of the process is destroyed the pool is trimmed to zero.
+// (hhl_solve called repeatedly) reuses the pool instead of unmapping/remapping pages (measured on the
+// B200: trimming after every solve makes the next 16 GiB allocation cost ~4.7 s). When the last live
+// state is destroyed the pool keeps at most one state's worth (the largest state allocated) for the
+// next solve; sv_trim_memory() releases everything, and state_create trims before reporting OOM.
 namespace {
 std::mutex g_pool_mu;
 cudaMemPool_t g_pools[64] = {};
 int g_live_states = 0;
+size_t g_keep_bytes[64] = {};       // largest single state allocation per device
 }  // namespace
+
+void pool_trim(int device, size_t keep) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (int d = 0; d < 64; d++)
+        if (g_pools[d] && (device < 0 || d == device)) cudaMemPoolTrimTo(g_pools[d], keep);
+}
 
 static cudaMemPool_t lib_pool(int device) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -111,7 +120,17 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
     size_t freeb = 0, totb = 0;
     cuda_check(cudaMemGetInfo(&freeb, &totb), "cudaMemGetInfo");
     freeb += pool_slack(device);     // reserved by the library pool but free for reuse
-    if (bytes * (virt ? world : 1) > freeb) fail(SV_E_OOM, "state does not fit in device memory");
+    if (bytes * (virt ? world : 1) > freeb) {   // release cached pool memory, then decide
+        cuda_check(cudaDeviceSynchronize(), "sync before trim");
+        pool_trim(device, 0);
+        cuda_check(cudaMemGetInfo(&freeb, &totb), "cudaMemGetInfo");
+        freeb += pool_slack(device);
+        if (bytes * (virt ? world : 1) > freeb) fail(SV_E_OOM, "state does not fit in device memory");
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (device < 64) g_keep_bytes[device] = std::max(g_keep_bytes[device], bytes * (virt ? world : 1));
+    }
     if (virt) {
         sv->vworld = world;
         sv->world = 1;
@@ -170,9 +189,10 @@ static void destroy_impl(sv_state *sv, bool top) {
     delete sv;
     if (!top) return;
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    if (--g_live_states <= 0) {      // last live state: hand the pool's memory back to the device
+    if (--g_live_states <= 0) {      // last live state: keep one state's worth for the next one
         g_live_states = 0;
-        if (device >= 0 && device < 64 && g_pools[device]) cudaMemPoolTrimTo(g_pools[device], 0);
+        if (device >= 0 && device < 64 && g_pools[device])
+            cudaMemPoolTrimTo(g_pools[device], g_keep_bytes[device] + (64ull << 20));
     }
 }
 
@@ -684,6 +704,42 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         p->sched.pass_bytes -= steps[0].bytes;                       // no separate init pass
         p->sched.pass_bytes -= 16.0 * (double)sv->local_amps();       // and the first pass reads nothing
     }
+    // Known-zero ("lazy") qubits, JIT tile programs that start with a product init:
+    // a qubit no init factor covers is |0> -- every amplitude with its bit set is 0 -- until the first
+    // op that acts on it non-diagonally. If that op runs in a JIT tile pass of this program and every
+    // step before it is a JIT tile pass (or the fused init), the passes before it skip the bit's
+    // zero half (tiles never read or written), and the activating pass reads only the bit's zero
+    // half. Exact: those amplitudes are 0 by construction (HHL: the ancilla before RECIP_RY halves
+    // the first passes' traffic and FP64 work).
+    std::vector<uint64_t> zin(steps.size(), 0), zout(steps.size(), 0);
+    if (use_jit && fuse_init) {
+        uint64_t covered = 0;
+        for (auto &f : steps[0].factors)
+            if (!f.diag)
+                for (int q : f.qubits) covered |= 1ull << q;
+        const uint64_t loc = nloc >= 64 ? ~0ull : ((1ull << nloc) - 1ull);
+        uint64_t zero = loc & ~covered, eligible = zero, seen_other = 0;
+        for (size_t si = 1; si < steps.size(); si++) {
+            const Step &st = steps[si];
+            zin[si] = zero;
+            if (st.kind != StepKind::Tile) {          // non-tile step: no bit still zero here may be skipped
+                eligible &= ~zero;
+                seen_other = 1;
+            }
+            for (const Gate &g : st.tile_ops)
+                if (g.kind == Kind::Dense || g.kind == Kind::Controlled || g.kind == Kind::RecipRY)
+                    for (int q : g.targets)
+                        if (q < 64) zero &= ~(1ull << q);
+            if (st.kind == StepKind::Exchange) zero = 0;
+            zout[si] = zero;
+        }
+        (void)seen_other;
+        eligible &= ~zero;                            // never activated in this program: not skipped
+        for (size_t si = 0; si < steps.size(); si++) {
+            zin[si] &= eligible;
+            zout[si] &= eligible;
+        }
+    }
     for (size_t si = 0; si < steps.size(); si++) {
         const Step &st = steps[si];
         LaunchRec rec;
@@ -697,7 +753,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 if (fuse_init) {
                     rec.skip = true;
                     rec.bytes = 0.0;
-                } else {
+                } else if (!co.dry_run) {
                     build_product(sv, p.get(), st, rec, bscale);
                 }
                 break;
@@ -796,12 +852,33 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 a.psi = sv->psi;
                 a.T = (int)st.tile_bits.size();
                 for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
-                a.n_tiles = 1ull << (nloc - a.T);
+                a.nskip = 0;
+                a.zload = a.zstore = 0;
+                uint64_t tmask = 0;
+                for (int i = 0; i < a.T; i++) tmask |= 1ull << a.tbits[i];
+                for (int b = 0; b < nloc && b < 64; b++) {
+                    const uint64_t m = 1ull << b;
+                    if ((zin[si] & zout[si] & m) && !(tmask & m) && a.nskip < 8) a.skip[a.nskip++] = b;
+                }
+                for (int i = 0; i < a.T; i++) {
+                    if (zin[si] >> a.tbits[i] & 1) a.zload |= 1u << i;
+                    if (zout[si] >> a.tbits[i] & 1) a.zstore |= 1u << i;
+                }
+                a.n_tiles = 1ull << (nloc - a.T - a.nskip);
+                {   // HBM bytes: tiles processed x (slots read + slots written)
+                    const double tiles = std::ldexp(1.0, -a.nskip);
+                    const double rd = (fuse_init && si == 1) ? 0.0 : std::ldexp(1.0, -__builtin_popcount(a.zload));
+                    const double wr = std::ldexp(1.0, -__builtin_popcount(a.zstore));
+                    const double before = rec.bytes;      // as already counted in sched.pass_bytes
+                    rec.bytes = 16.0 * (double)sv->local_amps() * tiles * (rd + wr);
+                    p->sched.pass_bytes += rec.bytes - before;
+                }
                 a.rank_base = rank_base;
                 size_t ph0 = 0, opbase = 0;
                 lower_tile_step(st, a, blob, rops, phases, ph0, opbase, use_jit, pending_scale);
                 pending_scale = 1.0;
-                for (size_t oi = opbase; oi < rops.size(); oi++) rec.flops += regop_flops(rops[oi]) * sv->local_amps();
+                for (size_t oi = opbase; oi < rops.size(); oi++)
+                    rec.flops += regop_flops(rops[oi]) * std::ldexp((double)sv->local_amps(), -a.nskip);
                 if (use_jit) {
                     std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
@@ -820,6 +897,27 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             }
         }
         p->recs.push_back(rec);
+    }
+    if (co.dry_run) {       // host-only planning: compile the generated passes, log every launch
+        std::string &L = *co.dry_log;
+        char line[512];
+        for (const LaunchRec &r : p->recs) {
+            if (r.kind == StepKind::Tile && r.jit >= 0) {
+                std::string err;
+                auto cubin = jit_compile_only(p->jit[r.jit].src, err);
+                if (cubin.empty()) fail(SV_E_CUDA, err);
+                snprintf(line, sizeof line,
+                         "JIT_PASS T=%d n_tiles=%llu skip=%d zload=%u zstore=%u bytes=%.0f flops=%.4g smem=%zu "
+                         "src=%s cubin_bytes=%zu\n",
+                         r.tile.T, (unsigned long long)r.tile.n_tiles, r.tile.nskip, r.tile.zload, r.tile.zstore,
+                         r.bytes, r.flops, p->jit[r.jit].smem_extra, jit_source_tag(p->jit[r.jit].src).c_str(),
+                         cubin.size());
+            } else {
+                snprintf(line, sizeof line, "LAUNCH kind=%d skip=%d bytes=%.0f\n", (int)r.kind, (int)r.skip, r.bytes);
+            }
+            L += line;
+        }
+        return p.release();
     }
     // upload blob and tile ops, then rebase pointers
     if (!blob.empty()) {

@@ -75,6 +75,8 @@ namespace hhlsv {
 void cuda_check(cudaError_t e, const char *what);
 sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zero_init = true);
 void state_destroy(sv_state *sv);
+// Release device memory the library's pool caches for reuse (device < 0: every device), keeping `keep` bytes.
+void pool_trim(int device, size_t keep);
 void state_reset(sv_state *sv);
 sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std::vector<ProductFactor> *init,
                            const CompileOptions &co, uint64_t n_logical);

@@ -364,7 +364,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
     // compute phases (default; measured faster than double buffering at half the occupancy),
     // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
-    int nbuf = cfg.nbuf == 2 ? 2 : 1;
+    int nbuf = (cfg.nbuf == 2 && !a.zload) ? 2 : 1;
     if (init) nbuf = 1;
     const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
                             dsub_max * 16;
@@ -431,9 +431,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     }
     if (dsub_max)
         k << "  const SArr dsub{depB.b + " << (8 << SB) << "u + " << wtot * 16 << "u};\n";
-    k << "  auto tile_base = [](u64 t) { u64 b = t;";
-    for (int i = 0; i < T; i++) k << " b = insz(b, " << a.tbits[i] << ");";
-    k << " return b; };\n";
+    {   // tile index -> base: zeros inserted at the tile bits and at the skipped known-zero bits
+        std::vector<int> ins(a.tbits, a.tbits + T);
+        for (int i = 0; i < a.nskip; i++) ins.push_back(a.skip[i]);
+        std::sort(ins.begin(), ins.end());
+        k << "  auto tile_base = [](u64 t) { u64 b = t;";
+        for (int b : ins) k << " b = insz(b, " << b << ");";
+        k << " return b; };\n";
+    }
     k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
       << "]; };\n";
     k << "  bar();\n";
@@ -549,7 +554,11 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "      }\n      cur[swz(u)] = amp;\n    }\n    bar();\n";
         } else {
-            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]);\n";
+            if (a.zload)      // known-zero slots are not read
+                k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") { if (u & " << a.zload
+                  << "u) cur[swz(u)] = mk(0.0, 0.0); else cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]); }\n";
+            else
+                k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") cp_async16s(cur.at(swz(u)), &psi[addr(base, u)]);\n";
             k << "    cp_async_commit();\n    cp_async_wait0();\n    bar();\n";
         }
     }
@@ -596,7 +605,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
         } else if (p == 0 && din) {
             k << "      const double2 *gin = psi + (base | pd_in);\n";
-            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
+            for (int j = 0; j < 16; j++) {
+                // known-zero slots (zload) are not read: register part decided at codegen, thread part per thread
+                if ((uint32_t)rd[j] & a.zload) k << "      double2 v" << j << " = mk(0.0, 0.0);\n";
+                else if (a.zload)
+                    k << "      double2 v" << j << " = (tb & " << a.zload << "u) ? mk(0.0, 0.0) : ldcs_v(gin + "
+                      << u64s(phys_slot(P, j)) << ");\n";
+                else k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
+            }
         } else {
             for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = " << sref(rd[j]) << ";\n";
         }
@@ -993,7 +1009,11 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
-            for (int j = 0; j < 16; j++) k << "      __stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+            for (int j = 0; j < 16; j++) {
+                if ((uint32_t)rd[j] & a.zstore) continue;          // still known zero: not written
+                k << "      " << (a.zstore ? "if (!(tb & " + std::to_string(a.zstore) + "u)) " : std::string())
+                  << "__stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+            }
             hoisted();
             k << "    }\n";
         } else {
@@ -1003,7 +1023,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      bar();\n    }\n";
         }
     }
-    if (!dout) k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+    if (!dout) {
+        if (a.zstore)
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") if (!(u & " << a.zstore
+              << "u)) psi[addr(base, u)] = cur[swz(u)];\n";
+        else
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+    }
     // one barrier per tile: the next tile's first shared-memory write (cp.async, phase-0 stores,
     // diagonal sub-tables) must not overtake a slower warp still reading this tile's last phase
     k << "    bar();\n  }\n  cp_async_wait0();\n}\n";

@@ -102,6 +102,14 @@ struct TileArgs {
     const RegOp *ops;            // device, this step's ops (phase op0/op1 index into it)
     const double2 *blob;         // program data blob
     uint64_t rank_base;
+    // Lazy zero qubits (JIT passes only, DESIGN.md §6 "Known-zero qubits"): physical bits whose
+    // amplitudes are known to be 0 when the bit is 1 (e.g. the HHL ancilla before the reciprocal
+    // rotation). Out-of-tile such bits that stay zero through the pass are skipped: tiles with the
+    // bit set are neither read nor written (n_tiles excludes them). Tile positions in zload are 0
+    // on input (not read); tile positions in zstore are still 0 on output (not written).
+    int nskip;
+    int skip[8];
+    uint32_t zload, zstore;
 };
 
 // ---- launchers (stream-ordered, no sync) ----

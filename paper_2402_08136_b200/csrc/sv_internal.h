@@ -146,6 +146,11 @@ struct CompileOptions {
                                // one table of <= this many qubits after scheduling (0 = off)
     std::vector<int> phys_init;  // programs that start with their own initialisation: logical->physical
                                  // map at program start (empty = identity)
+    // host-only planning (hhl_schedule_dump / sv_schedule_dump with tile_jit > 0): program_create
+    // lowers and generates every tile pass exactly as for a run, compiles them with NVRTC (no
+    // device, no uploads, no launches) and appends one line per launch to *dry_log
+    bool dry_run = false;
+    std::string *dry_log = nullptr;
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.

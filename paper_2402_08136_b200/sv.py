@@ -72,7 +72,8 @@ class hhl_report(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_destroy", "sv_reset", "sv_info",
+EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_destroy", "sv_trim_memory",
+           "sv_reset", "sv_info",
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
            "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
@@ -96,7 +97,7 @@ def load(path: str = LIB_PATH):
     sig = {
         "sv_nccl_unique_id": [ctypes.c_char_p],
         "sv_create": [c_int, P(sv_dist), vp, P(vp)],
-        "sv_destroy": [vp], "sv_reset": [vp],
+        "sv_destroy": [vp], "sv_reset": [vp], "sv_trim_memory": [c_int],
         "sv_info": [vp, P(c_int), P(c_u64), P(vp)],
         "sv_qubit_map": [vp, P(c_int)],
         "sv_sync": [vp],
@@ -185,6 +186,11 @@ class _GateArray:
 
 def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0, tile_jit=0):
     return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits), int(tile_jit))
+
+
+def trim_memory(device: int = -1):
+    """sv_trim_memory: release the device memory the library's pool caches for reuse."""
+    _check(load().sv_trim_memory(int(device)))
 
 
 def nccl_unique_id() -> bytes:
