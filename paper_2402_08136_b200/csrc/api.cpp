@@ -379,36 +379,30 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     return fuse(rest, fo);
 }
 
-// Optional initial physical layout of a single-rank eigenbasis HHL program: the three lowest
-// clock qubits take the three lowest physical bits -- every tile holds those (128-byte segments) and
-// their QFT/IQFT gates all fall in the middle pass anyway -- and the system register follows at
-// physical 3..3+n_b-1, so the final 4-qubit V runs in a last phase whose thread bits start with the
-// coalesced low bits (direct register->HBM stores instead of a shared-memory round trip).
-static std::vector<int> hhl_layout(const HHLPlanHost &p, const hhl_options *opt, int world) {
-    // Measured on S30: mode 1 makes the V pass 11.7 -> 8.1 ms but the greedy packer then
-    // loads the middle pass with 79 ops (12.2 -> 17.4 ms): net slower, so the default stays identity.
-    const int mode = 0;
-    if (mode == 0 || world != 1 || !opt || opt->qpe_mode != 1 || opt->tile_qubits < 0 || p.n_c < 4) return {};
+// Initial physical layout of a SHARDED eigenbasis HHL program, g global
+// qubits: the top g SYSTEM qubits take the global bits and [system rest | clock | ancilla] the local
+// ones. In the eigenbasis circuit the system register is touched non-diagonally only by V^T (folded
+// into the product init, which is rank-resolved) and by the final V, so every Hadamard of the
+// (I)QFT / H layers, the reciprocal rotation and all diagonal phase tables (rank-resolved table
+// slices) run without communication; the final V needs ONE exchange round, whose victims (clock /
+// ancilla qubits whose last use is past, chosen by the scheduler) never return. Single rank, the
+// textbook circuit or g > n_b: identity (the top logical qubits -- ancilla, clock MSBs -- global).
+static std::vector<int> hhl_layout(const HHLPlanHost &p, const hhl_options *opt, int g) {
+    if (g < 1 || !opt || opt->qpe_mode != 1 || g > p.n_b) return {};
     std::vector<int> phys(p.n, -1);
-    std::vector<int> low;                                          // logical qubits at physical 0..2
-    if (mode == 2)
-        for (int j = p.n_c - 3; j < p.n_c; j++) low.push_back(p.n_b + j);   // top clock qubits
-    else
-        for (int j = 0; j < 3; j++) low.push_back(p.n_b + j);               // bottom clock qubits
     int next = 0;
-    for (int q : low) phys[q] = next++;
-    for (int s = 0; s < p.n_b; s++) phys[s] = next++;              // system
-    for (int j = 0; j < p.n_c; j++)
-        if (phys[p.n_b + j] < 0) phys[p.n_b + j] = next++;        // remaining clock qubits
+    for (int s = 0; s < p.n_b - g; s++) phys[s] = next++;          // local system qubits
+    for (int j = 0; j < p.n_c; j++) phys[p.n_b + j] = next++;       // clock register
     phys[p.n - 1] = next++;                                        // ancilla
+    for (int s = p.n_b - g; s < p.n_b; s++) phys[s] = next++;      // global: top system qubits
     return phys;
 }
 
-static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost *p = nullptr, int world = 1) {
+static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost *p = nullptr, int g = 0) {
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
     if (opt) co.jit = opt->tile_jit;
-    if (p) co.phys_init = hhl_layout(*p, opt, world);
+    if (p) co.phys_init = hhl_layout(*p, opt, g);
     return co;
 }
 
@@ -423,7 +417,7 @@ static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int
     size_t n_logical = 0;
     std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
     prof_mark("fold + fuse");
-    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt, &p, sv->nloc == sv->n ? 1 : 2),
+    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt, &p, sv->n - sv->nloc),
                                       n_logical);
     prof_mark("program_create");
     if (rep) {
@@ -494,7 +488,7 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         host.rank = 0;
         host.phys.resize(p.n);
         for (int q = 0; q < p.n; q++) host.phys[q] = q;
-        CompileOptions hco = hhl_compile_opts(opt, &p, world);
+        CompileOptions hco = hhl_compile_opts(opt, &p, g);
         std::string jitlog;
         hco.dry_run = opt && opt->tile_jit > 0;
         hco.dry_log = &jitlog;

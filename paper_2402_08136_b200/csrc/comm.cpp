@@ -3,9 +3,11 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "nccl.h"
 
@@ -23,6 +25,8 @@ struct NcclApi {
     decltype(&ncclGroupEnd) groupEnd = nullptr;
     decltype(&ncclAllReduce) allReduce = nullptr;
     decltype(&ncclGetErrorString) errStr = nullptr;
+    decltype(&ncclCommGetAsyncError) asyncError = nullptr;
+    decltype(&ncclCommAbort) commAbort = nullptr;
     std::string why;
     bool ok = false;
 };
@@ -57,6 +61,8 @@ NcclApi &api() {
         LOAD(groupEnd, ncclGroupEnd)
         LOAD(allReduce, ncclAllReduce)
         LOAD(errStr, ncclGetErrorString)
+        LOAD(asyncError, ncclCommGetAsyncError)
+        LOAD(commAbort, ncclCommAbort)
 #undef LOAD
         a.ok = true;
     });
@@ -120,6 +126,51 @@ int nccl_sendrecv(Comm &c, const double *sendbuf, double *recvbuf, size_t count,
     int rc2 = check(a.recv(recvbuf, count, ncclDouble, peer, (ncclComm_t)c.comm, s));
     int rc3 = check(a.groupEnd());
     return rc ? rc : (rc2 ? rc2 : rc3);
+}
+
+int nccl_alltoall_pairs(Comm &c, const double *const *sendbufs, double *const *recvbufs, const int *peers, int npeers,
+                        size_t count, cudaStream_t s) {
+    NcclApi &a = api();
+    int rc = check(a.groupStart());
+    if (rc) return rc;
+    for (int i = 0; i < npeers && !rc; i++) {
+        rc = check(a.send(sendbufs[i], count, ncclDouble, peers[i], (ncclComm_t)c.comm, s));
+        if (!rc) rc = check(a.recv(recvbufs[i], count, ncclDouble, peers[i], (ncclComm_t)c.comm, s));
+    }
+    const int rc2 = check(a.groupEnd());
+    return rc ? rc : rc2;
+}
+
+int nccl_wait(Comm &c, cudaStream_t s, double timeout_s) {
+    // Poll the stream and the communicator's asynchronous error state; abort the communicator when
+    // NCCL reports an error or the collective does not finish in time (a lost peer would otherwise
+    // hang the caller forever). SURVEY §5 failure detection.
+    NcclApi &a = api();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return 0;
+        if (q != cudaErrorNotReady) {
+            g_err = std::string("CUDA error while waiting for NCCL: ") + cudaGetErrorString(q);
+            return -1;
+        }
+        ncclResult_t ae = ncclSuccess;
+        if (c.comm && a.asyncError((ncclComm_t)c.comm, &ae) == ncclSuccess && ae != ncclSuccess &&
+            ae != ncclInProgress) {
+            g_err = std::string("NCCL asynchronous error: ") + a.errStr(ae);
+            a.commAbort((ncclComm_t)c.comm);
+            c.comm = nullptr;
+            return (int)ae;
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > timeout_s) {
+            g_err = "NCCL operation timed out after " + std::to_string(timeout_s) + " s (peer lost?)";
+            if (c.comm) a.commAbort((ncclComm_t)c.comm);
+            c.comm = nullptr;
+            return -2;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
 }
 
 int nccl_allreduce_sum(Comm &c, double *buf, size_t count, cudaStream_t s) {

@@ -62,8 +62,12 @@ static void roles(const Gate &g, std::vector<int> &nd, std::vector<int> &dg) {
 // targets still fit, so e.g. the final Hadamard layer is absorbed into the QFT passes instead
 // of needing passes of its own. Returns a topological order of `ops` (the state is unchanged
 // up to rounding: only commuting ops are exchanged).
+// Multi-rank (nloc < n): an op whose non-diagonal target sits on a global bit needs an exchange.
+// Such ops are deferred while any other op is ready, so every op that commutes with them runs
+// first (e.g. the final Hadamard layer on the clock register before the system register's V, which
+// then needs ONE exchange round whose victims -- qubits with no further use -- never come back).
 static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const std::vector<int> &phys, int T,
-                                           int wmin, int R) {
+                                           int wmin, int R, int nloc) {
     const size_t m = ops.size();
     std::vector<std::vector<size_t>> succ(m);
     std::vector<int> indeg(m, 0);
@@ -111,6 +115,11 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
         for (int b : v) high += b >= wmin;
         return (int)v.size() <= T && high <= T - wmin;
     };
+    std::vector<char> needs_global(m, 0);
+    for (size_t i = 0; i < m; i++)
+        for (int b : pnd(ops[i]))
+            if (b >= nloc) needs_global[i] = 1;
+    bool exchanged = false;        // after the first global op the layout changes: stop deferring
     std::vector<Gate> out;
     out.reserve(m);
     std::vector<char> done(m, 0);
@@ -125,8 +134,23 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
             if (--indeg[b] == 0) ready.insert(b);
     };
     while (!ready.empty()) {
+        if (!exchanged) {
+            bool other = false;
+            for (size_t i : ready) other |= !needs_global[i];
+            if (!other) {              // only exchange-needing ops are ready: take one, stop deferring
+                exchanged = true;
+                take(*ready.begin());
+                continue;
+            }
+        }
         // a swap or an op too wide for a tile is scheduled alone, in original order
         size_t first = *ready.begin();
+        if (!exchanged)
+            for (size_t i : ready)
+                if (!needs_global[i]) {
+                    first = i;
+                    break;
+                }
         const Gate &g0 = ops[first];
         if (g0.kind == Kind::Swap ||
             ((g0.kind == Kind::Dense || g0.kind == Kind::Controlled) && (int)g0.targets.size() > R)) {
@@ -145,6 +169,7 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
                 if (g.kind == Kind::Swap ||
                     ((g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R))
                     continue;
+                if (!exchanged && needs_global[i]) continue;
                 std::vector<int> u = cur;
                 int nnew = 0;
                 for (int b : pnd(g))
@@ -297,8 +322,8 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     const int R = o.reg_bits;
     // single-rank tile schedules: commutation-aware reordering for packing (multi-rank keeps the
     // input order so exchanges follow the circuit)
-    const bool reorder = tiles && o.reorder && nloc == n;
-    const std::vector<Gate> ops = reorder ? reorder_for_tiles(ops_in, phys_in, T, wmin, R) : ops_in;
+    const bool reorder = tiles && o.reorder;
+    const std::vector<Gate> ops = reorder ? reorder_for_tiles(ops_in, phys_in, T, wmin, R, nloc) : ops_in;
 
     // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.
     std::vector<std::vector<size_t>> uses(n);
@@ -361,32 +386,40 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
         }
         s.n_fused++;
         s.alg_bytes += alg_bytes(g, n);
-        // ---- bring non-diagonal targets local (multi-GPU)
+        // ---- bring non-diagonal targets local (multi-GPU): ONE exchange round for all of them
         std::vector<int> nd = nd_targets(g);
-        for (int q : nd) {
-            if (phys[q] < nloc) continue;
+        std::vector<int> need;
+        for (int q : nd)
+            if (phys[q] >= nloc) need.push_back(q);
+        if (!need.empty()) {
             close_tile();
-            // victim: local logical qubit, not a target of g, farthest next nd use
-            int victim = -1;
-            size_t best = 0;
-            for (int l = 0; l < n; l++) {
-                if (phys[l] >= nloc) continue;
-                if (std::find(nd.begin(), nd.end(), l) != nd.end()) continue;
-                size_t nu = next_use(l, i);
-                // prefer high physical bits on ties (contiguous halves)
-                if (victim < 0 || nu > best || (nu == best && phys[l] > phys[victim])) {
-                    victim = l;
-                    best = nu;
-                }
-            }
-            if (victim < 0) fail(SV_E_ARG, "no local qubit available for a global swap");
             Step ex;
             ex.kind = StepKind::Exchange;
-            ex.gbit = phys[q];
-            ex.lbit = phys[victim];
-            ex.bytes = 2.0 * 16.0 * local_amps / 2.0;     // half the shard out and in (NVLink)
+            std::vector<int> taken;
+            for (int q : need) {
+                // victim: local logical qubit, not a target of g, farthest next nd use (Belady); on
+                // ties the highest physical bit (the top local bits make every slot contiguous)
+                int victim = -1;
+                size_t best = 0;
+                for (int l = 0; l < n; l++) {
+                    if (phys[l] >= nloc) continue;
+                    if (std::find(nd.begin(), nd.end(), l) != nd.end()) continue;
+                    if (std::find(taken.begin(), taken.end(), l) != taken.end()) continue;
+                    size_t nu = next_use(l, i);
+                    if (victim < 0 || nu > best || (nu == best && phys[l] > phys[victim])) {
+                        victim = l;
+                        best = nu;
+                    }
+                }
+                if (victim < 0) fail(SV_E_ARG, "no local qubit available for a global swap");
+                taken.push_back(victim);
+                ex.xg.push_back(phys[q]);
+                ex.xl.push_back(phys[victim]);
+            }
+            // (1 - 2^-k) of the shard out and in over NVLink
+            ex.bytes = 2.0 * 16.0 * local_amps * (1.0 - std::ldexp(1.0, -(int)need.size()));
+            for (size_t j = 0; j < need.size(); j++) std::swap(phys[need[j]], phys[taken[j]]);
             s.steps.push_back(ex);
-            std::swap(phys[q], phys[victim]);
         }
         Gate pg = to_physical(g, phys);
         const bool too_wide = (g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R;
@@ -484,7 +517,7 @@ std::string dump_schedule(const Schedule &s) {
                 break;
             case StepKind::Diagonal: os << "DIAGONAL q=" << bits(st.dbits) << "\n"; break;
             case StepKind::RecipRY: os << "RECIP_RY anc=" << st.anc << " clock=" << bits(st.clock_bits) << "\n"; break;
-            case StepKind::Exchange: os << "EXCHANGE global=" << st.gbit << " local=" << st.lbit << "\n"; break;
+            case StepKind::Exchange: os << "EXCHANGE global=" << bits(st.xg) << " local=" << bits(st.xl) << "\n"; break;
             case StepKind::Tile: {
                 os << "TILE bits=" << bits(st.tile_bits) << " ops=" << st.tile_ops.size() << " phases="
                    << st.phase_R.size() << "\n";

@@ -223,70 +223,125 @@ static void ensure_red(sv_state *sv, size_t n) {
 }
 
 // --------------------------------------------------------------- exchange ----
-// Swap physical global bit gbit with local bit lbit: send the half of the shard whose
-// lbit differs from this rank's gbit value to the partner rank, receive its half into
-// the same positions. Chunked: no half-state receive buffer.
-static void exchange(sv_state *sv, int gbit, int lbit) {
-    const int gb = gbit - sv->nloc;
-    const int partner = sv->rank ^ (1 << gb);
-    const int beta = (sv->rank >> gb) & 1;
-    const int val = 1 - beta;
-    const uint64_t half = sv->local_amps() >> 1;
-    const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);   // 1 GiB
-    if (sv->x_len < chunk) {
-        pool_free(sv->d_xsend, sv->stream);
-        pool_free(sv->d_xrecv, sv->stream);
-        sv->d_xsend = sv->d_xrecv = nullptr;
-        cuda_check(pool_malloc((void **)&sv->d_xsend, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xsend)");
-        cuda_check(pool_malloc((void **)&sv->d_xrecv, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xrecv)");
-        sv->x_len = chunk;
+// Multi-qubit exchange: swap the values of physical global bits G[i] with local bits
+// L[i]. With the pairs ordered by ascending L, bit i of a slot pattern p <-> L[i]. Rank r holds, in
+// slot p (its elements whose L bits equal p), amplitudes that belong to rank peer(r, p) = r with its
+// G bits set to p; they land there in slot own(r) = r's G pattern. So rank r sends slot p to
+// peer(r, p) and receives slot p from the same peer: an all-to-all among the 2^k ranks that share r's
+// other global bits, (1 - 2^-k) of the shard each way (k = 1: the pairwise half-swap). Chunked
+// (<= 2^24 amplitudes per slot per round); when L are the top k local bits every slot is contiguous
+// and is sent straight from the state (no pack kernel).
+struct XPlan {
+    int k = 0;
+    std::vector<int> Ls, Gs;
+    uint32_t own = 0;
+    uint64_t slot = 0;
+    bool top = false;
+};
+static XPlan xplan(const sv_state *sv, int rank, const std::vector<int> &G, const std::vector<int> &L) {
+    XPlan x;
+    x.k = (int)G.size();
+    std::vector<std::pair<int, int>> pr;
+    for (int i = 0; i < x.k; i++) pr.push_back({L[i], G[i]});
+    std::sort(pr.begin(), pr.end());
+    for (auto &q : pr) {
+        x.Ls.push_back(q.first);
+        x.Gs.push_back(q.second);
     }
-    const bool top = lbit == sv->nloc - 1;
-    for (uint64_t off = 0; off < half; off += chunk) {
-        const uint64_t cnt = std::min(chunk, half - off);
-        const double2 *sendp;
-        if (top) {
-            sendp = sv->psi + (uint64_t)val * half + off;
-        } else {
-            cuda_check(dev::launch_pack(sv->psi, sv->d_xsend, lbit, val, off, cnt, sv->stream), "pack");
-            sendp = sv->d_xsend;
+    for (int i = 0; i < x.k; i++) x.own |= (uint32_t)((rank >> (x.Gs[i] - sv->nloc)) & 1) << i;
+    x.slot = sv->local_amps() >> x.k;
+    x.top = true;
+    for (int i = 0; i < x.k; i++) x.top &= x.Ls[i] == sv->nloc - x.k + i;
+    return x;
+}
+static int xpeer(const sv_state *sv, const XPlan &x, int rank, uint32_t p) {
+    int r = rank;
+    for (int i = 0; i < x.k; i++) {
+        const int gb = x.Gs[i] - sv->nloc;
+        r = (r & ~(1 << gb)) | (int)(((p >> i) & 1u) << gb);
+    }
+    return r;
+}
+static uint64_t xchunk(const XPlan &x) { return std::min<uint64_t>(x.slot, 1ull << 24); }
+
+static void ensure_xbuf(sv_state *sv, size_t n) {
+    if (sv->x_len >= n) return;
+    pool_free(sv->d_xsend, sv->stream);
+    pool_free(sv->d_xrecv, sv->stream);
+    sv->d_xsend = sv->d_xrecv = nullptr;
+    sv->x_len = 0;
+    cuda_check(pool_malloc((void **)&sv->d_xsend, sizeof(double2) * n, sv->stream), "cudaMalloc(xsend)");
+    cuda_check(pool_malloc((void **)&sv->d_xrecv, sizeof(double2) * n, sv->stream), "cudaMalloc(xrecv)");
+    sv->x_len = n;
+}
+
+static void exchange(sv_state *sv, const std::vector<int> &G, const std::vector<int> &L) {
+    const XPlan x = xplan(sv, sv->rank, G, L);
+    const uint32_t np = (1u << x.k) - 1;
+    const uint64_t C = xchunk(x);
+    ensure_xbuf(sv, (size_t)np * C);
+    std::vector<const double *> sb(np);
+    std::vector<double *> rb(np);
+    std::vector<int> peers(np);
+    for (uint64_t off = 0; off < x.slot; off += C) {
+        const uint64_t cnt = std::min(C, x.slot - off);
+        uint32_t i = 0;
+        for (uint32_t p = 0; p <= np; p++) {
+            if (p == x.own) continue;
+            peers[i] = xpeer(sv, x, sv->rank, p);
+            rb[i] = (double *)(sv->d_xrecv + (size_t)i * C);
+            if (x.top) {
+                sb[i] = (const double *)(sv->psi + (uint64_t)p * x.slot + off);
+            } else {
+                cuda_check(dev::launch_pack_multi(sv->psi, sv->d_xsend + (size_t)i * C, x.Ls.data(), x.k, p, off, cnt,
+                                                  sv->stream),
+                           "exchange pack");
+                sb[i] = (const double *)(sv->d_xsend + (size_t)i * C);
+            }
+            i++;
         }
-        nccl_check(nccl_sendrecv(sv->comm, (const double *)sendp, (double *)sv->d_xrecv, 2 * cnt, partner,
-                                 sv->stream),
-                   "exchange sendrecv");
-        if (top)
-            cuda_check(cudaMemcpyAsync(sv->psi + (uint64_t)val * half + off, sv->d_xrecv, sizeof(double2) * cnt,
-                                       cudaMemcpyDeviceToDevice, sv->stream),
-                       "exchange copy");
-        else
-            cuda_check(dev::launch_unpack(sv->psi, sv->d_xrecv, lbit, val, off, cnt, sv->stream), "unpack");
+        nccl_check(nccl_alltoall_pairs(sv->comm, sb.data(), rb.data(), peers.data(), (int)np, 2 * cnt, sv->stream),
+                   "exchange all-to-all");
+        i = 0;
+        for (uint32_t p = 0; p <= np; p++) {
+            if (p == x.own) continue;
+            if (x.top)
+                cuda_check(cudaMemcpyAsync(sv->psi + (uint64_t)p * x.slot + off, sv->d_xrecv + (size_t)i * C,
+                                           sizeof(double2) * cnt, cudaMemcpyDeviceToDevice, sv->stream),
+                           "exchange copy");
+            else
+                cuda_check(dev::launch_unpack_multi(sv->psi, sv->d_xrecv + (size_t)i * C, x.Ls.data(), x.k, p, off, cnt,
+                                                    sv->stream),
+                           "exchange unpack");
+            i++;
+        }
     }
 }
 
-// Virtual sharding: the same exchange between in-process shards (pack both halves, swap).
-static void virtual_exchange(sv_state *sv, int gbit, int lbit) {
-    const int gb = gbit - sv->nloc;
-    const uint64_t half = sv->local_amps() >> 1;
-    const uint64_t chunk = std::min<uint64_t>(half, 1ull << 26);
-    if (sv->x_len < chunk) {
-        pool_free(sv->d_xsend, sv->stream);
-        pool_free(sv->d_xrecv, sv->stream);
-        sv->d_xsend = sv->d_xrecv = nullptr;
-        cuda_check(pool_malloc((void **)&sv->d_xsend, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xsend)");
-        cuda_check(pool_malloc((void **)&sv->d_xrecv, sizeof(double2) * chunk, sv->stream), "cudaMalloc(xrecv)");
-        sv->x_len = chunk;
-    }
+// Virtual sharding: the same exchange between the in-process shards (device copies): for every
+// rank r and pattern p != own(r) with s = peer(r, p) > r, swap r's slot p with s's slot own(r).
+static void virtual_exchange(sv_state *sv, const std::vector<int> &G, const std::vector<int> &L) {
+    const sv_state *v0 = sv->views[0];
+    const XPlan x0 = xplan(v0, 0, G, L);
+    const uint64_t C = xchunk(x0);
+    ensure_xbuf(sv, C);
     for (int r = 0; r < sv->vworld; r++) {
-        const int q = r ^ (1 << gb);
-        if (q < r) continue;
-        sv_state *A = sv->views[r], *B = sv->views[q];
-        const int va = 1 - ((r >> gb) & 1), vb = 1 - ((q >> gb) & 1);
-        for (uint64_t off = 0; off < half; off += chunk) {
-            const uint64_t cnt = std::min(chunk, half - off);
-            cuda_check(dev::launch_pack(A->psi, sv->d_xsend, lbit, va, off, cnt, sv->stream), "vpack");
-            cuda_check(dev::launch_pack(B->psi, sv->d_xrecv, lbit, vb, off, cnt, sv->stream), "vpack");
-            cuda_check(dev::launch_unpack(A->psi, sv->d_xrecv, lbit, va, off, cnt, sv->stream), "vunpack");
-            cuda_check(dev::launch_unpack(B->psi, sv->d_xsend, lbit, vb, off, cnt, sv->stream), "vunpack");
+        const XPlan xr = xplan(v0, r, G, L);
+        for (uint32_t p = 0; p < (1u << xr.k); p++) {
+            if (p == xr.own) continue;
+            const int s = xpeer(v0, xr, r, p);
+            if (s < r) continue;
+            sv_state *A = sv->views[r], *B = sv->views[s];
+            for (uint64_t off = 0; off < xr.slot; off += C) {
+                const uint64_t cnt = std::min(C, xr.slot - off);
+                cuda_check(dev::launch_pack_multi(A->psi, sv->d_xsend, xr.Ls.data(), xr.k, p, off, cnt, sv->stream), "vpack");
+                cuda_check(dev::launch_pack_multi(B->psi, sv->d_xrecv, xr.Ls.data(), xr.k, xr.own, off, cnt, sv->stream),
+                           "vpack");
+                cuda_check(dev::launch_unpack_multi(A->psi, sv->d_xrecv, xr.Ls.data(), xr.k, p, off, cnt, sv->stream),
+                           "vunpack");
+                cuda_check(dev::launch_unpack_multi(B->psi, sv->d_xsend, xr.Ls.data(), xr.k, xr.own, off, cnt, sv->stream),
+                           "vunpack");
+            }
         }
     }
 }
@@ -648,7 +703,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     if (p->resets) {
         p->phys_in.resize(sv->n);
         std::iota(p->phys_in.begin(), p->phys_in.end(), 0);
-        if ((int)co.phys_init.size() == sv->n && sv->nloc == sv->n) p->phys_in = co.phys_init;
+        if ((int)co.phys_init.size() == sv->n) p->phys_in = co.phys_init;
     } else {
         p->phys_in = sv->phys;
     }
@@ -758,8 +813,9 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 }
                 break;
             case StepKind::Exchange:
-                rec.gbit = st.gbit;
-                rec.lbit = st.lbit;
+                rec.xg = st.xg;
+                rec.xl = st.xl;
+                rec.bytes = 2.0 * 16.0 * (double)sv->local_amps() * (1.0 - std::ldexp(1.0, -(int)st.xg.size()));
                 break;
             case StepKind::Dense: {
                 const Gate &g = st.tile_ops[0];
@@ -957,9 +1013,10 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
 static int rec_launches(const sv_state *sv, const LaunchRec &r) {
     if (r.skip) return 0;
     if (r.kind != StepKind::Exchange) return 1;
-    const uint64_t half = sv->local_amps() >> 1;
-    const uint64_t chunks = (half + (1ull << 26) - 1) >> 26;
-    return r.lbit == sv->nloc - 1 ? 0 : (int)(2 * chunks);   // pack + unpack kernels
+    const XPlan x = xplan(sv, sv->rank, r.xg, r.xl);
+    const uint64_t C = xchunk(x);
+    const uint64_t chunks = (x.slot + C - 1) / C;
+    return x.top ? 0 : (int)(2 * chunks * ((1u << x.k) - 1));   // pack + unpack kernels
 }
 
 }  // namespace hhlsv
@@ -999,7 +1056,7 @@ void program_run(sv_state *sv, sv_program *p) {
         const size_t ns = p->subs[0]->recs.size();
         for (size_t i = 0; i < ns; i++) {
             if (p->subs[0]->recs[i].kind == StepKind::Exchange) {
-                virtual_exchange(sv, p->subs[0]->recs[i].gbit, p->subs[0]->recs[i].lbit);
+                virtual_exchange(sv, p->subs[0]->recs[i].xg, p->subs[0]->recs[i].xl);
                 continue;
             }
             for (size_t r = 0; r < p->subs.size(); r++) launch_rec(sv->views[r], p->subs[r], p->subs[r]->recs[i]);
@@ -1034,7 +1091,7 @@ void program_run(sv_state *sv, sv_program *p) {
                 else
                     cuda_check(dev::launch_tile(r.tile, sv->stream), "tile");
                 break;
-            case StepKind::Exchange: exchange(sv, r.gbit, r.lbit); break;
+            case StepKind::Exchange: exchange(sv, r.xg, r.xl); break;
         }
         if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
     }
@@ -1075,6 +1132,13 @@ static void allreduce_if_sharded(sv_state *sv, double *dbuf, size_t count) {
     if (sv->world > 1) nccl_check(nccl_allreduce_sum(sv->comm, dbuf, count, sv->stream), "allreduce");
 }
 
+// Stream synchronisation of a readout. Sharded states: poll with NCCL failure detection (asynchronous
+// communicator errors, a 300 s timeout for a lost peer) instead of blocking forever.
+static void sync_readout(sv_state *sv, const char *what) {
+    if (sv->world > 1) nccl_check(nccl_wait(sv->comm, sv->stream, 300.0), what);
+    else cuda_check(cudaStreamSynchronize(sv->stream), what);
+}
+
 double state_norm2(sv_state *sv) {
     if (sv->vworld > 1) {
         double t = 0.0;
@@ -1085,7 +1149,7 @@ double state_norm2(sv_state *sv) {
     allreduce_if_sharded(sv, sv->d_scalar, 1);
     double h = 0.0;
     cuda_check(cudaMemcpyAsync(&h, sv->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, sv->stream), "norm2 d2h");
-    cuda_check(cudaStreamSynchronize(sv->stream), "norm2 sync");
+    sync_readout(sv, "norm2 sync");
     return h;
 }
 
@@ -1142,7 +1206,7 @@ void state_probabilities(sv_state *sv, const int *qubits, int nq, double *out) {
         cuda_check(cudaMemcpyAsync(sv->d_red, out, sizeof(double) * nout, cudaMemcpyHostToDevice, sv->stream), "h2d");
         allreduce_if_sharded(sv, sv->d_red, nout);
         cuda_check(cudaMemcpyAsync(out, sv->d_red, sizeof(double) * nout, cudaMemcpyDeviceToHost, sv->stream), "d2h");
-        cuda_check(cudaStreamSynchronize(sv->stream), "probabilities sync");
+        sync_readout(sv, "probabilities sync");
     }
 }
 
@@ -1182,7 +1246,7 @@ void state_read(sv_state *sv, uint64_t first, uint64_t count, double *out) {
         cuda_check(cudaMemcpyAsync(out + 2 * off, sv->d_io, sizeof(double2) * c, cudaMemcpyDeviceToHost, sv->stream),
                    "read d2h");
     }
-    cuda_check(cudaStreamSynchronize(sv->stream), "read sync");
+    sync_readout(sv, "read sync");
 }
 
 void state_write(sv_state *sv, uint64_t first, uint64_t count, const double *in) {
@@ -1310,7 +1374,7 @@ void state_postselect(sv_state *sv, const int *fq, const int *fv, int nfixed, do
     allreduce_if_sharded(sv, (double *)sv->d_io, 2 * n_out);
     cuda_check(cudaMemcpyAsync(amps, sv->d_io, sizeof(double2) * n_out, cudaMemcpyDeviceToHost, sv->stream),
                "postselect d2h");
-    cuda_check(cudaStreamSynchronize(sv->stream), "postselect sync");
+    sync_readout(sv, "postselect sync");
     if (idx)
         for (uint64_t e = 0; e < n_out; e++) {
             uint64_t L = fixed;

@@ -44,7 +44,7 @@ struct LaunchRec {
     dev::RecipArgs recip{};
     dev::ProductArgs prod{};
     dev::TileArgs tile{};
-    int gbit = 0, lbit = 0;           // exchange
+    std::vector<int> xg, xl;          // exchange: physical global bits xg[i] <-> local bits xl[i]
     int jit = -1;                     // tile: index into sv_program::jit (specialised kernel) or -1
     double flops = 0;                 // FP64 flops the launch must execute (structure-aware count)
     double bytes = 0;

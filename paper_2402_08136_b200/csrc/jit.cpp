@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -220,6 +221,7 @@ const JitConfig &jit_config() {
             else if (key == "sparse") x.sparse = iv != 0;
             else if (key == "tail") x.tail = iv != 0;
             else if (key == "cw") x.cw = iv != 0;
+            else if (key == "ctab") x.ctab = iv != 0;
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "ru") x.ru = std::max(0, iv);
@@ -340,6 +342,59 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         dsub_max = std::max(dsub_max, used);
         used_ph.push_back(used);
     }
+    // Small diagonal tables as constant-bank operands: a diagonal op (not in a precomposed run) whose
+    // table index has no out-of-tile bits and at most 2 thread bits takes its entries from the by-value
+    // kernel parameter (values per launch, like the wide matrices), chosen per thread by selects on its
+    // thread bits: no L1/L2 table loads (their latency stalled the complex multiplies, ncu r02), no LSU
+    // traffic. Only the entries the op's touched register slots can reach are passed.
+    std::map<int, std::map<uint32_t, size_t>> ctab;     // op -> (table index -> position in cw[])
+    auto tbits_of = [](const dev::RegOp &op) {           // (tile position, table bit) of the thread part
+        std::vector<std::pair<int, int>> v;
+        for (int r = 0; r < op.ntr; r++)
+            for (int l = 0; l < op.t_len[r]; l++) v.push_back({op.t_src[r] + l, op.t_dst[r] + l});
+        return v;
+    };
+    if (cwide && cfg.cw && cfg.ctab) {
+        for (size_t i = 0; i < ops.size(); i++) {
+            const auto &op = ops[i];
+            if (op.kind != 1 || op.ngr != 0) continue;
+            bool in_run = false;
+            for (auto &dr : druns) in_run |= (int)i >= dr.a && (int)i < dr.b;
+            if (in_run) continue;
+            const auto tbv = tbits_of(op);
+            if (tbv.size() > 2) continue;
+            std::map<uint32_t, size_t> ent;
+            for (int j = 0; j < 16; j++) {
+                if ((j & op.rcm) != op.rcv) continue;
+                for (uint32_t c = 0; c < (1u << tbv.size()); c++) {
+                    uint32_t idx = op.ridx[j];
+                    for (size_t b = 0; b < tbv.size(); b++)
+                        if ((c >> b) & 1) idx |= 1u << tbv[b].second;
+                    ent.emplace(idx, 0);
+                }
+            }
+            if (ctot + ent.size() > 2040) continue;      // kernel parameter space: 32764 bytes
+            for (auto &e : ent) {
+                e.second = ctot++;
+                cwide->push_back({op.data_off + e.first, 1});
+            }
+            ctab[(int)i] = std::move(ent);
+        }
+    }
+    // table entry of diagonal op oi at register-slot index r; ibv = the op's runtime index variable
+    auto dval = [&](int oi, uint32_t r, const std::string &ibv) -> std::string {
+        const dev::RegOp &op = ops[oi];
+        auto it = ctab.find(oi);
+        if (it == ctab.end())
+            return "__ldg(blob + " + std::to_string(op.data_off) + "ull + (" + ibv + " | " + std::to_string(r) + "u))";
+        const auto tbv = tbits_of(op);
+        std::function<std::string(size_t, uint32_t)> sel = [&](size_t b, uint32_t idx) -> std::string {
+            if (b == tbv.size()) return "cwa.w[" + std::to_string(it->second.at(idx)) + "]";
+            return "(((tb >> " + std::to_string(tbv[b].first) + ") & 1u) ? " + sel(b + 1, idx | (1u << tbv[b].second)) +
+                   " : " + sel(b + 1, idx) + ")";
+        };
+        return sel(0, r);
+    };
     // Hoisted sub-tables (default): phase p+1's tables are built at the end of phase p (the next
     // tile's phase-0 tables at the end of the last phase) into a region phase p-1 no longer reads,
     // so the barrier that ends phase p also publishes them: no separate barrier per sub-table build.
@@ -519,14 +574,25 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             const int pfd = std::max(1, cfg.pf_dist);
             k << "    if (tile + " << pfd << "ull * gridDim.x < n_tiles) {\n      const u64 nb = tile_base(tile + " << pfd
               << "ull * gridDim.x);\n";
-            if (din) {
-                k << "      if ((threadIdx.x & 7u) == 0u) { const char *g = (const char *)(psi + (nb | pd_in));";
-                for (int j = 0; j < 16; j++)
+            if (din) {       // known-zero slots (zload) are never read: not prefetched either
+                uint32_t rz0 = 0;
+                for (int i = 0; i < dev::kRegBits; i++) rz0 |= 1u << ph.front().R[i];
+                const bool thr_z = (a.zload & ~rz0) != 0;
+                k << "      if ((threadIdx.x & 7u) == 0u" << (thr_z ? " && !((" + tb_expr(ph.front()) + ") & " +
+                                                                       std::to_string(a.zload) + "u)" : std::string())
+                  << ") { const char *g = (const char *)(psi + (nb | pd_in));";
+                for (int j = 0; j < 16; j++) {
+                    uint32_t rdj = 0;
+                    for (int i = 0; i < dev::kRegBits; i++)
+                        if ((j >> i) & 1) rdj |= 1u << ph.front().R[i];
+                    if (rdj & a.zload) continue;
                     k << " asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(g + " << u64s(16 * phys_slot(ph.front(), j)) << "));";
+                }
                 k << " }\n";
             } else {
-                k << "      for (u32 u = threadIdx.x * 8u; u < NT; u += " << 8 * NTHR
-                  << "u) asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(psi + addr(nb, u)));\n";
+                k << "      for (u32 u = threadIdx.x * 8u; u < NT; u += " << 8 * NTHR << "u) "
+                  << (a.zload ? "if (!(u & " + std::to_string(a.zload) + "u)) " : std::string())
+                  << "asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(psi + addr(nb, u)));\n";
             }
             k << "    }\n";
         }
@@ -805,10 +871,9 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 k << "        const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
                   << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
                 if (op.kind == 1) {
-                    k << "        const double2 *D = blob + " << op.data_off << "ull;\n";
                     for (int j = 0; j < 16; j++)
                         if ((j & op.rcm) == op.rcv)
-                            k << "        const double2 d" << j << " = __ldg(D + (ib | " << op.ridx[j] << "u));\n";
+                            k << "        const double2 d" << j << " = " << dval(oi, op.ridx[j], "ib") << ";\n";
                     for (int j = 0; j < 16; j++)
                         if ((j & op.rcm) == op.rcv) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
                 } else {
@@ -902,8 +967,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     const dev::RegOp &op = ops[oi];
                     int j0 = 0;
                     while (!((kv.first >> j0) & 1u)) j0++;
-                    std::string ld = "__ldg(blob + " + std::to_string(op.data_off) + "ull + (ib" + std::to_string(oi) +
-                                     " | " + std::to_string(op.ridx[j0]) + "u))";
+                    std::string ld = dval(oi, op.ridx[j0], "ib" + std::to_string(oi));
                     const std::string cnd = op_cond(op);      // guarded op: factor 1 where the guard fails
                     if (!cnd.empty()) ld = "((" + cnd + ") ? " + ld + " : mk(1.0, 0.0))";
                     if (first) k << "        double2 " << U << " = " << ld << ";\n";
@@ -922,8 +986,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     if (it == sym.end()) {
                         const std::string L = "L" + std::to_string(oi) + "_" + std::to_string(op.ridx[j]);
                         const std::string cnd = op_cond(op);
-                        k << "        const double2 " << L << " = " << (cnd.empty() ? "" : "(" + cnd + ") ? ") << "__ldg(blob + "
-                          << op.data_off << "ull + (ib" << oi << " | " << op.ridx[j] << "u))" << (cnd.empty() ? "" : " : mk(1.0, 0.0)")
+                        k << "        const double2 " << L << " = " << (cnd.empty() ? "" : "(" + cnd + ") ? ")
+                          << dval(oi, op.ridx[j], "ib" + std::to_string(oi)) << (cnd.empty() ? "" : " : mk(1.0, 0.0)")
                           << ";\n";
                         it = sym.emplace(op.ridx[j], L).first;
                     }

@@ -42,6 +42,7 @@ struct JitConfig {
     bool sparse = true;       // sparse: exact structural zeros of wide matrices skipped at codegen
     bool tail = true;         // tail: a trailing wide dense op writes straight into the store buffer
     bool cw = true;           // cw: >= 3-target matrices as by-value kernel parameters (constant bank)
+    bool ctab = true;         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
     int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)

@@ -823,6 +823,48 @@ __global__ void k_unpack(double2 *psi, const double2 *buf, int lbit, int val, ui
         psi[insz(off + j, lbit) | ((uint64_t)val << lbit)] = buf[j];
 }
 
+// Multi-bit form (multi-qubit exchanges): element j of the slot whose bits L (ascending, nl <= 8)
+// equal `pat` (bit i of pat <- L[i]) is psi[deposit(off + j) | pat bits], deposit = zeros inserted at L.
+struct PatBits {
+    int nl;
+    int L[8];
+    uint64_t patmask;
+};
+__device__ __forceinline__ uint64_t pat_index(const PatBits &b, uint64_t x) {
+    for (int i = 0; i < b.nl; i++) x = insz(x, b.L[i]);
+    return x | b.patmask;
+}
+__global__ void k_packm(const double2 *psi, double2 *buf, PatBits b, uint64_t off, uint64_t cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        buf[j] = psi[pat_index(b, off + j)];
+}
+__global__ void k_unpackm(double2 *psi, const double2 *buf, PatBits b, uint64_t off, uint64_t cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        psi[pat_index(b, off + j)] = buf[j];
+}
+static PatBits pat_bits(const int *L, int nl, uint32_t pat) {
+    PatBits b{};
+    b.nl = nl;
+    for (int i = 0; i < nl; i++) b.L[i] = L[i];
+    for (int i = 0; i < nl; i++)
+        if ((pat >> i) & 1) b.patmask |= 1ull << L[i];
+    return b;
+}
+cudaError_t launch_pack_multi(const double2 *psi, double2 *buf, const int *L, int nl, uint32_t pat, uint64_t off,
+                              uint64_t cnt, cudaStream_t s) {
+    if (nl < 1 || nl > 8) return cudaErrorInvalidValue;
+    k_packm<<<grid_for(cnt, kThreads), kThreads, 0, s>>>(psi, buf, pat_bits(L, nl, pat), off, cnt);
+    return cudaGetLastError();
+}
+cudaError_t launch_unpack_multi(double2 *psi, const double2 *buf, const int *L, int nl, uint32_t pat, uint64_t off,
+                                uint64_t cnt, cudaStream_t s) {
+    if (nl < 1 || nl > 8) return cudaErrorInvalidValue;
+    k_unpackm<<<grid_for(cnt, kThreads), kThreads, 0, s>>>(psi, buf, pat_bits(L, nl, pat), off, cnt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack(const double2 *psi, double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
                         cudaStream_t s) {
     k_pack<<<grid_for(cnt, kThreads), kThreads, 0, s>>>(psi, buf, lbit, val, off, cnt);

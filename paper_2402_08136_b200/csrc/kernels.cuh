@@ -182,6 +182,12 @@ cudaError_t launch_pack(const double2 *psi, double2 *buf, int lbit, int val, uin
                         cudaStream_t s);
 cudaError_t launch_unpack(double2 *psi, const double2 *buf, int lbit, int val, uint64_t off, uint64_t cnt,
                           cudaStream_t s);
+// Multi-qubit exchanges: pack/unpack elements [off, off+cnt) of the slot whose local bits L
+// (ASCENDING, nl <= 8) equal pattern pat (bit i of pat <- L[i]), in increasing order of the other bits.
+cudaError_t launch_pack_multi(const double2 *psi, double2 *buf, const int *L, int nl, uint32_t pat, uint64_t off,
+                              uint64_t cnt, cudaStream_t s);
+cudaError_t launch_unpack_multi(double2 *psi, const double2 *buf, const int *L, int nl, uint32_t pat, uint64_t off,
+                                uint64_t cnt, cudaStream_t s);
 
 }  // namespace dev
 }  // namespace hhlsv

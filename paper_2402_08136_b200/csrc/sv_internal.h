@@ -127,8 +127,8 @@ struct Step {
     // keeps the physical bits phase_R[p] (kRegBits of them) in registers
     std::vector<size_t> phase_start;
     std::vector<std::vector<int>> phase_R;
-    // ---- Exchange: swap physical global bit gbit with local bit lbit
-    int gbit = 0, lbit = 0;
+    // ---- Exchange: swap physical global bits xg[i] with local bits xl[i] (one all-to-all round)
+    std::vector<int> xg, xl;
     // ---- InitProduct: factors on physical bits
     std::vector<ProductFactor> factors;
     double bytes = 0;              // HBM bytes this step moves (read + write), per rank

@@ -276,7 +276,7 @@ def test_s30_engine_parity_oracle_gates(s30_reference):
 VMODES = [dict(tile_qubits=-1), dict(tile_qubits=8, tile_jit=-1), dict(tile_qubits=8, tile_jit=1)]
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("mode", VMODES)
 def test_virtual_shards_random_circuits(world, mode):
     """world > 1 without NCCL: the sharded scheduler (exchanges, rank-resolved controls/diagonals),
@@ -295,9 +295,13 @@ def test_virtual_shards_random_circuits(world, mode):
         assert abs(st.norm2() - 1.0) < 1e-12
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("opts", [dict(), dict(qpe_mode=1), dict(tile_qubits=-1), dict(tile_jit=1, tile_qubits=9)])
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("opts", [dict(), dict(qpe_mode=1), dict(tile_qubits=-1), dict(tile_jit=1, tile_qubits=9),
+                                  configs.BENCH_OPTS, dict(configs.BENCH_OPTS, tile_qubits=8)])
 def test_virtual_shards_hhl(world, opts):
+    """Sharded HHL (in-process virtual shards). With the bench options (eigenbasis) the top system
+    qubits are global and the circuit needs one multi-qubit exchange (all-to-all) before V.
+    """
     A, b, nc = configs.get("C3")
     xo, po, psi_o, p = ohhl.solve(A, b, nc)
     st = pkg.State(p.n, world=world)

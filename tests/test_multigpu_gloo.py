@@ -43,7 +43,8 @@ def _parse(txt):
         if not t:
             continue
         if t[0] == "EXCHANGE":
-            steps.append(("X", int(t[1].split("=")[1]), int(t[2].split("=")[1])))
+            steps.append(("X", [int(x) for x in t[1].split("=")[1].split(",")],
+                          [int(x) for x in t[2].split("=")[1].split(",")]))
         elif t[0] in ("DENSE", "CONTROLLED", "DIAGONAL", "RECIP_RY"):
             steps.append(("G", ln))
         elif t[0] == "FINAL_MAP":
@@ -136,17 +137,30 @@ def _worker(rank, world, port, n, gates, fk, tile, out_q):
         half = 1 << (nloc - 1)
         for st in steps:
             if st[0] == "X":
-                _, gbit, lbit = st
-                partner = rank ^ (1 << (gbit - nloc))
-                val = 1 - ((rank >> (gbit - nloc)) & 1)
-                idx = np.array([i for i in range(1 << nloc) if ((i >> lbit) & 1) == val])
-                send = torch.from_numpy(np.ascontiguousarray(psi[idx]).view(np.float64).copy())
-                recv = torch.empty_like(send)
-                reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
+                # swap the values of global bits G[i] and local bits L[i]: the amplitude at (rank, i)
+                # moves to the rank whose G bits equal i's L bits, where its L bits become this
+                # rank's G bits. Slot p (L bits == p) goes to peer(p); slot p is refilled from peer(p).
+                _, G, L = st
+                k = len(G)
+                own = sum(((rank >> (G[j] - nloc)) & 1) << j for j in range(k))
+                bufs, reqs = {}, []
+                for p_ in range(1 << k):
+                    if p_ == own:
+                        continue
+                    peer = rank
+                    for j in range(k):
+                        peer = (peer & ~(1 << (G[j] - nloc))) | (((p_ >> j) & 1) << (G[j] - nloc))
+                    idx = np.array([i for i in range(1 << nloc)
+                                    if all(((i >> L[j]) & 1) == ((p_ >> j) & 1) for j in range(k))])
+                    assert len(idx) == (1 << nloc) >> k
+                    send = torch.from_numpy(np.ascontiguousarray(psi[idx]).view(np.float64).copy())
+                    recv = torch.empty_like(send)
+                    bufs[p_] = (idx, recv, send)
+                    reqs += [dist.isend(send, peer), dist.irecv(recv, peer)]
                 for r in reqs:
                     r.wait()
-                psi[idx] = recv.numpy().view(np.complex128)
-                assert len(idx) == half
+                for idx, recv, _ in bufs.values():
+                    psi[idx] = recv.numpy().view(np.complex128)
                 continue
             gate = next(it)
             tg, cb = _phys_bits(st[1])
@@ -213,3 +227,33 @@ def test_hhl_circuit_sharded_gloo(world):
     got = _run(p.n, gates, world)
     ref = sim.run(gates, p.n)
     assert np.abs(got - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_multi_qubit_exchange_gloo(world):
+    """Ops with several non-diagonal targets on global qubits get ONE multi-qubit exchange (an
+    all-to-all among 2^k ranks, k = 2, 3): emulated here per the protocol of DESIGN.md §7."""
+    n = 8
+    gates = synthetic.random_circuit(n, 40, seed=4 + world, kmax=3)      # unfused 1-3 qubit gates
+    txt, _ = pkg.schedule_dump(n, gates, world=world, fusion_kmax=0, tile_qubits=-1)
+    assert any("," in ln.split()[1] for ln in txt.splitlines() if ln.startswith("EXCHANGE"))
+    got = _run(n, gates, world)
+    ref = sim.run(gates, n)
+    assert np.abs(got - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("cfg,world", [("S31", 2), ("S32", 4), ("S33", 8)])
+def test_weak_scaling_schedule(cfg, world):
+    """configs[4] weak-scaling schedules (host-only planner, bench options): the sharded eigenbasis
+    HHL keeps the top system qubits global, so the whole circuit needs ONE exchange round (before
+    the final V), with the top local bits as victims (zero-copy contiguous slots); at most 7 HBM
+    passes per rank (S30 on one GPU: 5)."""
+    A, b, nc = configs.get(cfg)
+    txt, rep = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, world=world, **configs.BENCH_OPTS)
+    ex = [ln for ln in txt.splitlines() if ln.startswith("EXCHANGE")]
+    g = world.bit_length() - 1
+    nloc = rep["n_total"] - g
+    assert rep["n_passes"] <= 7
+    assert len(ex) <= 2
+    loc = sorted(int(x) for x in ex[0].split()[2].split("=")[1].split(","))
+    assert loc == list(range(nloc - g, nloc))
