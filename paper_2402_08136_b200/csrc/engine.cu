@@ -6,6 +6,8 @@
 
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.h"
 
 namespace hhlsv {
@@ -1077,6 +1079,13 @@ void program_run(sv_state *sv, sv_program *p) {
             if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
             continue;
         }
+        // NVTX range per step (SURVEY §5 tracing): one per tile pass / streaming op / exchange, named by
+        // kind and step index; a no-op unless a tool (nsys, ncu --nvtx) is attached
+        static const char *knames[] = {"init_zero", "init_product", "dense", "diagonal", "recip_ry", "tile_pass",
+                                       "exchange"};
+        char rname[64];
+        snprintf(rname, sizeof rname, "hhlsv %s #%zu", knames[(int)r.kind], ri);
+        nvtxRangePushA(rname);
         switch (r.kind) {
             case StepKind::InitZero: cuda_check(dev::launch_zero_init(sv->psi, sv->local_amps(), sv->rank == 0, sv->stream), "init"); break;
             case StepKind::InitProduct: cuda_check(dev::launch_product(r.prod, sv->stream), "product init"); break;
@@ -1093,6 +1102,7 @@ void program_run(sv_state *sv, sv_program *p) {
                 break;
             case StepKind::Exchange: exchange(sv, r.xg, r.xl); break;
         }
+        nvtxRangePop();
         if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
     }
     sv->phys = p->sched.phys_out;

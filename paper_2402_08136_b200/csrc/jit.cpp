@@ -1239,13 +1239,21 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     const int threads = 1 << (T - dev::kRegBits);
     const size_t smem = jit_smem_bytes(T, p.smem_extra);
     const void *f = reinterpret_cast<const void *>(p.kern);
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    uint64_t grid = (uint64_t)148 * per_sm;
+    cudaError_t e = cudaSuccess;
+    if (p.per_sm == 0) {
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem);
+        if (e != cudaSuccess) return e;
+        p.per_sm = per_sm < 1 ? 1 : per_sm;
+        int dev = 0, sms = 0;
+        e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        p.sms = sms;                 // 148 on the B200: persistent grid = SMs x resident CTAs
+    }
+    uint64_t grid = (uint64_t)p.sms * p.per_sm;
     if (grid > n_tiles) grid = n_tiles;
     void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base, (void *)p.cwvals.data()};
     return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);

@@ -20,6 +20,9 @@ struct JitPass {
     // host copy of those values passed at every launch
     std::vector<std::pair<uint64_t, uint64_t>> cwide;
     std::vector<double2> cwvals;
+    // launch configuration, resolved on the first launch (attribute + occupancy queries are host
+    // work a launch-bound small program should not repeat)
+    mutable int per_sm = 0, sms = 0;
 };
 
 // Product-state init fused into the first tile pass: the pass computes its tile's amplitudes
