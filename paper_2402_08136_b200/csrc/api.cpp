@@ -546,12 +546,17 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
             prog = build_hhl(sv, A, b, N, &o, &r);
             const double t0 = now_s();
             program_run(sv, prog);
+            if (prof_on()) {
+                cudaStreamSynchronize(sv->stream);
+                prof_mark("  program_run");
+            }
             // one reduction gives the norm and P(ancilla = 1) (logical qubit n-1)
             double pa[2] = {0.0, 0.0};
             const int anc = p.n - 1;
             state_probabilities(sv, &anc, 1, pa);
             r.norm2 = pa[0] + pa[1];
             r.p_anc1 = pa[1];
+            prof_mark("  norm + P(ancilla)");
             readout(sv, &r, N, x_out, &r.p_success);
             r.t_sim_s = now_s() - t0;
             prof_mark("run + readout");

@@ -28,9 +28,13 @@ namespace hhlsv {
 // ------------------------------------------------------------------ errors ----
 void fail(sv_status code, const std::string &msg) { throw Error{code, msg}; }
 
-void prof_mark(const char *stage) {
+bool prof_on() {
     static const bool on = getenv("HHLSV_PROFILE") != nullptr;
-    if (!on) return;
+    return on;
+}
+
+void prof_mark(const char *stage) {
+    if (!prof_on()) return;
     using clk = std::chrono::steady_clock;
     static thread_local clk::time_point last = clk::now();
     const auto now = clk::now();

@@ -48,6 +48,7 @@ struct Error {
 [[noreturn]] void fail(sv_status code, const std::string &msg);
 // Developer stage timer: with HHLSV_PROFILE=1 in the environment prints "<stage> <ms>" to stderr.
 void prof_mark(const char *stage);
+bool prof_on();
 
 // Validation of one ABI gate -> internal Gate (copies the data).
 Gate gate_from_abi(const sv_gate &g, int n_qubits);
