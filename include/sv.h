@@ -145,6 +145,10 @@ typedef struct {
     int tile_qubits;
     int tile_jit;       /* 0: auto (NVRTC-specialised tile passes when the local state has >= 2^18 amplitudes),
                            1: always, -1: never (generic interpreting tile kernel) */
+    int fusion_mode;    /* 0: structure-preserving greedy window of <= fusion_kmax qubits (default);
+                           1: the paper's four prioritised strategies for one-/two-qubit gates (Fig. 4,
+                           PAPER.md:207): 1q+1q, 1q into the following 2q, 1q into the preceding 2q, 2q+2q
+                           on the same pair (fusion_kmax is ignored) */
 } sv_fuse_options;
 
 typedef struct {
@@ -244,6 +248,7 @@ typedef struct {
      * phi_s with gain ~2 pi 2^n_c). */
     const double *eig_lambda;
     const double *eig_vectors;
+    int fusion_mode;    /* as sv_fuse_options.fusion_mode */
 } hhl_options;
 
 typedef struct {

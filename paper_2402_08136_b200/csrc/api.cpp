@@ -44,6 +44,8 @@ FuseOptions fuse_opts(const sv_fuse_options *o) {
     if (o) {
         f.kmax = o->fusion_kmax;
         if (o->diag_kmax > 0) f.diag_kmax = o->diag_kmax;
+        if (o->fusion_mode < 0 || o->fusion_mode > 1) fail(SV_E_ARG, "fusion_mode must be 0 or 1");
+        f.mode = o->fusion_mode;
     }
     if (f.kmax > 5) fail(SV_E_ARG, "fusion_kmax must be <= 5");
     if (f.diag_kmax > 12) fail(SV_E_ARG, "diag_kmax must be <= 12");
@@ -239,32 +241,6 @@ sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_b
 }
 
 // Host-only: generate + NVRTC-compile every tile pass of a schedule; one log line per pass.
-static std::string jit_check_schedule(const Schedule &s) {
-    std::string why;
-    if (!jit_available(&why)) fail(SV_E_CUDA, "tile JIT unavailable: " + why);
-    std::string jitlog;
-    std::vector<double2> blob;
-    std::vector<dev::RegOp> rops;
-    std::vector<dev::RegPhase> phases;
-    for (const Step &st : s.steps) {
-        if (st.kind != StepKind::Tile) continue;
-        dev::TileArgs a{};
-        a.T = (int)st.tile_bits.size();
-        for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
-        size_t ph0 = 0, opb = 0;
-        lower_tile_step(st, a, blob, rops, phases, ph0, opb, true, 0.5);
-        std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
-        std::vector<dev::RegOp> lops(rops.begin() + opb, rops.end());
-        std::string err;
-        std::vector<std::pair<uint64_t, uint64_t>> cwide;
-        auto cubin = jit_compile_only(gen_tile_kernel("hhlsv_tile", a, lph, lops, nullptr, nullptr, &cwide), err);
-        if (cubin.empty()) fail(SV_E_CUDA, err);
-        jitlog += "JIT_PASS phases=" + std::to_string(lph.size()) + " regops=" + std::to_string(lops.size()) +
-                  " cubin_bytes=" + std::to_string(cubin.size()) + "\n";
-    }
-    return jitlog;
-}
-
 sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
                            char *buf, size_t buf_len, sv_plan_report *rep) {
     return guard([&] {
@@ -277,7 +253,23 @@ sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t
         for (int q = 0; q < n_qubits; q++) phys[q] = q;
         CompileOptions co = compile_opts(opt);
         if (co.tile_qubits > 14) co.tile_qubits = 14;
-        Schedule s = compile(gl, nullptr, n_qubits, n_qubits - g, phys, co);
+        std::string jitlog;
+        Schedule s;
+        if (opt && opt->tile_jit > 0) {     // rank 0's program exactly as sv_program_create lowers it (host only)
+            sv_state host{};
+            host.n = n_qubits;
+            host.g = g;
+            host.nloc = n_qubits - g;
+            host.world = world;
+            host.phys = phys;
+            co.dry_run = true;
+            co.dry_log = &jitlog;
+            if (const char *e = getenv("HHLSV_EMU_DIR")) co.emu_dir = e;     // test tooling (tests/jit_emulator.py)
+            std::unique_ptr<sv_program> prog(program_create(&host, gl, nullptr, co, n_gates));
+            s = prog->sched;
+        } else {
+            s = compile(gl, nullptr, n_qubits, n_qubits - g, phys, co);
+        }
         if (rep) {
             rep->n_logical = n_gates;
             rep->n_fused = s.n_fused;
@@ -285,7 +277,6 @@ sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
         }
-        std::string jitlog = (opt && opt->tile_jit > 0) ? jit_check_schedule(s) : std::string();
         if (buf && buf_len) {
             std::string t = dump_schedule(s) + jitlog;
             std::string perm = "FINAL_MAP";
@@ -375,6 +366,8 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     // afterwards); one HBM pass per op: merge them up front
     fo.diag_kmax = (opt && opt->tile_qubits < 0) ? 12 : 4;
     if (opt && opt->diag_kmax > 0) fo.diag_kmax = std::min(12, opt->diag_kmax);
+    if (opt && (opt->fusion_mode < 0 || opt->fusion_mode > 1)) fail(SV_E_ARG, "fusion_mode must be 0 or 1");
+    if (opt) fo.mode = opt->fusion_mode;
     if (n_logical) *n_logical = gates.size();
     return fuse(rest, fo);
 }
@@ -492,6 +485,7 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         std::string jitlog;
         hco.dry_run = opt && opt->tile_jit > 0;
         hco.dry_log = &jitlog;
+        if (const char *e = getenv("HHLSV_EMU_DIR")) hco.emu_dir = e;     // test tooling (tests/jit_emulator.py)
         Schedule s;
         if (hco.dry_run) {
             std::unique_ptr<sv_program> prog(program_create(&host, fused, factors.empty() ? nullptr : &factors, hco,
@@ -513,6 +507,9 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         }
         if (buf && buf_len) {
             std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s) + jitlog;
+            t += "FINAL_MAP";
+            for (int q = 0; q < p.n; q++) t += " " + std::to_string(s.phys_out[q]);
+            t += "\n";
             size_t n = std::min(buf_len - 1, t.size());
             std::memcpy(buf, t.data(), n);
             buf[n] = 0;

@@ -959,6 +959,32 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     if (co.dry_run) {       // host-only planning: compile the generated passes, log every launch
         std::string &L = *co.dry_log;
         char line[512];
+        if (!co.emu_dir.empty()) {      // export for tests/jit_emulator.py (host race/bounds checking)
+            auto wr = [&](const std::string &name, const void *data, size_t bytes) {
+                FILE *f = fopen((co.emu_dir + "/" + name).c_str(), "wb");
+                if (!f) fail(SV_E_ARG, "cannot write " + co.emu_dir + "/" + name);
+                if (bytes) fwrite(data, 1, bytes, f);
+                fclose(f);
+            };
+            wr("blob.bin", blob.data(), blob.size() * sizeof(double2));
+            std::string ls;
+            for (size_t i = 0; i < p->recs.size(); i++) {
+                const LaunchRec &r = p->recs[i];
+                if (r.kind == StepKind::Tile && r.jit >= 0) {
+                    const JitPass &jp = p->jit[r.jit];
+                    wr("src_" + std::to_string(i) + ".cu", jp.src.data(), jp.src.size());
+                    wr("cw_" + std::to_string(i) + ".bin", jp.cwvals.data(), jp.cwvals.size() * sizeof(double2));
+                    snprintf(line, sizeof line, "TILE %zu %llu %d %llu %zu %d\n", i, (unsigned long long)r.tile.n_tiles,
+                             r.tile.T, (unsigned long long)r.tile.rank_base, jp.smem_extra, 1 << (r.tile.T - dev::kRegBits));
+                } else if (r.skip) {
+                    snprintf(line, sizeof line, "SKIP %zu %d\n", i, (int)r.kind);
+                } else {
+                    snprintf(line, sizeof line, "OTHER %zu %d\n", i, (int)r.kind);
+                }
+                ls += line;
+            }
+            wr("launches.txt", ls.data(), ls.size());
+        }
         for (const LaunchRec &r : p->recs) {
             if (r.kind == StepKind::Tile && r.jit >= 0) {
                 std::string err;

@@ -652,6 +652,119 @@ static bool try_merge(Gate &cur, const Gate &nx, const FuseOptions &o) {
     return false;
 }
 
+// ---------------------------------------------------- paper mode (Fig. 4) ----
+// SV-Sim's gate fusion as PAPER.md:207 (Fig. 4 caption) describes it, for "applicable gates" (one-
+// and two-qubit gates): four strategies applied with priority (1) consecutive one-qubit gates on the
+// same qubit are fused; then (2) a one-qubit gate is absorbed into the two-qubit gate that follows it
+// on its qubit, and (3) into the one that precedes it; finally (4) consecutive two-qubit gates on the
+// same qubit pair are fused. "Consecutive" = no other gate touches those qubits in between (gates on
+// other qubits commute with them). Wider gates and the reciprocal rotation are kept as they are and
+// block fusion across them. Diagonal stays diagonal when both parts are diagonal.
+static bool applicable(const Gate &g) {
+    if (g.kind == Kind::Dense || g.kind == Kind::Diagonal) return g.targets.size() <= 2;
+    if (g.kind == Kind::Controlled) return g.targets.size() == 1 && g.controls.size() == 1;
+    return false;
+}
+static std::vector<int> qubits_of(const Gate &g) { return union_of(g.targets, g.controls); }
+static Gate as_plain(const Gate &g) {      // controlled 1+1 -> dense 4x4 on {target, control}
+    if (g.kind != Kind::Controlled) return g;
+    Gate d;
+    d.kind = Kind::Dense;
+    d.targets = {g.targets[0], g.controls[0]};
+    d.data.assign(16, 0.0);
+    const int want = (int)(g.cvals & 1);
+    for (int c = 0; c < 2; c++)
+        for (int r = 0; r < 2; r++)
+            for (int k = 0; k < 2; k++)
+                d.data[(size_t)((c << 1) | r) * 4 + ((c << 1) | k)] = (c == want) ? g.data[r * 2 + k] : cplx(r == k ? 1.0 : 0.0);
+    return d;
+}
+// b applied after a (both applicable, plain): the fused gate on the union of their qubits
+static Gate compose(const Gate &a, const Gate &b) {
+    Gate r;
+    if (a.kind == Kind::Diagonal && b.kind == Kind::Diagonal) {
+        r = a;
+        merge_diagonal(r, b, 64);
+        return r;
+    }
+    auto dense = [](const Gate &g) {
+        if (g.kind == Kind::Dense) return g.data;
+        const size_t d = g.data.size();
+        std::vector<cplx> m(d * d, 0.0);
+        for (size_t i = 0; i < d; i++) m[i * d + i] = g.data[i];
+        return m;
+    };
+    r.kind = Kind::Dense;
+    r.targets = union_of(a.targets, b.targets);
+    const auto ea = embed_dense(dense(a), a.targets, r.targets), eb = embed_dense(dense(b), b.targets, r.targets);
+    r.data = matmul(eb, ea, (size_t)1 << r.targets.size());
+    return r;
+}
+static std::vector<Gate> fuse_paper(std::vector<Gate> g) {
+    for (auto &x : g)
+        if (applicable(x)) x = as_plain(x);
+    std::vector<char> dead(g.size(), 0);
+    auto touches = [&](size_t i, int q) {
+        auto v = qubits_of(g[i]);
+        return std::find(v.begin(), v.end(), q) != v.end();
+    };
+    auto next_on = [&](size_t i, int q) -> long {      // next live gate touching q after i
+        for (size_t j = i + 1; j < g.size(); j++)
+            if (!dead[j] && touches(j, q)) return (long)j;
+        return -1;
+    };
+    auto prev_on = [&](size_t i, int q) -> long {
+        for (long j = (long)i - 1; j >= 0; j--)
+            if (!dead[j] && touches((size_t)j, q)) return j;
+        return -1;
+    };
+    auto is1 = [&](size_t i) { return !dead[i] && applicable(g[i]) && qubits_of(g[i]).size() == 1; };
+    auto is2 = [&](size_t i) { return !dead[i] && applicable(g[i]) && qubits_of(g[i]).size() == 2; };
+    // (1) one-qubit + one-qubit
+    for (size_t i = 0; i < g.size(); i++) {
+        if (!is1(i)) continue;
+        const long j = next_on(i, g[i].targets[0]);
+        if (j >= 0 && is1((size_t)j)) {
+            g[j] = compose(g[i], g[j]);
+            dead[i] = 1;
+        }
+    }
+    // (2) one-qubit into the following two-qubit gate, (3) into the preceding one
+    for (size_t i = 0; i < g.size(); i++) {
+        if (!is1(i)) continue;
+        const long j = next_on(i, g[i].targets[0]);
+        if (j >= 0 && is2((size_t)j)) {
+            g[j] = compose(g[i], g[j]);
+            dead[i] = 1;
+        }
+    }
+    for (size_t i = 0; i < g.size(); i++) {
+        if (!is1(i)) continue;
+        const long j = prev_on(i, g[i].targets[0]);
+        if (j >= 0 && is2((size_t)j)) {
+            g[j] = compose(g[j], g[i]);
+            dead[i] = 1;
+        }
+    }
+    // (4) two-qubit + two-qubit on the same pair
+    for (size_t i = 0; i < g.size(); i++) {
+        if (!is2(i)) continue;
+        auto qi = qubits_of(g[i]);
+        const long j0 = next_on(i, qi[0]), j1 = next_on(i, qi[1]);
+        if (j0 >= 0 && j0 == j1 && is2((size_t)j0)) {
+            auto qj = qubits_of(g[j0]);
+            if ((qj[0] == qi[0] && qj[1] == qi[1]) || (qj[0] == qi[1] && qj[1] == qi[0])) {
+                g[j0] = compose(g[i], g[j0]);
+                dead[i] = 1;
+            }
+        }
+    }
+    std::vector<Gate> out;
+    for (size_t i = 0; i < g.size(); i++)
+        if (!dead[i]) out.push_back(std::move(g[i]));
+    return out;
+}
+
 std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o) {
     // Relabel through SWAPs: name[q] = the qubit that currently holds original wire q's role.
     int nq = 0;
@@ -676,7 +789,7 @@ std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o) {
         Gate g = g0;
         for (int &q : g.targets) q = where[q];
         for (int &q : g.controls) q = where[q];
-        if (o.kmax <= 0) {
+        if (o.kmax <= 0 || o.mode == 1) {
             out.push_back(std::move(g));
             continue;
         }
@@ -686,6 +799,7 @@ std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o) {
         have = true;
     }
     flush();
+    if (o.mode == 1) out = fuse_paper(std::move(out));
     // Realise the accumulated relabelling as trailing swaps (executed as relabels, free).
     std::vector<int> pos = where;               // wire w sits at position pos[w]
     for (int w = 0; w < nq; w++) {

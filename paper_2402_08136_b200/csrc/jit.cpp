@@ -126,6 +126,7 @@ __device__ __forceinline__ double2 ldcs_v(const double2 *g) {
     return v;
 }
 __device__ __forceinline__ void bar() { asm volatile("bar.sync 0;" ::: "memory"); }
+__device__ __forceinline__ void pf_l2(const void *g) { asm volatile("prefetch.global.L2 [%0];" ::"l"(g)); }
 struct SRef {
     u32 a;
     __device__ __forceinline__ operator double2() const { return lds(a); }
@@ -586,13 +587,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     for (int i = 0; i < dev::kRegBits; i++)
                         if ((j >> i) & 1) rdj |= 1u << ph.front().R[i];
                     if (rdj & a.zload) continue;
-                    k << " asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(g + " << u64s(16 * phys_slot(ph.front(), j)) << "));";
+                    k << " pf_l2(g + " << u64s(16 * phys_slot(ph.front(), j)) << ");";
                 }
                 k << " }\n";
             } else {
                 k << "      for (u32 u = threadIdx.x * 8u; u < NT; u += " << 8 * NTHR << "u) "
                   << (a.zload ? "if (!(u & " + std::to_string(a.zload) + "u)) " : std::string())
-                  << "asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"(psi + addr(nb, u)));\n";
+                  << "pf_l2(psi + addr(nb, u));\n";
             }
             k << "    }\n";
         }

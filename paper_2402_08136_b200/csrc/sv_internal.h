@@ -77,6 +77,7 @@ void jacobi_eigh(int N, std::vector<double> A, std::vector<double> &lam, std::ve
 struct FuseOptions {
     int kmax = 4;          // dense/controlled target cap after fusion (0 = none)
     int diag_kmax = 10;    // diagonal width cap
+    int mode = 0;          // 0: greedy structure-preserving window (B200 mode); 1: the paper's Fig. 4 fusion
 };
 std::vector<Gate> fuse(const std::vector<Gate> &in, const FuseOptions &o);
 // cur <- nx * cur for two diagonal ops when their union has <= diag_kmax qubits (else false).
@@ -152,6 +153,9 @@ struct CompileOptions {
     // device, no uploads, no launches) and appends one line per launch to *dry_log
     bool dry_run = false;
     std::string *dry_log = nullptr;
+    // dry run only: also export the program for host emulation into this directory (blob.bin,
+    // launches.txt, src_<i>.cu = generated pass source without the device prelude, cw_<i>.bin)
+    std::string emu_dir;
 };
 
 // Schedule: logical fused ops (+ optional product init) -> physical steps.

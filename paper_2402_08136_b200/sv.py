@@ -43,7 +43,7 @@ class sv_gate(ctypes.Structure):
 
 class sv_fuse_options(ctypes.Structure):
     _fields_ = [("fusion_kmax", ctypes.c_int), ("diag_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
-                ("tile_jit", ctypes.c_int)]
+                ("tile_jit", ctypes.c_int), ("fusion_mode", ctypes.c_int)]
 
 
 class sv_plan_report(ctypes.Structure):
@@ -55,7 +55,8 @@ class hhl_options(ctypes.Structure):
     _fields_ = [("clock_qubits", ctypes.c_int), ("fusion_kmax", ctypes.c_int), ("tile_qubits", ctypes.c_int),
                 ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("tile_jit", ctypes.c_int),
                 ("diag_kmax", ctypes.c_int), ("qpe_mode", ctypes.c_int),
-                ("eig_lambda", ctypes.POINTER(ctypes.c_double)), ("eig_vectors", ctypes.POINTER(ctypes.c_double))]
+                ("eig_lambda", ctypes.POINTER(ctypes.c_double)), ("eig_vectors", ctypes.POINTER(ctypes.c_double)),
+                ("fusion_mode", ctypes.c_int)]
 
 
 class hhl_report(ctypes.Structure):
@@ -184,8 +185,8 @@ class _GateArray:
         self.n = len(gates)
 
 
-def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0, tile_jit=0):
-    return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits), int(tile_jit))
+def _fuse_opts(fusion_kmax=0, diag_kmax=0, tile_qubits=0, tile_jit=0, fusion_mode=0):
+    return sv_fuse_options(int(fusion_kmax), int(diag_kmax), int(tile_qubits), int(tile_jit), int(fusion_mode))
 
 
 def trim_memory(device: int = -1):
@@ -261,9 +262,9 @@ class State:
         ga = _GateArray(gates)
         _check(load().sv_apply_fused(self._h, ga.arr, ga.n))
 
-    def apply_circuit(self, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0) -> dict:
+    def apply_circuit(self, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0, fusion_mode=0) -> dict:
         ga = _GateArray(gates)
-        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit, fusion_mode)
         rep = sv_plan_report()
         _check(load().sv_apply_circuit(self._h, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(rep)))
         return {f: getattr(rep, f) for f, _ in rep._fields_}
@@ -306,9 +307,9 @@ class Program:
         self.report = report
 
     @classmethod
-    def create(cls, state: State, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0):
+    def create(cls, state: State, gates, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0, fusion_mode=0):
         ga = _GateArray(gates)
-        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
+        o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit, fusion_mode)
         h = ctypes.c_void_p()
         rep = sv_plan_report()
         _check(load().sv_program_create(state.handle, ga.arr, ga.n, ctypes.byref(o), ctypes.byref(h),
@@ -361,11 +362,12 @@ class Program:
 STEP_KINDS = ["init_zero", "init_product", "dense", "diagonal", "recip_ry", "tile", "exchange"]
 
 
-def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0):
+def schedule_dump(n_qubits: int, gates, world: int = 1, fusion_kmax=4, diag_kmax=0, tile_qubits=0, tile_jit=0,
+                  fusion_mode=0):
     """Host-only: fuse + schedule a logical gate list (no GPU needed). Returns (text, report).
     tile_jit=1 also generates and NVRTC-compiles (sm_100a) every tile pass."""
     ga = _GateArray(gates)
-    o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit)
+    o = _fuse_opts(fusion_kmax, diag_kmax, tile_qubits, tile_jit, fusion_mode)
     buf = ctypes.create_string_buffer(1 << 22)
     rep = sv_plan_report()
     _check(load().sv_schedule_dump(int(n_qubits), int(world), ga.arr, ga.n, ctypes.byref(o), buf, len(buf),
@@ -377,9 +379,10 @@ class _Opts:
     """hhl_options plus the buffers its eig_* pointers reference (kept alive with it)."""
 
     def __init__(self, clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0,
-                 diag_kmax=0, qpe_mode=0, eig=None):
+                 diag_kmax=0, qpe_mode=0, eig=None, fusion_mode=0):
         self.o = hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap),
                              int(init_fold), int(tile_jit), int(diag_kmax), int(qpe_mode))
+        self.o.fusion_mode = int(fusion_mode)
         if eig is not None:          # (lambda, V): caller-supplied eigendecomposition of the padded A
             self.lam = np.ascontiguousarray(eig[0], dtype=np.float64)
             self.V = np.ascontiguousarray(eig[1], dtype=np.float64)

@@ -211,3 +211,21 @@ def test_eig_option_host_checks_and_same_kernels():
     t2, r2 = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, eig=(p.lam, p.V), **configs.BENCH_OPTS)
     assert t1 == t2 and "JIT_PASS" in t1
     assert abs(r1["b_norm"] - float(np.linalg.norm(b))) < 1e-12 * r1["b_norm"] and r1["n_orig"] == 13
+
+
+def test_paper_mode_fusion_counts():
+    """Fig. 4 fusion (fusion_mode = 1) on the transpiled 2x2 HHL stream (C1 rewritten to
+    1q + CNOT): fewer fused gates than the sequential k <= 2 window, and a reduction of
+    the same order as the paper's 210 -> 67. Host-only planner."""
+    from oracle import hhl as ohhl
+    from oracle import transpile as tr
+    from workloads import configs
+    A, b, nc = configs.get("C1")
+    p = ohhl.plan(A, b, nc)
+    t = tr.transpile(ohhl.build(p))
+    _, rp = pkg.schedule_dump(p.n, t, fusion_mode=1, tile_qubits=-1)
+    _, r2 = pkg.schedule_dump(p.n, t, fusion_kmax=2, tile_qubits=-1)
+    assert rp["n_logical"] == len(t) == 101
+    assert rp["n_fused"] <= r2["n_fused"] and rp["n_fused"] <= len(t) / 3
+    with pytest.raises(pkg.SVError):
+        pkg.schedule_dump(p.n, t, fusion_mode=3)

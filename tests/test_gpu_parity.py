@@ -351,3 +351,18 @@ def test_jit_small_tiles_wide_ops(kinds, T):
         psi0 = synthetic.random_state(n, seed)
         got, ref, _ = run_both(n, gates, psi0, fusion_kmax=2, tile_qubits=T, tile_jit=1)
         assert np.abs(got - ref).max() < 1e-10, (seed, np.abs(got - ref).max())
+
+
+@pytest.mark.parametrize("mode", [dict(tile_qubits=-1), dict(tile_qubits=8, tile_jit=1), dict(tile_qubits=8, tile_jit=-1)])
+def test_paper_mode_fusion_transpiled_hhl(mode):
+    """Fig. 4 fusion (fusion_mode = 1) on the transpiled 2x2 HHL stream:
+    GPU state vs the oracle's unfused run, and the HHL post-selection of the 5-qubit register."""
+    from oracle import transpile as tr
+    A, b, nc = configs.get("C1")
+    xo, po, psi_o, p = ohhl.solve(A, b, nc)
+    t = tr.transpile(p.gates)
+    for n in (p.n, 10):
+        got, ref, st = run_both(n, t, None, fusion_mode=1, **mode)
+        assert np.abs(got - ref).max() < 1e-10
+    got5, _, _ = run_both(p.n, t, None, fusion_mode=1, **mode)
+    assert np.abs(got5 - psi_o).max() < 1e-10

@@ -324,3 +324,36 @@ def test_hermitian_embedding_random():
     xt = np.linalg.solve(A, b)
     errs = [np.linalg.norm(hhl.solve(A, b, nc)[0] - xt) / np.linalg.norm(xt) for nc in (6, 8, 10)]
     assert errs[0] > errs[2] and errs[2] < 5e-3
+
+
+@pytest.mark.parametrize("name", ["C1"])
+def test_transpiled_hhl_stream_equals_logical(name):
+    """oracle/transpile.py: the one-qubit + CNOT rewriting of the HHL list (PAPER.md:68's transpiled
+    form) is exact: same final state as the logical list (no dropped global phase), CNOTs and 1q only."""
+    from oracle import transpile as tr
+    A, b, nc = configs.get(name)
+    p = hhl.plan(A, b, nc)
+    g = hhl.build(p)
+    t = tr.transpile(g)
+    one, two = tr.counts(t)
+    assert one + two == len(t) and two > 0
+    assert all(len(x["targets"]) + len(x.get("controls", [])) <= 2 for x in t)
+    assert np.abs(sim.run(g, p.n) - sim.run(t, p.n)).max() < 1e-12
+
+
+def test_multiplexed_ry_bruteforce():
+    """Gray-code uniformly-controlled RY vs the direct multiplexed matrix (random angles, 3 controls)."""
+    from oracle import transpile as tr
+    g = synthetic.rng(9)
+    th = g.uniform(-3, 3, 8)
+    n = 4
+    psi0 = synthetic.random_state(n, 2)
+    ref = psi0.copy()
+    for i in range(1 << n):
+        if (i >> 3) & 1:
+            continue
+        m = i & 7
+        c, s = np.cos(th[m] / 2), np.sin(th[m] / 2)
+        a0, a1 = ref[i], ref[i | 8]
+        ref[i], ref[i | 8] = c * a0 - s * a1, s * a0 + c * a1
+    assert np.abs(sim.run(tr.multiplexed_ry([0, 1, 2], 3, th), n, psi0) - ref).max() < 1e-13
