@@ -274,9 +274,23 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             cstage.clear();
             ctot = 0;
         }
+        // small (1-, 2-qubit) dense matrices too, while space remains: their entries become constant-bank
+        // DFMA operands instead of 2^2k preloaded registers (a pass of many 2-qubit ops -- Fig. 4 fused
+        // transpiled streams -- otherwise spills kilobytes of registers)
+        for (size_t i = 0; i < ops.size(); i++) {
+            const auto &op = ops[i];
+            const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
+            if (op.kind == 0 && Kk >= 1 && Kk <= 2 && ctot + ((size_t)1 << (2 * Kk)) <= 2040) {
+                cstage[(int)i] = ctot;
+                ctot += (size_t)1 << (2 * Kk);
+            }
+        }
         cwide->clear();
-        for (auto &kv : cstage) {
-            const auto &op = ops[kv.first];
+        std::vector<std::pair<size_t, int>> by_off;      // cw[] layout order = assigned offsets
+        for (auto &kv : cstage) by_off.push_back({kv.second, kv.first});
+        std::sort(by_off.begin(), by_off.end());
+        for (auto &e : by_off) {
+            const auto &op = ops[e.second];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
             cwide->push_back({op.data_off, (uint64_t)1 << (2 * Kk)});
         }
@@ -425,7 +439,12 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
                             dsub_max * 16;
     if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
-    int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 512 / NTHR));
+    // resident CTAs per SM for __launch_bounds__: limited by shared memory, and by registers -- 128 per
+    // thread for the 16 register amplitudes, allocated per WARP (a CTA smaller than a warp still takes
+    // a whole warp): 65536 / (128 x 32) = 16 warps per SM. (Counting threads instead of warps gave a
+    // 16-thread CTA a 64-register cap, an 11 KB spill stack and, at ptxas -O3, wrong amplitudes.)
+    const int cta_warps = (NTHR + 31) / 32;
+    int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 16 / cta_warps));
     // Direct global I/O: when a phase's thread bits start with the tile's positions 0..2 and those are
     // the physical bits 0..2 (8 lanes cover 128 contiguous bytes), the first phase loads its 16
     // register amplitudes straight from HBM and the last phase stores them straight back; the tile
@@ -723,7 +742,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 const int D = 1 << K;
                 const bool real = op.is_signed != 0;
                 k << "        const double2 *U = blob + " << op.data_off << "ull;\n";
-                if (K <= 2)
+                const auto csK = cstage.find(oi);          // small matrix in the constant bank?
+                if (K <= 2 && csK == cstage.end())
                     for (int i = 0; i < D * D; i++) k << "        const double2 u" << i << " = __ldg(U + " << i << ");\n";
                 for (int g = 0; g < 16; g++) {
                     if (g & M) continue;
@@ -853,8 +873,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     for (int r = 0; r < D; r++) {
                         k << "          { double ax = 0.0, ay = 0.0;";
                         for (int cc = 0; cc < D; cc++) {
-                            std::string u = K <= 2 ? ("u" + std::to_string(r * D + cc))
-                                                   : ("__ldg(U + " + std::to_string(r * D + cc) + ")");
+                            std::string u = (K <= 2 && csK != cstage.end())
+                                                ? ("cwa.w[" + std::to_string(csK->second + (size_t)r * D + cc) + "]")
+                                            : K <= 2 ? ("u" + std::to_string(r * D + cc))
+                                                     : ("__ldg(U + " + std::to_string(r * D + cc) + ")");
                             if (real) {
                                 k << " ax = fma(" << u << ".x, i" << cc << ".x, ax); ay = fma(" << u << ".x, i" << cc
                                   << ".y, ay);";

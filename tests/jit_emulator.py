@@ -247,7 +247,7 @@ def build_pass(src: str) -> str:
         cpp = exe + ".cpp"
         with open(cpp, "w") as f:
             f.write(full)
-        subprocess.check_call(["g++", "-std=c++20", "-O1", "-g", "-ffp-contract=off", "-fsanitize=address",
+        subprocess.check_call(["g++", "-std=c++20", "-O1", "-g", "-ffp-contract=off", "-fsanitize=address,undefined",
                                "-fno-omit-frame-pointer", "-pthread", cpp, "-o", exe + ".tmp"])
         os.replace(exe + ".tmp", exe)
     return exe

@@ -366,3 +366,40 @@ def test_paper_mode_fusion_transpiled_hhl(mode):
         assert np.abs(got - ref).max() < 1e-10
     got5, _, _ = run_both(p.n, t, None, fusion_mode=1, **mode)
     assert np.abs(got5 - psi_o).max() < 1e-10
+
+
+@pytest.mark.parametrize("n,sampled", [(22, False), (30, True)])
+def test_padded_stress_circuit_tensor_factor(n, sampled):
+    """SURVEY §8(d) padded stress circuits P_n: C3's 15-qubit textbook HHL list on a seeded random
+    injective qubit map + brickwork pad layers. Tensor-factor pin: psi = perm(psi_HHL15 (x) psi_pad),
+    both factors from the small oracle runs. P22: every amplitude; P30 (16 GiB): 256 random
+    amplitudes plus the HHL factor's post-selection slice (pad factor at its first basis state)."""
+    A, b, nc = configs.get("C3")
+    p = ohhl.plan(A, b, nc)
+    g15 = ohhl.build(p)
+    gates, qmap, pad = synthetic.padded_circuit(g15, p.n, n)
+    psi15 = sim.run(g15, p.n)
+    psipad = sim.run(synthetic.pad_brickwork(list(range(n - p.n))), n - p.n)
+    st = pkg.State(n)
+    prog = pkg.Program.create(st, gates, fusion_kmax=2, tile_qubits=12)
+    prog.run()
+    if not sampled:
+        idx = np.arange(1 << n)
+        got = st.read()
+    else:
+        g = synthetic.rng(n)
+        idx = np.unique(g.integers(0, 1 << n, 1 << 17))
+        got = np.concatenate([st.read(int(i), 1) for i in idx[:256]])
+        idx = idx[:256]
+        # the HHL factor's post-selected slice with the pad factor at its first basis state
+        base = 1 << (p.n - 1)
+        sl = np.arange(base, base + (1 << p.n_b))
+        full_sl = np.zeros(sl.size, dtype=np.int64)
+        for j, q in enumerate(qmap):
+            full_sl |= ((sl >> j) & 1) << q
+        idx = np.concatenate([idx, full_sl])
+        got = np.concatenate([got, [st.read(int(i), 1)[0] for i in full_sl]])
+    ref = synthetic.tensor_factor_amplitudes(psi15, qmap, psipad, pad, idx)
+    err = float(np.abs(got - ref).max())
+    print(f"\n[parity] P{n} padded stress circuit ({len(gates)} gates): max|psi - tensor factors| = {err:.3e}")
+    assert err < 1e-10

@@ -83,3 +83,49 @@ def basis_circuit(width: int, n_gates: int, seed: int) -> list:
         else:
             out.append({"kind": "dense", "targets": [int(g.integers(width))], "data": haar_unitary(1, g)})
     return out
+
+
+def pad_brickwork(pad_qubits, layers: int = 8, seed: int = 2402) -> list:
+    """SURVEY §8(d) padded stress circuits, the pad part: `layers` brickwork layers on the pad qubits,
+    each a Haar U(2) on every pad qubit (QR of a complex Gaussian) then CZ on alternating neighbouring
+    pairs (offset 0 on even layers, 1 on odd layers)."""
+    g = rng(seed)
+    cz = np.array([1, 1, 1, -1], dtype=complex)
+    out = []
+    for layer in range(layers):
+        for q in pad_qubits:
+            out.append({"kind": "dense", "targets": [int(q)], "data": haar_unitary(1, g)})
+        for i in range(layer % 2, len(pad_qubits) - 1, 2):
+            out.append({"kind": "diagonal", "targets": [int(pad_qubits[i]), int(pad_qubits[i + 1])], "data": cz.copy()})
+    return out
+
+
+def padded_circuit(gates15: list, n15: int, n: int, layers: int = 8):
+    """P_n stress circuit: the n15-qubit gate list placed on a seeded random injective map
+    of its qubits into n physical qubits (seed 2402 + n), plus brickwork layers on the n - n15 pad
+    qubits. Returns (gates, qubit_map, pad_qubits): circuit qubit q of the small list -> qubit_map[q].
+    Its final state is the tensor product of the two factors' states, permuted (the tensor-factor pin)."""
+    g = rng(2402 + n)
+    perm = [int(x) for x in g.permutation(n)]
+    qmap = perm[:n15]
+    pad = sorted(perm[n15:])
+
+    def remap(x):
+        y = dict(x)
+        y["targets"] = [qmap[q] for q in x["targets"]]
+        if "controls" in x:
+            y["controls"] = [qmap[q] for q in x["controls"]]
+        return y
+    return [remap(x) for x in gates15] + pad_brickwork(pad, layers), qmap, pad
+
+
+def tensor_factor_amplitudes(psi_small: np.ndarray, qmap, psi_pad: np.ndarray, pad, idx) -> np.ndarray:
+    """psi_full[i] = psi_small[bits of i at qmap] * psi_pad[bits of i at pad] (layout bookkeeping only)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    a = np.zeros_like(idx)
+    for j, q in enumerate(qmap):
+        a |= ((idx >> q) & 1) << j
+    b = np.zeros_like(idx)
+    for j, q in enumerate(pad):
+        b |= ((idx >> q) & 1) << j
+    return psi_small[a] * psi_pad[b]
