@@ -399,13 +399,10 @@ static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost
     return co;
 }
 
-static sv_program *build_hhl(sv_state *sv, const double *A, const double *b, int N, const hhl_options *opt,
-                             hhl_report *rep) {
-    const double t0 = now_s();
+static sv_program *build_hhl(sv_state *sv, const HHLPlanHost &p, const hhl_options *opt, hhl_report *rep,
+                             double t0) {
     prof_mark("build_hhl start");
-    HHLPlanHost p = plan_of(A, b, N, opt);
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
-    prof_mark("hhl_plan");
     std::vector<ProductFactor> factors;
     size_t n_logical = 0;
     std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
@@ -432,7 +429,8 @@ sv_status hhl_build_program(sv_state *sv, const double *A, const double *b, int 
     return guard([&] {
         if (!sv || !out) fail(SV_E_ARG, "null argument");
         *out = nullptr;
-        *out = build_hhl(sv, A, b, N, opt, rep);
+        const double t0 = now_s();
+        *out = build_hhl(sv, plan_of(A, b, N, opt), opt, rep, t0);
     });
 }
 
@@ -533,14 +531,17 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         if (clock_qubits > 0) o.clock_qubits = clock_qubits;
         if (!opt) o.recip_snap = -1.0;
         prof_mark("hhl_solve start");
+        const double tf0 = now_s();
         HHLPlanHost p = plan_of(A, b, N, &o);
+        const double t_plan = now_s() - tf0;
+        prof_mark("hhl_plan");
         // the HHL program starts with its own initialisation step: no |0...0> fill needed
         sv_state *sv = state_create(p.n, dist, (cudaStream_t)cuda_stream, false);
         prof_mark("state_create");
         sv_program *prog = nullptr;
         try {
             hhl_report r{};
-            prog = build_hhl(sv, A, b, N, &o, &r);
+            prog = build_hhl(sv, p, &o, &r, now_s() - t_plan);      // front end = plan + build
             const double t0 = now_s();
             program_run(sv, prog);
             if (prof_on()) {

@@ -315,11 +315,13 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
         s.n_passes++;
     }
     const int T = std::min(o.tile_qubits, nloc);
-    const bool tiles = o.tile_qubits > 0 && nloc >= o.reg_bits + 3;
+    // register bits per phase: o.reg_bits (3 or 4) by default; a pass holding a 4-target op uses 4
+    const int RMAX = 4;
+    const bool tiles = o.tile_qubits > 0 && nloc >= RMAX + 3;
     int wmin_opt = o.wmin;   // default 3 (128-byte segments): more tile bits for op targets per pass
     if (jit_config().wmin != 3) wmin_opt = jit_config().wmin;     // developer experiments (HHLSV_JIT=wmin=..)
-    const int wmin = std::min(wmin_opt, T - o.reg_bits);
-    const int R = o.reg_bits;
+    const int wmin = std::min(wmin_opt, T - RMAX);
+    const int R = RMAX;                 // widest op a tile pass can hold in registers
     // single-rank tile schedules: commutation-aware reordering for packing (multi-rank keeps the
     // input order so exchanges follow the circuit)
     const bool reorder = tiles && o.reorder;
@@ -346,8 +348,13 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
             if (std::find(set.begin(), set.end(), b) == set.end()) set.push_back(b);
         std::sort(set.begin(), set.end());
         tile.tile_bits = set;
-        // register phases: each phase's ops have their nd targets inside R (|R| <= reg_bits)
-        phase_schedule(tile.tile_ops, R, tile.phase_R, tile.phase_start);
+        // register phases: each phase's ops have their nd targets inside R (|R| <= reg_bits); the
+        // pass uses the default count unless one of its ops is wider
+        int Rp = std::max(1, std::min(o.reg_bits, RMAX));
+        for (const Gate &g : tile.tile_ops)
+            if (g.kind == Kind::Dense || g.kind == Kind::Controlled) Rp = std::max(Rp, (int)g.targets.size());
+        tile.reg_bits = Rp;
+        phase_schedule(tile.tile_ops, Rp, tile.phase_R, tile.phase_start);
         const int dm = jit_config().diag_merge >= 0 ? jit_config().diag_merge : o.diag_merge;
         if (dm > 0) merge_phase_diagonals(tile, dm);
         // Fill each phase's register set up to R bits with the highest tile bits (lanes keep the
@@ -366,7 +373,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
                 cand.push_back({cost, -b});
             }
             std::sort(cand.begin(), cand.end());
-            for (size_t i = 0; (int)rr.size() < R && i < cand.size(); i++) rr.push_back(-cand[i].second);
+            for (size_t i = 0; (int)rr.size() < Rp && i < cand.size(); i++) rr.push_back(-cand[i].second);
             std::sort(rr.begin(), rr.end());
         }
         tile.bytes = 32.0 * local_amps;
@@ -520,7 +527,8 @@ std::string dump_schedule(const Schedule &s) {
             case StepKind::Exchange: os << "EXCHANGE global=" << bits(st.xg) << " local=" << bits(st.xl) << "\n"; break;
             case StepKind::Tile: {
                 os << "TILE bits=" << bits(st.tile_bits) << " ops=" << st.tile_ops.size() << " phases="
-                   << st.phase_R.size() << "\n";
+                   << st.phase_R.size() << (st.reg_bits != 4 ? " regbits=" + std::to_string(st.reg_bits) : std::string())
+                   << "\n";
                 for (size_t oi = 0; oi < st.tile_ops.size(); oi++) {
                     const Gate &g = st.tile_ops[oi];
                     for (size_t p = 0; p < st.phase_R.size(); p++)

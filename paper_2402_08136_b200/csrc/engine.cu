@@ -528,7 +528,7 @@ void lower_tile_step(const Step &st, dev::TileArgs &a, std::vector<double2> &blo
         const std::vector<int> &Rp = st.phase_R[pi];   // physical bits, ascending
         std::vector<int> Rt;                            // tile positions
         for (int b : Rp) Rt.push_back(index_in(st.tile_bits, b));
-        for (int i = 0; i < dev::kRegBits; i++) ph.R[i] = Rt[i];
+        for (int i = 0; i < dev::kRegBits; i++) ph.R[i] = i < st.reg_bits ? Rt[i] : -1;
         int nt = 0;
         for (int tp = 0; tp < a.T; tp++)
             if (std::find(Rt.begin(), Rt.end(), tp) == Rt.end()) ph.tpos[nt++] = tp;
@@ -712,6 +712,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     CompileOptions c2 = co;
     if (c2.tile_qubits > 12) c2.tile_qubits = 12;
     const bool use_jit = co.jit > 0 || (co.jit == 0 && sv->nloc >= 18);
+    // 8-amplitude register phases (3 register bits) only in NVRTC passes; the interpreter has 16
+    c2.reg_bits = use_jit ? jit_config().reg_bits : 4;
     p->sched = compile(ops, init, sv->n, sv->nloc, p->phys_in, c2);
     prof_mark("  compile");
     const int nloc = sv->nloc;
@@ -909,6 +911,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 dev::TileArgs &a = rec.tile;
                 a.psi = sv->psi;
                 a.T = (int)st.tile_bits.size();
+                a.nreg = st.reg_bits;
                 for (int i = 0; i < a.T; i++) a.tbits[i] = st.tile_bits[i];
                 a.nskip = 0;
                 a.zload = a.zstore = 0;
@@ -942,6 +945,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
                     JitPass jp;
                     jp.name = "hhlsv_tile";
+                    jp.nthr = 1 << (a.T - a.nreg);
                     jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
                                              (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide, &blob);
                     for (auto &c : jp.cwide)
@@ -975,7 +979,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     wr("src_" + std::to_string(i) + ".cu", jp.src.data(), jp.src.size());
                     wr("cw_" + std::to_string(i) + ".bin", jp.cwvals.data(), jp.cwvals.size() * sizeof(double2));
                     snprintf(line, sizeof line, "TILE %zu %llu %d %llu %zu %d\n", i, (unsigned long long)r.tile.n_tiles,
-                             r.tile.T, (unsigned long long)r.tile.rank_base, jp.smem_extra, 1 << (r.tile.T - dev::kRegBits));
+                             r.tile.T, (unsigned long long)r.tile.rank_base, jp.smem_extra, 1 << (r.tile.T - r.tile.nreg));
                 } else if (r.skip) {
                     snprintf(line, sizeof line, "SKIP %zu %d\n", i, (int)r.kind);
                 } else {

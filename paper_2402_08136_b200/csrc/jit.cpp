@@ -225,6 +225,7 @@ const JitConfig &jit_config() {
             else if (key == "ctab") x.ctab = iv != 0;
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
+            else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "ru") x.ru = std::max(0, iv);
             else if (key == "clobber") x.smem_clobber = iv != 0;
             else if (key == "ptxas") x.ptxas_opt = "-Xptxas=" + val;
@@ -250,7 +251,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                             std::vector<std::pair<uint64_t, uint64_t>> *cwide, const std::vector<double2> *hblob) {
     const JitConfig &cfg = jit_config();
     const int T = a.T;
-    const int NTHR = 1 << (T - dev::kRegBits);
+    const int RB = a.nreg, RA = 1 << RB;      // register bits / amplitudes per thread in a phase
+    const int NTHR = 1 << (T - RB);
     const int SA = (T + 1) / 2, SB = T - SA;
     int wide_ops = 0;          // dense ops with >= 3 targets: unrolled when few, rolled (bounded code) when many
     for (auto &op : ops)
@@ -316,7 +318,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     std::vector<size_t> used_ph;
     auto op_vary = [&](const dev::RegOp &op, const dev::RegPhase &P) {
         std::vector<int> v;
-        for (int i = 0; i < 4; i++)
+        for (int i = 0; i < RB; i++)
             if (op.ridx[1 << i]) v.push_back(P.R[i]);
         for (int r = 0; r < op.ntr; r++)
             for (int l = 0; l < op.t_len[r]; l++) v.push_back(op.t_src[r] + l);
@@ -349,7 +351,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             if (ops[oi].kind != 2 || !cfg.rtab) continue;
             std::vector<int> V = op_vary(ops[oi], ph[p]);
             std::sort(V.begin(), V.end());
-            if (V.size() <= 9 && (1u << V.size()) <= 2u * (1u << (T - dev::kRegBits))) {
+            if (V.size() <= 9 && (1u << V.size()) <= 2u * (1u << (T - RB))) {
                 rtabs.push_back({(int)p, oi, oi + 1, V, used});
                 used += (size_t)1 << V.size();
             }
@@ -379,7 +381,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             const auto tbv = tbits_of(op);
             if (tbv.size() > 2) continue;
             std::map<uint32_t, size_t> ent;
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < RA; j++) {
                 if ((j & op.rcm) != op.rcv) continue;
                 for (uint32_t c = 0; c < (1u << tbv.size()); c++) {
                     uint32_t idx = op.ridx[j];
@@ -444,7 +446,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // a whole warp): 65536 / (128 x 32) = 16 warps per SM. (Counting threads instead of warps gave a
     // 16-thread CTA a 64-register cap, an 11 KB spill stack and, at ptxas -O3, wrong amplitudes.)
     const int cta_warps = (NTHR + 31) / 32;
-    int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 16 / cta_warps));
+    const int reg_target = RB >= 4 ? 128 : 64;      // 16 or 8 register amplitudes per thread
+    int min_blocks = std::max(1, std::min((int)((227 * 1024) / smem_cta), 65536 / (reg_target * 32 * cta_warps)));
     // Direct global I/O: when a phase's thread bits start with the tile's positions 0..2 and those are
     // the physical bits 0..2 (8 lanes cover 128 contiguous bytes), the first phase loads its 16
     // register amplitudes straight from HBM and the last phase stores them straight back; the tile
@@ -463,12 +466,12 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     auto tb_expr = [&](const dev::RegPhase &P) {
         std::ostringstream o;
         o << "0u";
-        for (int i = 0; i < T - dev::kRegBits; i++) o << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
+        for (int i = 0; i < T - RB; i++) o << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
         return o.str();
     };
     auto phys_slot = [&](const dev::RegPhase &P, int j) {      // physical offset of register slot j
         uint64_t c = 0;
-        for (int i = 0; i < dev::kRegBits; i++)
+        for (int i = 0; i < RB; i++)
             if ((j >> i) & 1) c |= 1ull << a.tbits[P.R[i]];
         return c;
     };
@@ -534,7 +537,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 const dev::RegOp &op = ops[oi];
                 k << "        { const u64 ib = (" << runs_expr("gpre", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
                   << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
-                for (int i = 0; i < 4; i++)
+                for (int i = 0; i < RB; i++)
                     if (op.ridx[1 << i]) {
                         int ob = 0;
                         while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
@@ -553,7 +556,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (int i = 0; i < nv; i++) k << " | (((c >> " << i << ") & 1u) << " << rt.V[i] << ")";
             k << ";\n        const u64 m = (" << runs_expr("gpre", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
               << runs_expr("loc", op.ntr, op.t_src, op.t_len, op.t_dst) << ")";
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < RB; i++)
                 if (op.ridx[1 << i]) {
                     int ob = 0;
                     while (!((op.ridx[1 << i] >> ob) & 1u)) ob++;
@@ -596,14 +599,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
               << "ull * gridDim.x);\n";
             if (din) {       // known-zero slots (zload) are never read: not prefetched either
                 uint32_t rz0 = 0;
-                for (int i = 0; i < dev::kRegBits; i++) rz0 |= 1u << ph.front().R[i];
+                for (int i = 0; i < RB; i++) rz0 |= 1u << ph.front().R[i];
                 const bool thr_z = (a.zload & ~rz0) != 0;
                 k << "      if ((threadIdx.x & 7u) == 0u" << (thr_z ? " && !((" + tb_expr(ph.front()) + ") & " +
                                                                        std::to_string(a.zload) + "u)" : std::string())
                   << ") { const char *g = (const char *)(psi + (nb | pd_in));";
-                for (int j = 0; j < 16; j++) {
+                for (int j = 0; j < RA; j++) {
                     uint32_t rdj = 0;
-                    for (int i = 0; i < dev::kRegBits; i++)
+                    for (int i = 0; i < RB; i++)
                         if ((j >> i) & 1) rdj |= 1u << ph.front().R[i];
                     if (rdj & a.zload) continue;
                     k << " pf_l2(g + " << u64s(16 * phys_slot(ph.front(), j)) << ");";
@@ -651,15 +654,15 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     for (size_t p = 0; p < ph.size(); p++) {
         const dev::RegPhase &P = ph[p];
         k << "    { // phase " << p << "\n      const u32 tb = 0u";
-        for (int i = 0; i < T - dev::kRegBits; i++) k << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
+        for (int i = 0; i < T - RB; i++) k << " | (((threadIdx.x >> " << i << ") & 1u) << " << P.tpos[i] << ")";
         k << ";\n";
         // the swizzle is XOR-linear and tb / slot bits are disjoint: swz(tb | c) = swz(tb) ^ swz(c), so a
         // register slot's shared-memory index is one XOR with a codegen constant
         k << "      const u32 stb = swz(tb);\n";
         int rd[16];
-        for (int j = 0; j < 16; j++) {
+        for (int j = 0; j < RA; j++) {
             rd[j] = 0;
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < RB; i++)
                 if ((j >> i) & 1) rd[j] |= 1 << P.R[i];
         }
         if (!hoist) {
@@ -667,7 +670,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         }
 
         if (p == 0 && din && init) {
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < RA; j++) {
                 k << "      double2 v" << j << " = mk(0.0, 0.0);\n      { const u64 gi = gbase | pd_in | " << u64s(phys_slot(P, j))
                   << ";\n        if (!(gi & " << u64s(init->zero_mask) << ")) {\n";
                 for (size_t g = 0; g < init->off.size(); g++) {
@@ -691,7 +694,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
         } else if (p == 0 && din) {
             k << "      const double2 *gin = psi + (base | pd_in);\n";
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < RA; j++) {
                 // known-zero slots (zload) are not read: register part decided at codegen, thread part per thread
                 if ((uint32_t)rd[j] & a.zload) k << "      double2 v" << j << " = mk(0.0, 0.0);\n";
                 else if (a.zload)
@@ -700,7 +703,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 else k << "      double2 v" << j << " = ldcs_v(gin + " << u64s(phys_slot(P, j)) << ");\n";
             }
         } else {
-            for (int j = 0; j < 16; j++) k << "      double2 v" << j << " = " << sref(rd[j]) << ";\n";
+            for (int j = 0; j < RA; j++) k << "      double2 v" << j << " = " << sref(rd[j]) << ";\n";
         }
         // The last op of a last phase that stores through shared memory is a wide dense op without
         // controls: its rows are written to their final shared-memory slots, so neither the register
@@ -725,11 +728,11 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      " << (c.empty() ? "{" : "if (" + c + ") {") << " // op " << oi << "\n";
             if (op.kind == 3) {          // deferred global scale
                 k << "        const double sc = __ldg(&blob[" << op.data_off << "ull].x);\n";
-                for (int j = 0; j < 16; j++) k << "        v" << j << " = mk(v" << j << ".x * sc, v" << j << ".y * sc);\n";
+                for (int j = 0; j < RA; j++) k << "        v" << j << " = mk(v" << j << ".x * sc, v" << j << ".y * sc);\n";
             } else if (op.kind == 4) {   // unscaled butterfly (Hadamard-like gate)
                 int A = 0;
                 while (!((op.mask >> A) & 1)) A++;
-                for (int j = 0; j < 16; j++) {
+                for (int j = 0; j < RA; j++) {
                     if ((j >> A) & 1) continue;
                     const int j1 = j | (1 << A);
                     k << "        { const double2 x0 = v" << j << ", x1 = v" << j1 << "; v" << j
@@ -745,7 +748,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 const auto csK = cstage.find(oi);          // small matrix in the constant bank?
                 if (K <= 2 && csK == cstage.end())
                     for (int i = 0; i < D * D; i++) k << "        const double2 u" << i << " = __ldg(U + " << i << ");\n";
-                for (int g = 0; g < 16; g++) {
+                for (int g = 0; g < RA; g++) {
                     if (g & M) continue;
                     if ((g & op.rcm) != op.rcv) continue;
                     if (K >= 3) {
@@ -894,10 +897,10 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 k << "        const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
                   << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
                 if (op.kind == 1) {
-                    for (int j = 0; j < 16; j++)
+                    for (int j = 0; j < RA; j++)
                         if ((j & op.rcm) == op.rcv)
                             k << "        const double2 d" << j << " = " << dval(oi, op.ridx[j], "ib") << ";\n";
-                    for (int j = 0; j < 16; j++)
+                    for (int j = 0; j < RA; j++)
                         if ((j & op.rcm) == op.rcv) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
                 } else {
                     int A = 0;
@@ -909,7 +912,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     else {
                         k << "        const u32 bt = 0u";
                         for (size_t i = 0; i < rt->V.size(); i++)
-                            if (std::find(P.R, P.R + 4, rt->V[i]) == P.R + 4)
+                            if (std::find(P.R, P.R + RB, rt->V[i]) == P.R + RB)
                                 k << " | (((tb >> " << rt->V[i] << ") & 1u) << " << i << ")";
                         k << ";\n";
                     }
@@ -917,7 +920,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     // (once per thread when no clock bit is a register bit), or one lookup in the
                     // tile's precomputed (s, c) table
                     std::map<uint32_t, int> sc;
-                    for (int j = 0; j < 16; j++) {
+                    for (int j = 0; j < RA; j++) {
                         if ((j >> A) & 1) continue;
                         if (sc.count(op.ridx[j])) continue;
                         const int id = (int)sc.size();
@@ -925,7 +928,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                         if (rt) {
                             int cj = 0;
                             for (size_t i = 0; i < rt->V.size(); i++)
-                                for (int r = 0; r < 4; r++)
+                                for (int r = 0; r < RB; r++)
                                     if (P.R[r] == rt->V[i] && ((j >> r) & 1)) cj |= 1 << i;
                             k << "        const double2 sc" << id << " = dsub[" << rt->off << " + (bt | " << cj
                               << "u)]; const double s" << id << " = sc" << id << ".x, c" << id << " = sc" << id << ".y;\n";
@@ -935,7 +938,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                               << ", s" << id << ", 1.0));\n";
                         }
                     }
-                    for (int j = 0; j < 16; j++) {
+                    for (int j = 0; j < RA; j++) {
                         if ((j >> A) & 1) continue;
                         const int j1 = j | (1 << A);
                         const std::string s = "s" + std::to_string(sc[op.ridx[j]]);
@@ -974,7 +977,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                   << ") | (" << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
                 uint32_t m = 0;
                 std::vector<uint32_t> rs;
-                for (int j = 0; j < 16; j++)
+                for (int j = 0; j < RA; j++)
                     if ((j & op.rcm) == op.rcv) {
                         m |= 1u << j;
                         if (std::find(rs.begin(), rs.end(), op.ridx[j]) == rs.end()) rs.push_back(op.ridx[j]);
@@ -997,13 +1000,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     else k << "        " << U << " = cmul(" << U << ", " << ld << ");\n";
                     first = false;
                 }
-                for (int j = 0; j < 16; j++)
+                for (int j = 0; j < RA; j++)
                     if ((kv.first >> j) & 1u) fac[j].push_back(U);
             }
             for (int oi : var) {
                 const dev::RegOp &op = ops[oi];
                 std::map<uint32_t, std::string> sym;
-                for (int j = 0; j < 16; j++) {
+                for (int j = 0; j < RA; j++) {
                     if ((j & op.rcm) != op.rcv) continue;
                     auto it = sym.find(op.ridx[j]);
                     if (it == sym.end()) {
@@ -1019,7 +1022,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             std::map<std::vector<std::string>, std::string> prod;
             int nf = 0;
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < RA; j++) {
                 if (fac[j].empty()) continue;
                 std::string f = fac[j][0];
                 for (size_t q = 1; q < fac[j].size(); q++) {
@@ -1046,17 +1049,17 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     const int nv = (int)run->V.size();
                     k << "      { const u32 bt = 0u";
                     for (int i = 0; i < nv; i++)
-                        if (std::find(P.R, P.R + 4, run->V[i]) == P.R + 4)
+                        if (std::find(P.R, P.R + RB, run->V[i]) == P.R + RB)
                             k << " | (((tb >> " << run->V[i] << ") & 1u) << " << i << ")";
                     k << "; // diagonal run of " << (run->b - run->a) << " ops\n";
-                    for (int j = 0; j < 16; j++) {
+                    for (int j = 0; j < RA; j++) {
                         bool touched = false;      // slots outside every op's register controls keep factor 1
                         for (int q = run->a; q < run->b; q++)
                             if ((j & ops[q].rcm) == ops[q].rcv) touched = true;
                         if (!touched) continue;
                         int cj = 0;
                         for (int i = 0; i < nv; i++)
-                            for (int r = 0; r < 4; r++)
+                            for (int r = 0; r < RB; r++)
                                 if (P.R[r] == run->V[i] && ((j >> r) & 1)) cj |= 1 << i;
                         k << "        v" << j << " = cmul(dsub[" << run->off << " + (bt | " << cj << "u)], v" << j << ");\n";
                     }
@@ -1096,7 +1099,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < RA; j++) {
                 if ((uint32_t)rd[j] & a.zstore) continue;          // still known zero: not written
                 k << "      " << (a.zstore ? "if (!(tb & " + std::to_string(a.zstore) + "u)) " : std::string())
                   << "__stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
@@ -1105,7 +1108,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "    }\n";
         } else {
             if (!tail_in_smem)
-                for (int j = 0; j < 16; j++) k << "      " << sref(rd[j]) << " = v" << j << ";\n";
+                for (int j = 0; j < RA; j++) k << "      " << sref(rd[j]) << " = v" << j << ";\n";
             hoisted();
             k << "      bar();\n    }\n";
         }
@@ -1259,7 +1262,7 @@ size_t jit_smem_bytes(int T, size_t total) {
 
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
                        int T, cudaStream_t s) {
-    const int threads = 1 << (T - dev::kRegBits);
+    const int threads = p.nthr;
     const size_t smem = jit_smem_bytes(T, p.smem_extra);
     const void *f = reinterpret_cast<const void *>(p.kern);
     cudaError_t e = cudaSuccess;

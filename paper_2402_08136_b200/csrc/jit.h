@@ -14,6 +14,7 @@ struct JitPass {
     std::string src;
     cudaKernel_t kern = nullptr;
     size_t smem_extra = 0;     // total dynamic shared memory of the generated kernel (bytes)
+    int nthr = 256;            // threads per CTA = 2^(T - register bits)
     // wide (>= 3-target) dense matrices read as constant-bank operands: (blob offset, entries) in
     // the order of the kernel's by-value parameter cwa (<= 32 KB of kernel parameters: per-launch,
     // hence coherent even when passes with identical structure share one cached module), and the
@@ -48,6 +49,7 @@ struct JitConfig {
     bool ctab = true;         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
+    int reg_bits = 4;         // rb: register bits per phase (4: 16 amplitudes per thread, 3: 8)
     int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)
     bool smem_clobber = false;  // clobber: "memory" clobber on every shared-memory asm access
     std::string ptxas_opt = "-Xptxas=-O3";   // ptxas: optimisation level passed to NVRTC's ptxas

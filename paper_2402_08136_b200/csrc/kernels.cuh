@@ -95,6 +95,7 @@ struct TileArgs {
     double2 *psi;
     uint64_t n_tiles;            // 2^(nloc - T)
     int T;
+    int nreg = 4;                // register bits per phase (JIT passes: 3 or 4; the interpreter: 4)
     int tbits[16];               // sorted physical local bits of the tile
     int nphase;
     const RegPhase *phases;      // device

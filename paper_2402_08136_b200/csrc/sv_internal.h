@@ -129,6 +129,7 @@ struct Step {
     // keeps the physical bits phase_R[p] (kRegBits of them) in registers
     std::vector<size_t> phase_start;
     std::vector<std::vector<int>> phase_R;
+    int reg_bits = 4;              // register bits per phase of this pass (16 or 8 amplitudes per thread)
     // ---- Exchange: swap physical global bits xg[i] with local bits xl[i] (one all-to-all round)
     std::vector<int> xg, xl;
     // ---- InitProduct: factors on physical bits
