@@ -226,6 +226,7 @@ const JitConfig &jit_config() {
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
+            else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "ru") x.ru = std::max(0, iv);
             else if (key == "clobber") x.smem_clobber = iv != 0;
             else if (key == "ptxas") x.ptxas_opt = "-Xptxas=" + val;
@@ -1040,7 +1041,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      }\n";
         };
         const bool group_on = cfg.group;
-        for (int oi = P.op0; oi < P.op1; oi++) {
+        for (int oi = P.op0; oi < P.op1 && !cfg.skeleton; oi++) {
             const DRun *run = nullptr;
             for (auto &dr : druns)
                 if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;

@@ -50,6 +50,7 @@ struct JitConfig {
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
     int reg_bits = 4;         // rb: register bits per phase (4: 16 amplitudes per thread, 3: 8)
+    bool skeleton = false;    // skeleton: TIMING EXPERIMENT (wrong results): passes move data, apply no op
     int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)
     bool smem_clobber = false;  // clobber: "memory" clobber on every shared-memory asm access
     std::string ptxas_opt = "-Xptxas=-O3";   // ptxas: optimisation level passed to NVRTC's ptxas
