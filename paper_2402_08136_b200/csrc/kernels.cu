@@ -520,7 +520,19 @@ __global__ void __launch_bounds__(kThreads) k_norm2_partial(const double2 *psi, 
     uint64_t hi = lo + chunk;
     if (hi > n) hi = n;
     double acc = 0.0;
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    uint64_t i = lo + threadIdx.x;
+    // 8 independent loads in flight per thread (the element order of the sum is unchanged)
+    for (; i + 7ull * blockDim.x < hi; i += 8ull * blockDim.x) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = __ldcs(psi + i + (uint64_t)u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            acc = fma(v[u].x, v[u].x, acc);
+            acc = fma(v[u].y, v[u].y, acc);
+        }
+    }
+    for (; i < hi; i += blockDim.x) {
         const double2 v = psi[i];
         acc = fma(v.x, v.x, acc);
         acc = fma(v.y, v.y, acc);
@@ -582,7 +594,25 @@ __global__ void __launch_bounds__(kThreads) k_marginal(const MargArgs a, double 
         const uint64_t sdep = deposit_list(v, a.S, a.q);
         uint64_t cur = deposit_list(r0, a.O, a.nO);
         const uint64_t cnt = seg >= 32 ? seg / 32 : 1;
-        for (uint64_t j = 0; j < cnt; j++) {
+        uint64_t j = 0;
+        // 8 independent loads in flight per lane (the element order of the sum is unchanged)
+        for (; j + 8 <= cnt; j += 8) {
+            uint64_t ad[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                ad[u] = sdep | cur;
+                cur = ((cur | ~a.Omask) + a.step_dep) & a.Omask;
+            }
+            double2 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = __ldcs(a.psi + ad[u]);
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                acc = fma(x[u].x, x[u].x, acc);
+                acc = fma(x[u].y, x[u].y, acc);
+            }
+        }
+        for (; j < cnt; j++) {
             const double2 x = a.psi[sdep | cur];
             acc = fma(x.x, x.x, acc);
             acc = fma(x.y, x.y, acc);
