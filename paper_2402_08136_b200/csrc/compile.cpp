@@ -403,9 +403,17 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
             Step ex;
             ex.kind = StepKind::Exchange;
             std::vector<int> taken;
+            // bits of the pass just before the exchange: a victim outside them lets that pass be split by
+            // exchange slot and pipelined with the transfer (engine.cu slot_split)
+            std::vector<int> prev_tile;
+            if (!s.steps.empty() && s.steps.back().kind == StepKind::Tile) prev_tile = s.steps.back().tile_bits;
+            auto in_prev = [&](int l) {
+                return std::find(prev_tile.begin(), prev_tile.end(), phys[l]) != prev_tile.end();
+            };
             for (int q : need) {
                 // victim: local logical qubit, not a target of g, farthest next nd use (Belady); on
-                // ties the highest physical bit (the top local bits make every slot contiguous)
+                // ties one outside the previous pass's tile, then the highest physical bit (the top local
+                // bits make every slot contiguous)
                 int victim = -1;
                 size_t best = 0;
                 for (int l = 0; l < n; l++) {
@@ -413,7 +421,9 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
                     if (std::find(nd.begin(), nd.end(), l) != nd.end()) continue;
                     if (std::find(taken.begin(), taken.end(), l) != taken.end()) continue;
                     size_t nu = next_use(l, i);
-                    if (victim < 0 || nu > best || (nu == best && phys[l] > phys[victim])) {
+                    const bool better_tie = victim >= 0 && nu == best &&
+                                            (in_prev(victim) != in_prev(l) ? !in_prev(l) : phys[l] > phys[victim]);
+                    if (victim < 0 || nu > best || better_tie) {
                         victim = l;
                         best = nu;
                     }

@@ -186,6 +186,9 @@ static void destroy_impl(sv_state *sv, bool top) {
     pool_free(sv->d_xsend, sv->stream);
     pool_free(sv->d_xrecv, sv->stream);
     nccl_destroy(sv->comm);
+    if (sv->comm_stream) cudaStreamDestroy(sv->comm_stream);
+    if (sv->ev_a) cudaEventDestroy(sv->ev_a);
+    if (sv->ev_b) cudaEventDestroy(sv->ev_b);
     const int device = sv->device;
     cudaStreamSynchronize(sv->stream);
     delete sv;
@@ -926,6 +929,20 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     if (zout[si] >> a.tbits[i] & 1) a.zstore |= 1u << i;
                 }
                 a.n_tiles = 1ull << (nloc - a.T - a.nskip);
+                a.nlift = 0;
+                if (jit_config().xoverlap && use_jit && si + 1 < steps.size() && steps[si + 1].kind == StepKind::Exchange) {
+                    // the exchange that follows takes these local bits: lift them to the top of the tile
+                    // index so the pass can run slot by slot, pipelined with the transfer
+                    std::vector<int> L = steps[si + 1].xl;
+                    std::sort(L.begin(), L.end());
+                    bool ok = L.size() <= 8;
+                    for (int l : L) {
+                        for (int i = 0; i < a.T; i++) ok &= a.tbits[i] != l;
+                        for (int i = 0; i < a.nskip; i++) ok &= a.skip[i] != l;
+                    }
+                    if (ok)
+                        for (int l : L) a.lift[a.nlift++] = l;
+                }
                 {   // HBM bytes: tiles processed x (slots read + slots written)
                     const double tiles = std::ldexp(1.0, -a.nskip);
                     const double rd = (fuse_init && si == 1) ? 0.0 : std::ldexp(1.0, -__builtin_popcount(a.zload));
@@ -1061,6 +1078,51 @@ uint64_t sv_program::launches() const {
 
 namespace hhlsv {
 
+// Pipelined pass + exchange: a JIT tile pass immediately followed by an exchange whose
+// local bits are the top k local bits, none of them a tile bit or a skipped known-zero bit, splits into
+// the 2^k slot ranges of the exchange -- the top k bits of the pass's tile index ARE the slot pattern,
+// so tiles [p S, (p+1) S) produce exactly slot p. The slots are computed in XOR order (step d: slot
+// own ^ d; the rank holding pattern own ^ d computes this rank's slot at the same step d), and slot p is sent to
+// peer(p) on a communication stream while the next slot is computed: the NVLink transfer overlaps the
+// pass (only slot own, kept locally, is computed first).
+static bool slot_split(const sv_state *sv, const LaunchRec &tile, const LaunchRec &ex, uint64_t *per_slot) {
+    if (!jit_config().xoverlap || tile.kind != StepKind::Tile || tile.jit < 0 || ex.kind != StepKind::Exchange ||
+        tile.skip)
+        return false;
+    const XPlan x = xplan(sv, sv->rank, ex.xg, ex.xl);
+    if (tile.tile.nlift != x.k) return false;
+    for (int i = 0; i < x.k; i++)
+        if (tile.tile.lift[i] != x.Ls[i]) return false;
+    const uint64_t n = tile.tile.n_tiles;
+    if ((n >> x.k) << x.k != n || (n >> x.k) == 0) return false;
+    *per_slot = n >> x.k;
+    return true;
+}
+
+// Send slot p to peer(p) and receive peer(p)'s slot into it, chunked, on stream cs (contiguous slots
+// straight from the state, others through the pack / unpack kernels).
+static void exchange_slot(sv_state *sv, const XPlan &x, uint32_t p, cudaStream_t cs) {
+    const uint64_t C = xchunk(x);
+    ensure_xbuf(sv, C);
+    const int peer = xpeer(sv, x, sv->rank, p);
+    for (uint64_t off = 0; off < x.slot; off += C) {
+        const uint64_t cnt = std::min(C, x.slot - off);
+        const double *sb = (const double *)(sv->psi + (uint64_t)p * x.slot + off);
+        if (!x.top) {
+            cuda_check(dev::launch_pack_multi(sv->psi, sv->d_xsend, x.Ls.data(), x.k, p, off, cnt, cs), "slot pack");
+            sb = (const double *)sv->d_xsend;
+        }
+        double *rb = (double *)sv->d_xrecv;
+        nccl_check(nccl_alltoall_pairs(sv->comm, &sb, &rb, &peer, 1, 2 * cnt, cs), "exchange slot");
+        if (x.top)
+            cuda_check(cudaMemcpyAsync(sv->psi + (uint64_t)p * x.slot + off, sv->d_xrecv, sizeof(double2) * cnt,
+                                       cudaMemcpyDeviceToDevice, cs),
+                       "exchange slot copy");
+        else
+            cuda_check(dev::launch_unpack_multi(sv->psi, sv->d_xrecv, x.Ls.data(), x.k, p, off, cnt, cs), "slot unpack");
+    }
+}
+
 static void launch_rec(sv_state *sv, sv_program *p, const LaunchRec &r) {
     if (r.skip) return;
     switch (r.kind) {
@@ -1091,6 +1153,23 @@ void program_run(sv_state *sv, sv_program *p) {
                 virtual_exchange(sv, p->subs[0]->recs[i].xg, p->subs[0]->recs[i].xl);
                 continue;
             }
+            uint64_t per = 0;
+            if (i + 1 < ns && slot_split(sv->views[0], p->subs[0]->recs[i], p->subs[0]->recs[i + 1], &per)) {
+                // the slot-range launches of the pipelined path (same kernels, same ranges)
+                const XPlan x0 = xplan(sv->views[0], 0, p->subs[0]->recs[i + 1].xg, p->subs[0]->recs[i + 1].xl);
+                for (size_t r = 0; r < p->subs.size(); r++) {
+                    const LaunchRec &tr = p->subs[r]->recs[i];
+                    const uint32_t own = xplan(sv->views[r], (int)r, p->subs[r]->recs[i + 1].xg,
+                                               p->subs[r]->recs[i + 1].xl).own;
+                    for (uint32_t d = 0; d < (1u << x0.k); d++) {
+                        const uint64_t slot = own ^ d;
+                        cuda_check(jit_launch(p->subs[r]->jit[tr.jit], tr.tile.psi, tr.tile.blob, (slot + 1) * per,
+                                              tr.tile.rank_base, tr.tile.T, sv->stream, slot * per),
+                                   "tile (jit, slot range)");
+                    }
+                }
+                continue;
+            }
             for (size_t r = 0; r < p->subs.size(); r++) launch_rec(sv->views[r], p->subs[r], p->subs[r]->recs[i]);
         }
         sv->phys = p->sched.phys_out;
@@ -1105,6 +1184,37 @@ void program_run(sv_state *sv, sv_program *p) {
     for (size_t ri = 0; ri < p->recs.size(); ri++) {
         const LaunchRec &r = p->recs[ri];
         if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri], sv->stream), "event");
+        uint64_t per = 0;
+        if (sv->world > 1 && ri + 1 < p->recs.size() && slot_split(sv, r, p->recs[ri + 1], &per)) {
+            const LaunchRec &ex = p->recs[ri + 1];
+            const XPlan x = xplan(sv, sv->rank, ex.xg, ex.xl);
+            if (!sv->comm_stream) cuda_check(cudaStreamCreateWithFlags(&sv->comm_stream, cudaStreamNonBlocking), "comm stream");
+            if (!sv->ev_a) {
+                cuda_check(cudaEventCreateWithFlags(&sv->ev_a, cudaEventDisableTiming), "event");
+                cuda_check(cudaEventCreateWithFlags(&sv->ev_b, cudaEventDisableTiming), "event");
+            }
+            nvtxRangePushA("hhlsv tile_pass+exchange (pipelined)");
+            for (uint32_t d = 0; d < (1u << x.k); d++) {
+                const uint32_t slot = x.own ^ d;
+                cuda_check(jit_launch(p->jit[r.jit], r.tile.psi, r.tile.blob, (slot + 1) * per, r.tile.rank_base, r.tile.T,
+                                      sv->stream, (uint64_t)slot * per),
+                           "tile (jit, slot range)");
+                if (d == 0) continue;                    // own slot: stays here
+                cuda_check(cudaEventRecord(sv->ev_a, sv->stream), "event");
+                cuda_check(cudaStreamWaitEvent(sv->comm_stream, sv->ev_a, 0), "wait");
+                exchange_slot(sv, x, slot, sv->comm_stream);
+            }
+            if (p->timing) {
+                cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
+                cuda_check(cudaEventRecord(p->ev[2 * ri + 2], sv->stream), "event");
+            }
+            cuda_check(cudaEventRecord(sv->ev_b, sv->comm_stream), "event");
+            cuda_check(cudaStreamWaitEvent(sv->stream, sv->ev_b, 0), "wait");
+            nvtxRangePop();
+            ri++;                                        // the exchange step is done
+            if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
+            continue;
+        }
         if (r.skip) {
             if (p->timing) cuda_check(cudaEventRecord(p->ev[2 * ri + 1], sv->stream), "event");
             continue;

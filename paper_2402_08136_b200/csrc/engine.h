@@ -26,6 +26,8 @@ struct sv_state {
     size_t io_len = 0;              // in double2
     double2 *d_xsend = nullptr, *d_xrecv = nullptr;  // exchange buffers
     size_t x_len = 0;
+    cudaStream_t comm_stream = nullptr;              // pipelined exchanges (created on first use)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     hhlsv::Comm comm;
     // virtual sharding (world > 1 without an NCCL id): all shards in this process on one GPU,
     // one view per virtual rank, exchanges by device copies (tests the rank-dependent paths)

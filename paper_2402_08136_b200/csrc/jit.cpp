@@ -227,6 +227,7 @@ const JitConfig &jit_config() {
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
+            else if (key == "xoverlap") x.xoverlap = iv != 0;
             else if (key == "ru") x.ru = std::max(0, iv);
             else if (key == "clobber") x.smem_clobber = iv != 0;
             else if (key == "ptxas") x.ptxas_opt = "-Xptxas=" + val;
@@ -480,7 +481,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     std::ostringstream k;
     if (ctot) k << "struct CWArg { double2 w[" << ctot << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
-      << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base"
+      << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base, u64 tile0"
       << (ctot ? ", const CWArg cwa" : "") << ") {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
@@ -510,12 +511,19 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     }
     if (dsub_max)
         k << "  const SArr dsub{depB.b + " << (8 << SB) << "u + " << wtot * 16 << "u};\n";
-    {   // tile index -> base: zeros inserted at the tile bits and at the skipped known-zero bits
+    {   // tile index -> base: zeros inserted at the tile bits and at the skipped known-zero bits; lifted
+        // bits (if any) take the top bits of the tile index
         std::vector<int> ins(a.tbits, a.tbits + T);
         for (int i = 0; i < a.nskip; i++) ins.push_back(a.skip[i]);
+        for (int i = 0; i < a.nlift; i++) ins.push_back(a.lift[i]);
         std::sort(ins.begin(), ins.end());
-        k << "  auto tile_base = [](u64 t) { u64 b = t;";
+        int ltiles = 0;
+        while ((1ull << ltiles) < a.n_tiles) ltiles++;
+        const int nlow = ltiles - a.nlift;
+        k << "  auto tile_base = [](u64 t) { u64 b = " << (a.nlift ? "t & " + u64s((1ull << nlow) - 1ull) : std::string("t"))
+          << ";";
         for (int b : ins) k << " b = insz(b, " << b << ");";
+        for (int i = 0; i < a.nlift; i++) k << " b |= ((t >> " << nlow + i << ") & 1ull) << " << a.lift[i] << ";";
         k << " return b; };\n";
     }
     k << "  auto addr = [&](u64 base, u32 u) { return base | depA[u & " << ((1u << SA) - 1) << "u] | depB[u >> " << SA
@@ -570,7 +578,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      }\n";
             return any_run;
         };
-    k << "  u64 tile = blockIdx.x;\n";
+    k << "  u64 tile = tile0 + blockIdx.x;      // tiles [tile0, n_tiles) of the pass\n";
     if (hoist) {
         k << "  if (tile < n_tiles) {\n";
         emit_pre(0, "rank_base | tile_base(tile)");
@@ -1262,7 +1270,7 @@ size_t jit_smem_bytes(int T, size_t total) {
 }
 
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
-                       int T, cudaStream_t s) {
+                       int T, cudaStream_t s, uint64_t tile0) {
     const int threads = p.nthr;
     const size_t smem = jit_smem_bytes(T, p.smem_extra);
     const void *f = reinterpret_cast<const void *>(p.kern);
@@ -1280,9 +1288,10 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
         if (e != cudaSuccess) return e;
         p.sms = sms;                 // 148 on the B200: persistent grid = SMs x resident CTAs
     }
+    if (tile0 >= n_tiles) return cudaSuccess;
     uint64_t grid = (uint64_t)p.sms * p.per_sm;
-    if (grid > n_tiles) grid = n_tiles;
-    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base, (void *)p.cwvals.data()};
+    if (grid > n_tiles - tile0) grid = n_tiles - tile0;
+    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base, &tile0, (void *)p.cwvals.data()};
     return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 

@@ -50,6 +50,7 @@ struct JitConfig {
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
     int reg_bits = 4;         // rb: register bits per phase (4: 16 amplitudes per thread, 3: 8)
+    bool xoverlap = true;     // xoverlap: a pass followed by a top-bit exchange is split by slot and pipelined
     bool skeleton = false;    // skeleton: TIMING EXPERIMENT (wrong results): passes move data, apply no op
     int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)
     bool smem_clobber = false;  // clobber: "memory" clobber on every shared-memory asm access
@@ -72,8 +73,9 @@ void jit_build(std::vector<JitPass> &passes);            // compile (cached) + l
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.
 std::string jit_source_tag(const std::string &src);
+// Launch tiles [tile0, n_tiles) of a pass (tile0 = 0: the whole pass).
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
-                       int T, cudaStream_t s);
+                       int T, cudaStream_t s, uint64_t tile0 = 0);
 size_t jit_smem_bytes(int T, size_t extra);
 
 }  // namespace hhlsv

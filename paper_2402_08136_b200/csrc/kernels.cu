@@ -632,6 +632,15 @@ __global__ void k_marginal_final(const double *ws, int logC, uint64_t nbins, dou
     }
 }
 
+__global__ void __launch_bounds__(1024) k_marginal_final_blocks(const double *ws, int logC, double *out) {
+    const uint64_t v = blockIdx.x;
+    const uint64_t C = 1ull << logC;
+    double acc = 0.0;
+    for (uint64_t c = threadIdx.x; c < C; c += blockDim.x) acc += ws[(v << logC) + c];
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) out[v] = acc;
+}
+
 cudaError_t launch_marginal(const double2 *psi, int nloc, const int *S, int q, double *ws, double *out,
                             cudaStream_t s) {
     MargArgs a{};
@@ -664,7 +673,10 @@ cudaError_t launch_marginal(const double2 *psi, int nloc, const int *S, int q, d
     const uint64_t blocks = (nwarps * 32 + kThreads - 1) / kThreads;
     k_marginal<<<(unsigned)blocks, kThreads, 0, s>>>(a, ws);
     const uint64_t nbins = 1ull << q;
-    k_marginal_final<<<grid_for(nbins, kThreads), kThreads, 0, s>>>(ws, logC, nbins, out);
+    if (logC >= 8)      // many partials per bin: one block per bin (fixed-order strided sums + block tree)
+        k_marginal_final_blocks<<<(unsigned)nbins, 1024, 0, s>>>(ws, logC, out);
+    else
+        k_marginal_final<<<grid_for(nbins, kThreads), kThreads, 0, s>>>(ws, logC, nbins, out);
     return cudaGetLastError();
 }
 

@@ -111,6 +111,11 @@ struct TileArgs {
     int nskip;
     int skip[8];
     uint32_t zload, zstore;
+    // Out-of-tile bits mapped to the TOP of the tile index (ascending): with the exchange that follows
+    // the pass on these local bits, tiles [p 2^nlow, (p+1) 2^nlow) are exactly exchange slot p
+    // (pipelined pass + exchange). nlift = 0: plain ascending mapping.
+    int nlift = 0;
+    int lift[8];
 };
 
 // ---- launchers (stream-ordered, no sync) ----

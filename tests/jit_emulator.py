@@ -238,8 +238,8 @@ def build_pass(src: str) -> str:
     """Compile one pass source into an emulator executable (cached by content)."""
     os.makedirs(_BUILD_DIR, exist_ok=True)
     body, has_cw = _host_source(src)
-    call = ("hhlsv_tile(psi, blob, n_tiles, rank_base, *(const CWArg *)cw_b.data())" if has_cw
-            else "hhlsv_tile(psi, blob, n_tiles, rank_base)")
+    call = ("hhlsv_tile(psi, blob, n_tiles, rank_base, 0ull, *(const CWArg *)cw_b.data())" if has_cw
+            else "hhlsv_tile(psi, blob, n_tiles, rank_base, 0ull)")
     full = HOST_PRELUDE + body + MAIN.replace("KERNEL_CALL", call)
     tag = hashlib.sha1(full.encode()).hexdigest()[:16]
     exe = os.path.join(_BUILD_DIR, f"pass_{tag}")
