@@ -79,10 +79,9 @@ sv_status sv_nccl_unique_id(unsigned char out_id[128]);
 sv_status sv_create(int n_qubits, const sv_dist *dist, void *cuda_stream, sv_state **out);
 sv_status sv_destroy(sv_state *sv);
 /* State and workspace memory comes from a stream-ordered pool owned by the library (never the
- * process-wide default pool). Freed memory stays cached for the next state -- up to one state's
- * worth once no state is alive (re-mapping a 16 GiB state costs seconds) -- and is released when a
- * new state would not fit otherwise, or by this call (device < 0: every device). Synchronises the
- * device. SV_E_CUDA without a device. */
+ * process-wide default pool). Freed memory stays cached for the next state (re-mapping a 16 GiB
+ * state costs milliseconds to seconds) and is released when a new state would not fit otherwise, or
+ * by this call (device < 0: every device). Synchronises the device. SV_E_CUDA without a device. */
 sv_status sv_trim_memory(int device);
 /* Re-initialise to |0...0> and reset the logical->physical qubit map to identity. */
 sv_status sv_reset(sv_state *sv);

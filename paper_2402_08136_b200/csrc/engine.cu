@@ -27,14 +27,13 @@ static void nccl_check(int rc, const char *what) {
 // the process-wide default pool, so other allocators in the process -- e.g. torch -- are not
 // starved) with an unbounded release threshold: freeing a 16 GiB state and creating the next one
 // (hhl_solve called repeatedly) reuses the pool instead of unmapping/remapping pages (measured on the
-// B200: trimming after every solve makes the next 16 GiB allocation cost ~4.7 s). When the last live
-// state is destroyed the pool keeps at most one state's worth (the largest state allocated) for the
-// next solve; sv_trim_memory() releases everything, and state_create trims before reporting OOM.
+// B200: trimming after every solve makes the next 16 GiB allocation cost ~4.7 s, a partial trim ~5 ms).
+// The memory stays cached for the next state; sv_trim_memory() releases it, and state_create trims
+// before reporting OOM (so the cache never makes a state fail to fit).
 namespace {
 std::mutex g_pool_mu;
 cudaMemPool_t g_pools[64] = {};
 int g_live_states = 0;
-size_t g_keep_bytes[64] = {};       // largest single state allocation per device
 }  // namespace
 
 void pool_trim(int device, size_t keep) {
@@ -129,10 +128,7 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
         freeb += pool_slack(device);
         if (bytes * (virt ? world : 1) > freeb) fail(SV_E_OOM, "state does not fit in device memory");
     }
-    {
-        std::lock_guard<std::mutex> lk(g_pool_mu);
-        if (device < 64) g_keep_bytes[device] = std::max(g_keep_bytes[device], bytes * (virt ? world : 1));
-    }
+
     if (virt) {
         sv->vworld = world;
         sv->world = 1;
@@ -193,12 +189,12 @@ static void destroy_impl(sv_state *sv, bool top) {
     cudaStreamSynchronize(sv->stream);
     delete sv;
     if (!top) return;
+    (void)device;
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    if (--g_live_states <= 0) {      // last live state: keep one state's worth for the next one
-        g_live_states = 0;
-        if (device >= 0 && device < 64 && g_pools[device])
-            cudaMemPoolTrimTo(g_pools[device], g_keep_bytes[device] + (64ull << 20));
-    }
+    if (--g_live_states < 0) g_live_states = 0;
+    // the pool keeps its memory for the next state (measured: even a trim that keeps one state's worth
+    // costs the next 16 GiB allocation ~5 ms of re-mapping); it is released when a new state would not
+    // fit otherwise (state_create) or by sv_trim_memory
 }
 
 void state_reset(sv_state *sv) {
@@ -780,13 +776,12 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             if (!f.diag)
                 for (int q : f.qubits) covered |= 1ull << q;
         const uint64_t loc = nloc >= 64 ? ~0ull : ((1ull << nloc) - 1ull);
-        uint64_t zero = loc & ~covered, eligible = zero, seen_other = 0;
+        uint64_t zero = loc & ~covered, eligible = zero;
         for (size_t si = 1; si < steps.size(); si++) {
             const Step &st = steps[si];
             zin[si] = zero;
             if (st.kind != StepKind::Tile) {          // non-tile step: no bit still zero here may be skipped
                 eligible &= ~zero;
-                seen_other = 1;
             }
             for (const Gate &g : st.tile_ops)
                 if (g.kind == Kind::Dense || g.kind == Kind::Controlled || g.kind == Kind::RecipRY)
@@ -795,7 +790,6 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             if (st.kind == StepKind::Exchange) zero = 0;
             zout[si] = zero;
         }
-        (void)seen_other;
         eligible &= ~zero;                            // never activated in this program: not skipped
         for (size_t si = 0; si < steps.size(); si++) {
             zin[si] &= eligible;
