@@ -85,6 +85,13 @@ static cudaError_t pool_malloc(void **p, size_t bytes, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     return state_alloc(p, bytes, s, dev);
 }
+// Stream-ordered allocation without the synchronisation (the caller synchronises once for a batch).
+static cudaError_t pool_malloc_nosync(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    return cudaMallocFromPoolAsync(p, bytes, lib_pool(dev), s);
+}
 static void pool_free(void *p, cudaStream_t s) { state_free(p, s); }
 
 sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zero_init) {
@@ -153,8 +160,9 @@ sv_state *state_create(int n, const sv_dist *dist, cudaStream_t stream, bool zer
         cuda_check(state_alloc((void **)&sv->psi, bytes, stream, device), "alloc(state)");
     }
     sv->red_len = dev::kRedBlocks;
-    cuda_check(pool_malloc((void **)&sv->d_red, sizeof(double) * sv->red_len, stream), "cudaMalloc(red)");
-    cuda_check(pool_malloc((void **)&sv->d_scalar, sizeof(double) * 8, stream), "cudaMalloc(scalar)");
+    cuda_check(pool_malloc_nosync((void **)&sv->d_red, sizeof(double) * sv->red_len, stream), "cudaMalloc(red)");
+    cuda_check(pool_malloc_nosync((void **)&sv->d_scalar, sizeof(double) * 8, stream), "cudaMalloc(scalar)");
+    cuda_check(cudaStreamSynchronize(stream), "alloc sync");
     if (world > 1 && !virt) nccl_check(nccl_init(sv->comm, world, rank, dist->nccl_id), "ncclCommInitRank");
     if (zero_init) state_reset(sv.get());
     {
@@ -1018,23 +1026,26 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         }
         return p.release();
     }
-    // upload blob and tile ops, then rebase pointers
+    // upload blob and tile ops (stream-ordered allocations and copies, one synchronisation: the host
+    // vectors live until then), then rebase pointers
+    cudaStream_t us = p->sv->stream;
     if (!blob.empty()) {
-        cuda_check(pool_malloc((void **)&p->d_blob, sizeof(double2) * blob.size(), p->sv->stream), "cudaMalloc(blob)");
-        cuda_check(cudaMemcpy(p->d_blob, blob.data(), sizeof(double2) * blob.size(), cudaMemcpyHostToDevice),
+        cuda_check(pool_malloc_nosync((void **)&p->d_blob, sizeof(double2) * blob.size(), us), "cudaMalloc(blob)");
+        cuda_check(cudaMemcpyAsync(p->d_blob, blob.data(), sizeof(double2) * blob.size(), cudaMemcpyHostToDevice, us),
                    "upload blob");
     }
     if (!rops.empty()) {
-        cuda_check(pool_malloc((void **)&p->d_ops, sizeof(dev::RegOp) * rops.size(), p->sv->stream), "cudaMalloc(tile ops)");
-        cuda_check(cudaMemcpy(p->d_ops, rops.data(), sizeof(dev::RegOp) * rops.size(), cudaMemcpyHostToDevice),
+        cuda_check(pool_malloc_nosync((void **)&p->d_ops, sizeof(dev::RegOp) * rops.size(), us), "cudaMalloc(tile ops)");
+        cuda_check(cudaMemcpyAsync(p->d_ops, rops.data(), sizeof(dev::RegOp) * rops.size(), cudaMemcpyHostToDevice, us),
                    "upload tile ops");
     }
     if (!phases.empty()) {
-        cuda_check(pool_malloc((void **)&p->d_phases, sizeof(dev::RegPhase) * phases.size(), p->sv->stream), "cudaMalloc(phases)");
-        cuda_check(cudaMemcpy(p->d_phases, phases.data(), sizeof(dev::RegPhase) * phases.size(),
-                              cudaMemcpyHostToDevice),
+        cuda_check(pool_malloc_nosync((void **)&p->d_phases, sizeof(dev::RegPhase) * phases.size(), us), "cudaMalloc(phases)");
+        cuda_check(cudaMemcpyAsync(p->d_phases, phases.data(), sizeof(dev::RegPhase) * phases.size(),
+                                   cudaMemcpyHostToDevice, us),
                    "upload phases");
     }
+    cuda_check(cudaStreamSynchronize(us), "upload sync");
     p->h2d_bytes += sizeof(double2) * blob.size() + sizeof(dev::RegOp) * rops.size() +
                     sizeof(dev::RegPhase) * phases.size();
     for (size_t r : blob_fix) {
@@ -1170,6 +1181,35 @@ void program_run(sv_state *sv, sv_program *p) {
         for (auto *v : sv->views) v->phys = sv->phys;
         return;
     }
+    // CUDA graph for small single-rank programs (launch-bound: Table 1's 13-16 qubit circuits run a few
+    // passes of tens of microseconds): the launches of the second run are captured on a private stream
+    // and replayed from then on, ordered after / before the state's stream by events
+    bool graphable = sv->world == 1 && !p->timing && sv->local_amps() <= (1ull << 20) && jit_config().graphs;
+    for (const LaunchRec &r : p->recs) graphable &= r.kind != StepKind::Exchange;
+    if (graphable && ++p->runs >= 2) {
+        if (!p->gstream) {
+            cuda_check(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking), "graph stream");
+            cuda_check(cudaEventCreateWithFlags(&p->gev_a, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&p->gev_b, cudaEventDisableTiming), "event");
+        }
+        cuda_check(cudaEventRecord(p->gev_a, sv->stream), "event");
+        cuda_check(cudaStreamWaitEvent(p->gstream, p->gev_a, 0), "wait");
+        if (!p->graph_exec) {
+            cudaStream_t user = sv->stream;
+            sv->stream = p->gstream;                         // launch_rec enqueues on sv->stream
+            cuda_check(cudaStreamBeginCapture(p->gstream, cudaStreamCaptureModeThreadLocal), "begin capture");
+            for (const LaunchRec &r : p->recs) launch_rec(sv, p, r);
+            const cudaError_t ce = cudaStreamEndCapture(p->gstream, &p->graph);
+            sv->stream = user;
+            cuda_check(ce, "end capture");
+            cuda_check(cudaGraphInstantiate(&p->graph_exec, p->graph, 0), "graph instantiate");
+        }
+        cuda_check(cudaGraphLaunch(p->graph_exec, p->gstream), "graph launch");
+        cuda_check(cudaEventRecord(p->gev_b, p->gstream), "event");
+        cuda_check(cudaStreamWaitEvent(sv->stream, p->gev_b, 0), "wait");
+        sv->phys = p->sched.phys_out;
+        return;
+    }
     if (p->timing && p->ev.size() != 2 * p->recs.size()) {
         for (auto e : p->ev) cudaEventDestroy(e);
         p->ev.assign(2 * p->recs.size(), nullptr);
@@ -1268,6 +1308,11 @@ void program_destroy(sv_program *p) {
     pool_free(p->d_phases, p->sv ? p->sv->stream : nullptr);
     for (auto *d : p->d_tabs) pool_free(d, p->sv ? p->sv->stream : nullptr);
     for (auto e : p->ev) cudaEventDestroy(e);
+    if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    if (p->gstream) cudaStreamDestroy(p->gstream);
+    if (p->gev_a) cudaEventDestroy(p->gev_a);
+    if (p->gev_b) cudaEventDestroy(p->gev_b);
     delete p;
 }
 

@@ -70,6 +70,12 @@ struct sv_program {
     std::vector<sv_program *> subs;   // virtual sharding: one program per view
     bool timing = false;
     std::vector<cudaEvent_t> ev;      // 2 per rec when timing
+    // small single-rank programs replay a CUDA graph of their launches (captured on the 2nd run)
+    int runs = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t gev_a = nullptr, gev_b = nullptr;
     uint64_t launches() const;
 };
 

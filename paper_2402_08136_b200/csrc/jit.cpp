@@ -223,11 +223,13 @@ const JitConfig &jit_config() {
             else if (key == "tail") x.tail = iv != 0;
             else if (key == "cw") x.cw = iv != 0;
             else if (key == "ctab") x.ctab = iv != 0;
+            else if (key == "ctabbits") x.ctab_bits = std::max(0, std::min(6, iv));
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
+            else if (key == "graphs") x.graphs = iv != 0;
             else if (key == "ru") x.ru = std::max(0, iv);
             else if (key == "clobber") x.smem_clobber = iv != 0;
             else if (key == "ptxas") x.ptxas_opt = "-Xptxas=" + val;
@@ -381,7 +383,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (auto &dr : druns) in_run |= (int)i >= dr.a && (int)i < dr.b;
             if (in_run) continue;
             const auto tbv = tbits_of(op);
-            if (tbv.size() > 2) continue;
+            if ((int)tbv.size() > cfg.ctab_bits) continue;
             std::map<uint32_t, size_t> ent;
             for (int j = 0; j < RA; j++) {
                 if ((j & op.rcm) != op.rcv) continue;

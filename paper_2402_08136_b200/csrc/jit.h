@@ -46,10 +46,12 @@ struct JitConfig {
     bool sparse = true;       // sparse: exact structural zeros of wide matrices skipped at codegen
     bool tail = true;         // tail: a trailing wide dense op writes straight into the store buffer
     bool cw = true;           // cw: >= 3-target matrices as by-value kernel parameters (constant bank)
-    bool ctab = true;         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
+    bool ctab = true;
+    int ctab_bits = 2;        // ctabbits: max thread bits of a constant-bank table index (selected per thread)         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
     int reg_bits = 4;         // rb: register bits per phase (4: 16 amplitudes per thread, 3: 8)
+    bool graphs = true;       // graphs: small single-rank programs replay a captured CUDA graph
     bool xoverlap = true;     // xoverlap: a pass followed by a top-bit exchange is split by slot and pipelined
     bool skeleton = false;    // skeleton: TIMING EXPERIMENT (wrong results): passes move data, apply no op
     int ru = 0;               // ru: rows per block of the rolled wide-op loop (0 = 16 real / 2 complex)

@@ -157,3 +157,21 @@ def test_readout_rejects_wrong_n():
         rc = L.hhl_readout(st.handle, ctypes.byref(prog._rep), N, x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                            ctypes.byref(ps))
         assert pkg.sv.STATUS[rc] == "SV_E_ARG"
+
+
+@pytest.mark.parametrize("name", ["C3p", "C3"])
+def test_small_program_graph_replay(name):
+    """Small single-rank programs replay a captured CUDA graph from their second run on (Table 1's
+    launch-bound regime): every run, graph or not, gives the oracle's state bit for bit the same."""
+    A, b, nc = configs.get(name)
+    xo, po, psi_o, p = ohhl.solve(A, b, nc)
+    st = pkg.State(p.n)
+    prog = pkg.HHLProgram.build(st, A, b, clock_qubits=nc, **BENCH)
+    outs = []
+    for _ in range(3):
+        prog.run()
+        outs.append(st.read())
+        x, ps = prog.readout()
+        assert abs(ps - po) < 1e-12
+    assert np.abs(outs[0] - psi_o).max() < 1e-10
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
