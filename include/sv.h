@@ -99,6 +99,13 @@ sv_status sv_sync(sv_state *sv);
 sv_status sv_read(sv_state *sv, uint64_t first, uint64_t count, double *interleaved_out);
 sv_status sv_write(sv_state *sv, uint64_t first, uint64_t count, const double *interleaved_in);
 
+/* Checkpoint / restore of the whole state (SPEC "External Interfaces": a uint64 length header then
+ * 2^n interleaved re, im doubles, little-endian, LOGICAL order). sv_restore requires the header to
+ * equal 2^n of `sv` (SV_E_ARG otherwise, also on I/O errors). Streams through a 64 MiB host buffer.
+ * Synchronous; collective when sharded (every rank reads / writes the full logical state). */
+sv_status sv_dump(sv_state *sv, const char *path);
+sv_status sv_restore(sv_state *sv, const char *path);
+
 /* ------------------------------------------------------------------ gates ---- */
 /* Fused-gate IR (SURVEY §2.2 D-FG; the paper's "single fused gate", Fig. 4).
  *  SV_DENSE       targets (1..5): data = 2^k × 2^k matrix.

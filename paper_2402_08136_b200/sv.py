@@ -74,7 +74,7 @@ class hhl_report(ctypes.Structure):
 
 
 EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_destroy", "sv_trim_memory",
-           "sv_reset", "sv_info",
+           "sv_reset", "sv_info", "sv_dump", "sv_restore",
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
            "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
         "sv_qubit_map": [vp, P(c_int)],
         "sv_sync": [vp],
         "sv_read": [vp, c_u64, c_u64, P(c_dbl)],
+        "sv_dump": [vp, ctypes.c_char_p], "sv_restore": [vp, ctypes.c_char_p],
         "sv_write": [vp, c_u64, c_u64, P(c_dbl)],
         "sv_apply_fused": [vp, P(sv_gate), ctypes.c_size_t],
         "sv_apply_circuit": [vp, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), P(sv_plan_report)],
@@ -253,6 +254,14 @@ class State:
         out = np.empty(count, dtype=np.complex128)
         _check(load().sv_read(self._h, first, count, _dp(out.view(np.float64))))
         return out
+
+    def dump(self, path: str):
+        """sv_dump: checkpoint the state (uint64 length + interleaved re/im doubles, logical order)."""
+        _check(load().sv_dump(self._h, os.fsencode(path)))
+
+    def restore(self, path: str):
+        """sv_restore: load a checkpoint written by dump() into this state."""
+        _check(load().sv_restore(self._h, os.fsencode(path)))
 
     def write(self, amps, first: int = 0):
         a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128))

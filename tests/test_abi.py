@@ -227,5 +227,6 @@ def test_paper_mode_fusion_counts():
     _, r2 = pkg.schedule_dump(p.n, t, fusion_kmax=2, tile_qubits=-1)
     assert rp["n_logical"] == len(t) == 101
     assert rp["n_fused"] <= r2["n_fused"] and rp["n_fused"] <= len(t) / 3
+    assert 1 - rp["n_fused"] / rp["n_logical"] >= 0.60          # SPEC acceptance 4: >= 60 % reduction
     with pytest.raises(pkg.SVError):
         pkg.schedule_dump(p.n, t, fusion_mode=3)

@@ -403,3 +403,74 @@ def test_padded_stress_circuit_tensor_factor(n, sampled):
     err = float(np.abs(got - ref).max())
     print(f"\n[parity] P{n} padded stress circuit ({len(gates)} gates): max|psi - tensor factors| = {err:.3e}")
     assert err < 1e-10
+
+
+def test_dump_restore_checkpoint(tmp_path):
+    """sv_dump / sv_restore (SPEC "External Interfaces"): uint64 length header + interleaved re/im
+    doubles, little-endian, logical order -- read back by numpy -- and a restore into another state
+    (after a permuting circuit, so logical != physical order)."""
+    n = 12
+    gates = synthetic.random_circuit(n, 30, seed=4, kmax=2) + [{"kind": "swap", "targets": [0, 11]}]
+    got, ref, st = run_both(n, gates, synthetic.random_state(n, 4), fusion_kmax=2, tile_qubits=8)
+    path = str(tmp_path / "state.bin")
+    st.dump(path)
+    raw = np.fromfile(path, dtype="<u8", count=1)
+    assert int(raw[0]) == 1 << n
+    data = np.fromfile(path, dtype="<f8", offset=8).view(np.complex128)
+    assert np.array_equal(data, got)
+    st2 = pkg.State(n)
+    st2.restore(path)
+    assert np.array_equal(st2.read(), got)
+    st3 = pkg.State(n + 1)
+    with pytest.raises(pkg.SVError):
+        st3.restore(path)
+
+
+def test_random_hermitian_systems():
+    """SPEC acceptance 5: 50 seeded random symmetric systems (dim 2 and 4, kappa <= 8) through
+    hhl_solve: x equal to the oracle's HHL x (1e-10) at n_qpe = 8, and within 5e-2 relative of the dense
+    direct solve; systems with exactly representable eigenvalues to 1e-8."""
+    g = synthetic.rng(611)
+    for i in range(50):
+        d = 2 if i % 2 == 0 else 4
+        Q, _ = np.linalg.qr(g.standard_normal((d, d)))
+        lam = g.uniform(1.0, 8.0, d) * np.where(g.random(d) < 0.3, -1.0, 1.0)
+        lam[0] = 1.0 if abs(lam[0]) < 1 else lam[0]
+        if np.abs(lam).max() / np.abs(lam).min() > 8:
+            lam = np.sign(lam) * np.clip(np.abs(lam), 1.0, 8.0)
+        A = (Q * lam) @ Q.T
+        A = (A + A.T) / 2
+        b = g.standard_normal(d)
+        x, rep = pkg.hhl_solve(A, b, clock_qubits=8)
+        xo, po, _, p = ohhl.solve(A, b, 8)
+        assert np.abs(x - xo).max() < 1e-10
+        xt = np.linalg.solve(A, b)
+        assert np.linalg.norm(x - xt) / np.linalg.norm(xt) < 5e-2, (i, lam)
+    for lam in ([1.0, 2.0], [1.0, 4.0], [0.5, 1.0, 2.0, 4.0]):
+        d = len(lam)
+        Q, _ = np.linalg.qr(g.standard_normal((d, d)))
+        A = (Q * np.array(lam)) @ Q.T
+        A = (A + A.T) / 2
+        b = g.standard_normal(d)
+        x, rep = pkg.hhl_solve(A, b, clock_qubits=6)
+        xt = np.linalg.solve(A, b)
+        assert np.linalg.norm(x - xt) / np.linalg.norm(xt) < 1e-8, lam
+
+
+@pytest.mark.parametrize("nc", [3, 4, 5])
+def test_qpe_exact_on_gpu(nc):
+    """SPEC acceptance 6: QPE on an eigenvector with a representable eigenphase puts probability
+    >= 1 - 1e-9 on the correct clock bitstring (GPU run of the oracle's H / c-U / IQFT list)."""
+    A = np.diag([1.0, 3.0])
+    p = ohhl.plan(A, np.ones(2), nc)
+    gates = ohhl.build(p)
+    q = gates[1: 1 + 2 * nc + nc + nc * (nc - 1) // 2 + nc // 2]
+    for s in range(2):
+        psi0 = np.zeros(1 << p.n, complex)
+        psi0[: 1 << p.n_b] = p.V[:, s]
+        st = pkg.State(p.n)
+        st.write(psi0)
+        st.apply_circuit(q, fusion_kmax=2)
+        probs = st.probabilities(list(range(p.n_b, p.n_b + nc)))
+        m0 = round(p.phi[s] * (1 << nc))
+        assert probs[m0] >= 1 - 1e-9
