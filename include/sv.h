@@ -231,7 +231,9 @@ sv_status sv_sample(sv_state *sv, uint64_t shots, uint64_t seed, uint64_t *out);
  * PAPER.md:225-242 read per DESIGN.md R2/R3). */
 typedef struct {
     int clock_qubits;   /* n_c including the sign qubit; <= 0: max(n_b+1, ceil(log2(kappa+1))) + 1 */
-    int fusion_kmax;    /* 0 -> library default (4) ; -1 -> no fusion */
+    int fusion_kmax;    /* 0 -> chosen by the a2 cost model among 1..5 (predicted time of each
+                           candidate schedule from HBM bytes, FP64 flops, register-phase exchanges,
+                           launches, NVLink exchanges); -1 -> no fusion; 1..5 -> that width */
     int tile_qubits;    /* 0 -> library default ; -1 -> one pass per fused op */
     double recip_snap;  /* reciprocal snapping tolerance (qlsarepo: 1e-5); < 0 -> default 1e-5 */
     int init_fold;      /* 0 (default): fold the leading product-state gates into the init kernel; 1: also the
@@ -273,6 +275,8 @@ typedef struct {
     double p_anc1;                 /* P(ancilla = 1) summed over every clock value (hhl_solve only;
                                       the paper's "measure ancilla and get 1", before
                                       the clock = 0 post-selection of R7) */
+    int fusion_kmax_used;          /* fusion width used (the cost model's choice when fusion_kmax = 0) */
+    double model_ms;               /* the a2 cost model's predicted B200 time of the schedule (ms) */
 } hhl_report;
 
 /* hhl_plan_size: the register sizes (n_data, n_clock, n_total) hhl_build_program needs for (A, b).

@@ -408,8 +408,18 @@ sv_status hhl_plan_size(const double *A, const double *b, int N, const hhl_optio
 
 // Host part of the HHL program: logical circuit, product-state prefix folded into init factors,
 // fusion of the rest. Shared by hhl_build_program and the host-only hhl_schedule_dump.
+struct FuseChoice {
+    int kmax = 0;                 // fusion width used
+    double model_ms = 0.0;        // cost-model prediction of the chosen schedule
+};
+
+// Host part of the HHL program: logical circuit, product-state prefix folded into init factors,
+// fusion of the rest. fusion_kmax = 0 (default): the a2 cost model (compile.cpp schedule_cost_ms)
+// picks the width among 1..5 by scheduling each candidate for this state (nloc local qubits, initial
+// layout phys) and predicting its B200 time. Shared by hhl_build_program and hhl_schedule_dump.
 static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options *opt,
-                                         std::vector<ProductFactor> &factors, size_t *n_logical) {
+                                         std::vector<ProductFactor> &factors, size_t *n_logical,
+                                         const CompileOptions &co, int nloc, FuseChoice *choice) {
     std::vector<Gate> gates = hhl_build(p, opt ? opt->qpe_mode : 0);
     prof_mark("hhl_build");
     const bool fold = !opt || opt->init_fold >= 0;
@@ -425,7 +435,40 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     if (opt && (opt->fusion_mode < 0 || opt->fusion_mode > 1)) fail(SV_E_ARG, "fusion_mode must be 0 or 1");
     if (opt) fo.mode = opt->fusion_mode;
     if (n_logical) *n_logical = gates.size();
-    return fuse(rest, fo);
+    std::vector<int> phys(p.n);
+    for (int q = 0; q < p.n; q++) phys[q] = q;
+    if (!co.phys_init.empty()) phys = co.phys_init;
+    CompileOptions cc = co;
+    if (cc.tile_qubits > 12) cc.tile_qubits = 12;
+    const bool auto_k = (!opt || opt->fusion_kmax == 0) && fo.mode == 0;
+    if (!auto_k) {
+        std::vector<Gate> f = fuse(rest, fo);
+        if (choice) {
+            choice->kmax = fo.kmax;
+            choice->model_ms = schedule_cost_ms(compile(f, factors.empty() ? nullptr : &factors, p.n, nloc, phys, cc), nloc);
+        }
+        return f;
+    }
+    std::vector<Gate> best;
+    double best_ms = INFINITY;
+    int best_k = 1;
+    for (int k = 1; k <= 5; k++) {
+        FuseOptions fk = fo;
+        fk.kmax = k;
+        std::vector<Gate> f = fuse(rest, fk);
+        const double ms = schedule_cost_ms(compile(f, factors.empty() ? nullptr : &factors, p.n, nloc, phys, cc), nloc);
+        if (ms < best_ms * (1.0 - 1e-9)) {      // ties: the narrower width
+            best_ms = ms;
+            best_k = k;
+            best = std::move(f);
+        }
+    }
+    prof_mark("fusion width (cost model)");
+    if (choice) {
+        choice->kmax = best_k;
+        choice->model_ms = best_ms;
+    }
+    return best;
 }
 
 // Initial physical layout of a SHARDED eigenbasis HHL program, g global
@@ -461,10 +504,11 @@ static sv_program *build_hhl(sv_state *sv, const HHLPlanHost &p, const hhl_optio
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
     std::vector<ProductFactor> factors;
     size_t n_logical = 0;
-    std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
+    const CompileOptions hco = hhl_compile_opts(opt, &p, sv->n - sv->nloc);
+    FuseChoice fc;
+    std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical, hco, sv->nloc, &fc);
     prof_mark("fold + fuse");
-    sv_program *prog = program_create(sv, fused, &factors, hhl_compile_opts(opt, &p, sv->n - sv->nloc),
-                                      n_logical);
+    sv_program *prog = program_create(sv, fused, &factors, hco, n_logical);
     prof_mark("program_create");
     if (rep) {
         report_plan(rep, p);
@@ -475,6 +519,8 @@ static sv_program *build_hhl(sv_state *sv, const HHLPlanHost &p, const hhl_optio
         rep->pass_bytes = prog->sched.pass_bytes;
         rep->h2d_bytes = prog->h2d_bytes;
         rep->d2h_bytes = 16.0 * (double)(1ull << p.n_b) + 8.0;
+        rep->fusion_kmax_used = fc.kmax;
+        rep->model_ms = fc.model_ms;
         rep->t_frontend_s = now_s() - t0;
     }
     return prog;
@@ -524,7 +570,8 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
         if (p.n - g < 1) fail(SV_E_ARG, "too many ranks for this system");
         std::vector<ProductFactor> factors;
         size_t n_logical = 0;
-        std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical);
+        FuseChoice fc;
+        std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical, hhl_compile_opts(opt, &p, g), p.n - g, &fc);
         // rank 0's program exactly as hhl_build_program creates it, on a host-only stand-in state
         // (no device memory): same schedule, same lowering, same generated tile passes
         sv_state host{};
@@ -558,6 +605,8 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
             rep->n_passes = s.n_passes;
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
+            rep->fusion_kmax_used = fc.kmax;
+            rep->model_ms = fc.model_ms;
         }
         if (buf && buf_len) {
             std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s) + jitlog;

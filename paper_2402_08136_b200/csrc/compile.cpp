@@ -515,6 +515,51 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     return s;
 }
 
+// ------------------------------------------------------------- cost model ----
+// predicted time of a schedule on the B200, used to choose the fusion width.
+// Per step: max(HBM bytes / HBM bandwidth, FP64 flops / FP64 peak) + the shared-memory round trips of
+// its register phases (each moves the tile twice through shared memory, 32 B per amplitude at the
+// SMs' aggregate shared-memory bandwidth) + a launch; exchanges at NVLink bandwidth.
+// Flops per amplitude: a Hadamard-like real 2x2 runs as an unscaled butterfly (2), a k-qubit dense op
+// 8·2^k (4·2^k real), a diagonal 6, the reciprocal rotation ~8; controls scale by 2^-c.
+static double op_flops(const Gate &g) {
+    switch (g.kind) {
+        case Kind::Dense:
+        case Kind::Controlled: {
+            bool real = true;
+            for (auto &z : g.data) real &= z.imag() == 0.0;
+            const size_t k = g.targets.size();
+            if (k == 1 && real && g.data.size() == 4 && g.data[0] == g.data[1] && g.data[0] == g.data[2] &&
+                g.data[3] == -g.data[0])
+                return 2.0 * std::ldexp(1.0, -(int)g.controls.size());
+            return (real ? 4.0 : 8.0) * std::ldexp(1.0, (int)k) * std::ldexp(1.0, -(int)g.controls.size());
+        }
+        case Kind::Diagonal: return 6.0;
+        case Kind::RecipRY: return 8.0;
+        default: return 0.0;
+    }
+}
+
+double schedule_cost_ms(const Schedule &s, int nloc) {
+    const double amps = std::ldexp(1.0, nloc);
+    const double hbm = 6.5e12, fp64 = 37.0e12, smem = 37.0e12, nvlink = 770e9, launch = 5e-6;
+    double t = 0.0;
+    for (const Step &st : s.steps) {
+        double fl = 0.0;
+        for (const Gate &g : st.tile_ops) fl += op_flops(g) * amps;
+        switch (st.kind) {
+            case StepKind::Exchange: t += st.bytes / nvlink + launch; break;
+            case StepKind::Tile: {
+                const double xch = st.phase_R.empty() ? 0.0 : (double)(st.phase_R.size() - 1);
+                t += std::max(st.bytes / hbm, fl / fp64) + xch * 32.0 * amps / smem + launch;
+                break;
+            }
+            default: t += std::max(st.bytes / hbm, fl / fp64) + launch; break;
+        }
+    }
+    return t * 1e3;
+}
+
 std::string dump_schedule(const Schedule &s) {
     std::ostringstream os;
     auto bits = [&](const std::vector<int> &v) {

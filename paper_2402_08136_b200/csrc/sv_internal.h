@@ -171,5 +171,7 @@ struct Schedule {
 Schedule compile(const std::vector<Gate> &ops, const std::vector<ProductFactor> *init, int n, int nloc,
                  const std::vector<int> &phys_in, const CompileOptions &o);
 std::string dump_schedule(const Schedule &s);
+// SURVEY §8(a) a2 cost model: predicted B200 time (ms) of a schedule of an nloc-qubit (local) state.
+double schedule_cost_ms(const Schedule &s, int nloc);
 
 }  // namespace hhlsv

@@ -67,7 +67,8 @@ class hhl_report(ctypes.Structure):
                 ("n_passes", ctypes.c_uint64), ("alg_bytes", ctypes.c_double), ("pass_bytes", ctypes.c_double),
                 ("t_frontend_s", ctypes.c_double), ("t_sim_s", ctypes.c_double), ("h2d_bytes", ctypes.c_double),
                 ("d2h_bytes", ctypes.c_double), ("x_offset", ctypes.c_int), ("n_orig", ctypes.c_int),
-                ("b_norm", ctypes.c_double), ("p_anc1", ctypes.c_double)]
+                ("b_norm", ctypes.c_double), ("p_anc1", ctypes.c_double), ("fusion_kmax_used", ctypes.c_int),
+                ("model_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -230,3 +230,18 @@ def test_paper_mode_fusion_counts():
     assert 1 - rp["n_fused"] / rp["n_logical"] >= 0.60          # SPEC acceptance 4: >= 60 % reduction
     with pytest.raises(pkg.SVError):
         pkg.schedule_dump(p.n, t, fusion_mode=3)
+
+
+def test_cost_model_fusion_width():
+    """SURVEY §8(a) a2 cost model (fusion_kmax = 0): with tile passes the predicted time grows with the
+    fusion width (wider dense matrices only add FP64 work once many ops share an HBM pass), so k = 1
+    is chosen; one HBM pass per op (tile_qubits = -1) favours wider fusion up to the FP64 bound (k = 4:
+    k = 5 is FP64-bound). The report carries the choice and the prediction."""
+    A, b, nc = configs.get("S30")
+    _, r = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, qpe_mode=1, tile_qubits=12)
+    assert r["fusion_kmax_used"] == 1 and r["model_ms"] > 0
+    ks = [pkg.hhl_schedule_dump(A, b, clock_qubits=nc, qpe_mode=1, tile_qubits=12, fusion_kmax=k)[1]["model_ms"]
+          for k in (1, 2, 3)]
+    assert ks[0] == r["model_ms"] and ks[0] < ks[1] < ks[2]
+    _, rs = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, qpe_mode=1, tile_qubits=-1)
+    assert rs["fusion_kmax_used"] == 4
