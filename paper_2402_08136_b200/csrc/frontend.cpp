@@ -77,8 +77,8 @@ Gate gate_from_abi(const sv_gate &a, int n) {
     g.kind = (Kind)a.kind;
     if (a.n_targets < 1 || (a.n_targets > 0 && !a.targets)) fail(SV_E_ARG, "gate needs targets");
     if (a.n_controls < 0 || (a.n_controls > 0 && !a.controls)) fail(SV_E_ARG, "bad controls");
-    g.targets.assign(a.targets, a.targets + a.n_targets);
-    if (a.n_controls > 0) g.controls.assign(a.controls, a.controls + a.n_controls);
+    for (int i = 0; i < a.n_targets; i++) g.targets.push_back(a.targets[i]);
+    for (int i = 0; i < a.n_controls; i++) g.controls.push_back(a.controls[i]);
     g.cvals = a.control_values;
     std::vector<int> all = g.targets;
     all.insert(all.end(), g.controls.begin(), g.controls.end());
