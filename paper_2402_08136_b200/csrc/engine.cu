@@ -1153,7 +1153,22 @@ void program_run(sv_state *sv, sv_program *p) {
     if (!p->resets && sv->phys != p->phys_in) fail(SV_E_ARG, "qubit map changed since the program was created");
     if (!p->subs.empty()) {             // virtual sharding: step-interleaved over the shards
         const size_t ns = p->subs[0]->recs.size();
+        sv_program *t0 = p->subs[0];     // timing: one event pair per step, spanning every shard's launches
+        if (p->timing && t0->ev.size() != 2 * ns) {
+            for (auto e : t0->ev) cudaEventDestroy(e);
+            t0->ev.assign(2 * ns, nullptr);
+            for (auto &e : t0->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        }
         for (size_t i = 0; i < ns; i++) {
+            if (p->timing) cuda_check(cudaEventRecord(t0->ev[2 * i], sv->stream), "event");
+            struct EndEv {
+                sv_program *p, *t0;
+                sv_state *sv;
+                size_t i;
+                ~EndEv() {
+                    if (p->timing) cudaEventRecord(t0->ev[2 * i + 1], sv->stream);
+                }
+            } end_ev{p, t0, sv, i};
             if (p->subs[0]->recs[i].kind == StepKind::Exchange) {
                 virtual_exchange(sv, p->subs[0]->recs[i].xg, p->subs[0]->recs[i].xl);
                 continue;
@@ -1284,6 +1299,30 @@ void program_run(sv_state *sv, sv_program *p) {
 
 void program_timings(sv_program *p, float *ms, int *kind, double *bytes, double *flops, int *launches, size_t cap,
                      size_t *n_out) {
+    if (!p->subs.empty()) {      // virtual shards: per step over all shards (bytes / flops / launches summed)
+        sv_program *t0 = p->subs[0];
+        if (!p->timing || t0->ev.size() != 2 * t0->recs.size()) fail(SV_E_ARG, "timing not enabled or program not run");
+        cuda_check(cudaStreamSynchronize(p->sv->stream), "timings sync");
+        const size_t n = std::min(cap, t0->recs.size());
+        for (size_t i = 0; i < n; i++) {
+            float t = 0.0f;
+            cuda_check(cudaEventElapsedTime(&t, t0->ev[2 * i], t0->ev[2 * i + 1]), "elapsed");
+            if (ms) ms[i] = t;
+            if (kind) kind[i] = (int)t0->recs[i].kind;
+            double by = 0, fl = 0;
+            int la = 0;
+            for (size_t r = 0; r < p->subs.size(); r++) {
+                by += p->subs[r]->recs[i].bytes;
+                fl += p->subs[r]->recs[i].flops;
+                la += rec_launches(p->subs[r]->sv, p->subs[r]->recs[i]);
+            }
+            if (bytes) bytes[i] = by;
+            if (flops) flops[i] = fl;
+            if (launches) launches[i] = la;
+        }
+        if (n_out) *n_out = t0->recs.size();
+        return;
+    }
     if (!p->timing || p->ev.size() != 2 * p->recs.size()) fail(SV_E_ARG, "timing not enabled or program not run");
     cuda_check(cudaStreamSynchronize(p->sv->stream), "timings sync");
     const size_t n = std::min(cap, p->recs.size());
