@@ -44,6 +44,10 @@ t30 = run("S30", 1)
 T30 = sum(x[0] for x in t30)
 print(json.dumps({"workload": "S30", "world": 1, "ms": T30, "steps": [round(x[0], 3) for x in t30]}), flush=True)
 for cfg, world in (("S31", 2), ("S32", 4), ("S33", 8)):
+    # the same circuit on ONE GPU (S33 = 128 GiB fits in 180 GB): separates the sharding overhead from the
+    # circuit's growth with the clock register (per-amplitude work rises with n_clock)
+    t1 = run(cfg, 1)
+    T1 = sum(x[0] for x in t1)
     t = run(cfg, world)
     passes = [(ms / world, kind, by) for ms, kind, by, la, fl in t if kind != 6]
     ex = [(ms, by) for ms, kind, by, la, fl in t if kind == 6]
@@ -60,5 +64,6 @@ for cfg, world in (("S31", 2), ("S32", 4), ("S33", 8)):
     print(json.dumps({"workload": cfg, "world": world, "per_rank_pass_ms": per_rank,
                       "virtual_exchange_ms": [round(e[0], 3) for e in ex], "modelled_nvlink_ms": round(xfer, 3),
                       "projected_ms_per_rank": round(proj, 3), "projected_weak_scaling_E": round(T30 / proj, 3),
+                      "one_gpu_ms": round(T1, 3), "projected_speedup_vs_one_gpu": round(T1 / proj, 3),
                       "how": "per-rank passes measured (virtual shards, one GPU), exchange modelled at 770 GB/s "
                              "and overlapped with the pass before it"}), flush=True)
