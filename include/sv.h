@@ -195,6 +195,13 @@ sv_status sv_program_timings(sv_program *prog, float *ms, int *kind, double *byt
 /* Number of kernel launches one sv_program_run makes on this rank, and the host->device
  * bytes uploaded when the program was created. */
 sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_bytes);
+/* Fused readout (single-GPU HHL programs; SURVEY §8 a8 (ii) for the ancilla, "P(measure
+ * ancilla and get 1)"): the program's last tile pass accumulates sum |a|^2 split by the ancilla while it
+ * stores the final state, so no separate full-state read is needed. out[0] / out[1] = P(ancilla = 0 / 1)
+ * of the last run (their sum is the norm); deterministic (fixed grid, fixed summation order).
+ * Synchronises the library stream. SV_E_ARG if the program has no fused marginal (sharded state,
+ * no JIT passes, or a program not built by hhl_build_program); use sv_probabilities then. */
+sv_status sv_program_marginal(sv_program *prog, double *out2);
 
 /* HOST-ONLY planning (no GPU needed): fuse + schedule a LOGICAL gate list for an n-qubit
  * state sharded over `world` ranks (power of two), and dump the schedule text. Used to test
@@ -257,6 +264,10 @@ typedef struct {
     const double *eig_lambda;
     const double *eig_vectors;
     int fusion_mode;    /* as sv_fuse_options.fusion_mode */
+    int fused_marginal; /* hhl_build_program: 1 -> the program's last tile pass also accumulates P(ancilla) while
+                           it stores the final state (sv_program_marginal; single GPU, NVRTC passes; costs
+                           ~1 % of the run); 0 (default) -> not. hhl_solve always fuses it when it can (it
+                           replaces the separate full-state read of the readout). */
 } hhl_options;
 
 typedef struct {

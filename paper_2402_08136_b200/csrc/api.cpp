@@ -296,6 +296,17 @@ sv_status sv_program_stats(sv_program *prog, uint64_t *launches, uint64_t *h2d_b
     });
 }
 
+sv_status sv_program_marginal(sv_program *prog, double *out2) {
+    return guard([&] {
+        if (!prog || !out2) fail(SV_E_ARG, "null argument");
+        if (!prog->d_mred) fail(SV_E_ARG, "program has no fused marginal");
+        cuda_check(cudaMemcpyAsync(out2, prog->d_mred + 2 * sv_program::kMredCtas, 2 * sizeof(double),
+                                   cudaMemcpyDeviceToHost, prog->sv->stream),
+                   "marginal d2h");
+        cuda_check(cudaStreamSynchronize(prog->sv->stream), "marginal sync");
+    });
+}
+
 // Host-only: generate + NVRTC-compile every tile pass of a schedule; one log line per pass.
 sv_status sv_schedule_dump(int n_qubits, int world, const sv_gate *gates, size_t n_gates, const sv_fuse_options *opt,
                            char *buf, size_t buf_len, sv_plan_report *rep) {
@@ -490,21 +501,24 @@ static std::vector<int> hhl_layout(const HHLPlanHost &p, const hhl_options *opt,
     return phys;
 }
 
-static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost *p = nullptr, int g = 0) {
+static CompileOptions hhl_compile_opts(const hhl_options *opt, const HHLPlanHost *p = nullptr, int g = 0,
+                                       bool marginal = false) {
     CompileOptions co;
     if (opt && opt->tile_qubits != 0) co.tile_qubits = opt->tile_qubits;
     if (opt) co.jit = opt->tile_jit;
     if (p) co.phys_init = hhl_layout(*p, opt, g);
+    // single-GPU programs: the last tile pass also accumulates P(ancilla) (hhl_report.p_anc1, norm2)
+    if (p && g == 0 && (marginal || (opt && opt->fused_marginal))) co.red_qubit = p->n - 1;
     return co;
 }
 
 static sv_program *build_hhl(sv_state *sv, const HHLPlanHost &p, const hhl_options *opt, hhl_report *rep,
-                             double t0) {
+                             double t0, bool marginal = false) {
     prof_mark("build_hhl start");
     if (p.n != sv->n) fail(SV_E_ARG, "state has the wrong number of qubits for this system (use hhl_plan_size)");
     std::vector<ProductFactor> factors;
     size_t n_logical = 0;
-    const CompileOptions hco = hhl_compile_opts(opt, &p, sv->n - sv->nloc);
+    const CompileOptions hco = hhl_compile_opts(opt, &p, sv->n - sv->nloc, marginal);
     FuseChoice fc;
     std::vector<Gate> fused = hhl_fused_gates(p, opt, factors, &n_logical, hco, sv->nloc, &fc);
     prof_mark("fold + fuse");
@@ -646,17 +660,25 @@ sv_status hhl_solve(const double *A, const double *b, int N, int clock_qubits, c
         sv_program *prog = nullptr;
         try {
             hhl_report r{};
-            prog = build_hhl(sv, p, &o, &r, now_s() - t_plan);      // front end = plan + build
+            prog = build_hhl(sv, p, &o, &r, now_s() - t_plan, true);      // front end = plan + build
             const double t0 = now_s();
             program_run(sv, prog);
             if (prof_on()) {
                 cudaStreamSynchronize(sv->stream);
                 prof_mark("  program_run");
             }
-            // one reduction gives the norm and P(ancilla = 1) (logical qubit n-1)
+            // norm and P(ancilla = 1) (logical qubit n-1): fused into the last tile pass when the program
+            // has it (single GPU, JIT), else one marginal reduction over the state
             double pa[2] = {0.0, 0.0};
             const int anc = p.n - 1;
-            state_probabilities(sv, &anc, 1, pa);
+            if (prog->d_mred) {
+                cuda_check(cudaMemcpyAsync(pa, prog->d_mred + 2 * sv_program::kMredCtas, sizeof pa,
+                                           cudaMemcpyDeviceToHost, sv->stream),
+                           "marginal d2h");
+                cuda_check(cudaStreamSynchronize(sv->stream), "marginal sync");
+            } else {
+                state_probabilities(sv, &anc, 1, pa);
+            }
             r.norm2 = pa[0] + pa[1];
             r.p_anc1 = pa[1];
             prof_mark("  norm + P(ancilla)");

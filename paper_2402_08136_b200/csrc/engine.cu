@@ -954,6 +954,10 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                     p->sched.pass_bytes += rec.bytes - before;
                 }
                 a.rank_base = rank_base;
+                // fused marginal: only the last step, a single-launch JIT pass over the whole (unsharded) state
+                if (co.red_qubit >= 0 && co.red_qubit < sv->n && use_jit && jit_config().mred && si + 1 == steps.size() && sv->g == 0 &&
+                    a.nlift == 0)
+                    a.red = p->sched.phys_out[co.red_qubit];
                 size_t ph0 = 0, opbase = 0;
                 lower_tile_step(st, a, blob, rops, phases, ph0, opbase, use_jit, pending_scale);
                 pending_scale = 1.0;
@@ -1054,6 +1058,12 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         if (rec.kind == StepKind::Diagonal) rec.diag.table = p->d_blob + (size_t)rec.diag.table;
     }
     prof_mark("  lower + upload");
+    for (const LaunchRec &r : p->recs)
+        if (r.kind == StepKind::Tile && r.jit >= 0 && r.tile.red >= 0) {
+            cuda_check(pool_malloc((void **)&p->d_mred, sizeof(double) * (2 * sv_program::kMredCtas + 2), us),
+                       "cudaMalloc(marginal partials)");
+            p->jit[r.jit].red = p->d_mred;
+        }
     if (!p->jit.empty()) jit_build(p->jit);
     prof_mark("  jit_build");
     for (auto &t : tiles) {
@@ -1066,6 +1076,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
 
 static int rec_launches(const sv_state *sv, const LaunchRec &r) {
     if (r.skip) return 0;
+    if (r.kind == StepKind::Tile && r.jit >= 0 && r.tile.red >= 0) return 2;     // + the partials' sum
     if (r.kind != StepKind::Exchange) return 1;
     const XPlan x = xplan(sv, sv->rank, r.xg, r.xl);
     const uint64_t C = xchunk(x);
@@ -1128,6 +1139,19 @@ static void exchange_slot(sv_state *sv, const XPlan &x, uint32_t p, cudaStream_t
     }
 }
 
+// One JIT tile pass over all its tiles; a pass with the fused marginal also sums its CTA partials.
+static void launch_jit_rec(sv_state *sv, sv_program *p, const LaunchRec &r) {
+    const JitPass &jp = p->jit[r.jit];
+    cuda_check(jit_launch(jp, r.tile.psi, r.tile.blob, r.tile.n_tiles, r.tile.rank_base, r.tile.T, sv->stream),
+               "tile (jit)");
+    if (jp.red) {
+        const uint64_t grid = jit_grid(jp, r.tile.n_tiles);
+        if (grid > (uint64_t)sv_program::kMredCtas) fail(SV_E_CUDA, "fused marginal: launch grid too large");
+        cuda_check(dev::launch_pair_sum(jp.red, (int)grid, jp.red + 2 * sv_program::kMredCtas, sv->stream),
+                   "marginal partial sum");
+    }
+}
+
 static void launch_rec(sv_state *sv, sv_program *p, const LaunchRec &r) {
     if (r.skip) return;
     switch (r.kind) {
@@ -1138,9 +1162,7 @@ static void launch_rec(sv_state *sv, sv_program *p, const LaunchRec &r) {
         case StepKind::RecipRY: cuda_check(dev::launch_recip(r.recip, sv->stream), "recip_ry"); break;
         case StepKind::Tile:
             if (r.jit >= 0)
-                cuda_check(jit_launch(p->jit[r.jit], r.tile.psi, r.tile.blob, r.tile.n_tiles, r.tile.rank_base, r.tile.T,
-                                      sv->stream),
-                           "tile (jit)");
+                launch_jit_rec(sv, p, r);
             else
                 cuda_check(dev::launch_tile(r.tile, sv->stream), "tile");
             break;
@@ -1283,9 +1305,7 @@ void program_run(sv_state *sv, sv_program *p) {
             case StepKind::RecipRY: cuda_check(dev::launch_recip(r.recip, sv->stream), "recip_ry"); break;
             case StepKind::Tile:
                 if (r.jit >= 0)
-                    cuda_check(jit_launch(p->jit[r.jit], r.tile.psi, r.tile.blob, r.tile.n_tiles, r.tile.rank_base,
-                                          r.tile.T, sv->stream),
-                               "tile (jit)");
+                    launch_jit_rec(sv, p, r);
                 else
                     cuda_check(dev::launch_tile(r.tile, sv->stream), "tile");
                 break;
@@ -1346,6 +1366,7 @@ void program_destroy(sv_program *p) {
     pool_free(p->d_ops, p->sv ? p->sv->stream : nullptr);
     pool_free(p->d_phases, p->sv ? p->sv->stream : nullptr);
     for (auto *d : p->d_tabs) pool_free(d, p->sv ? p->sv->stream : nullptr);
+    pool_free(p->d_mred, p->sv ? p->sv->stream : nullptr);
     for (auto e : p->ev) cudaEventDestroy(e);
     if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
     if (p->graph) cudaGraphDestroy(p->graph);

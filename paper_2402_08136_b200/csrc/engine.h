@@ -76,6 +76,10 @@ struct sv_program {
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t gstream = nullptr;
     cudaEvent_t gev_a = nullptr, gev_b = nullptr;
+    // fused marginal of the last tile pass (CompileOptions::red_qubit): per-CTA partials, then
+    // d_mred[2 * kMredCtas + {0, 1}] = P(qubit = 0 / 1) after every run; nullptr = not fused
+    double *d_mred = nullptr;
+    static constexpr int kMredCtas = 148 * 32;
     uint64_t launches() const;
 };
 

@@ -226,6 +226,7 @@ const JitConfig &jit_config() {
             else if (key == "ctabbits") x.ctab_bits = std::max(0, std::min(6, iv));
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
+            else if (key == "mred") x.mred = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
@@ -480,11 +481,17 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         return c;
     };
     if (cfg.min_blocks > 0) min_blocks = cfg.min_blocks;
+    // Fused marginal (a.red >= 0): while the pass stores the final amplitudes each thread accumulates
+    // Σ|a|² split by physical bit a.red (q0: bit 0, q1: bit 1) over all its tiles; at the end the CTA
+    // combines its threads in a fixed order and writes red[2 blockIdx.x + {0, 1}] (summed by
+    // k_pair_sum). Saves the readout's separate full-state read (16 B/amplitude).
+    const bool red = a.red >= 0;
+    const std::string rbs = std::to_string(a.red);
     std::ostringstream k;
     if (ctot) k << "struct CWArg { double2 w[" << ctot << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base, u64 tile0"
-      << (ctot ? ", const CWArg cwa" : "") << ") {\n";
+      << (red ? ", double *__restrict__ red" : "") << (ctot ? ", const CWArg cwa" : "") << ") {\n";
     k << "  constexpr u32 NT = " << (1u << T) << "u;\n";
     k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
     k << "  const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);\n";
@@ -581,6 +588,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             return any_run;
         };
     k << "  u64 tile = tile0 + blockIdx.x;      // tiles [tile0, n_tiles) of the pass\n";
+    if (red) k << "  double q0 = 0.0, q1 = 0.0;      // fused marginal over bit " << a.red << "\n";
     if (hoist) {
         k << "  if (tile < n_tiles) {\n";
         emit_pre(0, "rank_base | tile_base(tile)");
@@ -1110,11 +1118,18 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         if (p + 1 == ph.size() && dout) {
             k << "      double2 *gout = psi + (base | pd_out);\n";
+            if (red) k << "      double r0 = 0.0, r1 = 0.0;\n";
             for (int j = 0; j < RA; j++) {
                 if ((uint32_t)rd[j] & a.zstore) continue;          // still known zero: not written
-                k << "      " << (a.zstore ? "if (!(tb & " + std::to_string(a.zstore) + "u)) " : std::string())
-                  << "__stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+                const std::string zc = a.zstore ? "if (!(tb & " + std::to_string(a.zstore) + "u)) " : std::string();
+                k << "      " << zc << "__stcs(gout + " << u64s(phys_slot(P, j)) << ", v" << j << ");\n";
+                if (red)      // slot offsets with the bit set go to r1; the rest follow (base | pd_out)'s bit
+                    k << "      " << zc << ((phys_slot(P, j) >> a.red) & 1 ? "r1" : "r0") << " = fma(v" << j << ".x, v"
+                      << j << ".x, fma(v" << j << ".y, v" << j << ".y, " << ((phys_slot(P, j) >> a.red) & 1 ? "r1" : "r0")
+                      << "));\n";
             }
+            if (red)
+                k << "      if (((base | pd_out) >> " << rbs << ") & 1ull) q1 += r0 + r1; else { q0 += r0; q1 += r1; }\n";
             hoisted();
             k << "    }\n";
         } else {
@@ -1125,15 +1140,28 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         }
     }
     if (!dout) {
-        if (a.zstore)
-            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") if (!(u & " << a.zstore
-              << "u)) psi[addr(base, u)] = cur[swz(u)];\n";
+        const std::string zc = a.zstore ? "if (!(u & " + std::to_string(a.zstore) + "u)) " : std::string();
+        if (red)
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") " << zc
+              << "{ const u64 ad = addr(base, u); const double2 x = cur[swz(u)]; psi[ad] = x; const double w = "
+                 "fma(x.x, x.x, x.y * x.y); if ((ad >> "
+              << rbs << ") & 1ull) q1 += w; else q0 += w; }\n";
         else
-            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") psi[addr(base, u)] = cur[swz(u)];\n";
+            k << "    for (u32 u = threadIdx.x; u < NT; u += " << NTHR << ") " << zc << "psi[addr(base, u)] = cur[swz(u)];\n";
     }
     // one barrier per tile: the next tile's first shared-memory write (cp.async, phase-0 stores,
     // diagonal sub-tables) must not overtake a slower warp still reading this tile's last phase
-    k << "    bar();\n  }\n  cp_async_wait0();\n}\n";
+    k << "    bar();\n  }\n  cp_async_wait0();\n";
+    if (red) {      // every thread left the loop after the last tile's barrier: the tile buffer is free
+        const int g = NTHR >= 16 ? 16 : NTHR;
+        k << "  buf0[threadIdx.x] = mk(q0, q1);\n  bar();\n";
+        k << "  if (threadIdx.x < " << g << "u) { double s0 = 0.0, s1 = 0.0; for (u32 i = threadIdx.x; i < " << NTHR
+          << "u; i += " << g << "u) { const double2 t = buf0[i]; s0 += t.x; s1 += t.y; } buf0[" << NTHR
+          << "u + threadIdx.x] = mk(s0, s1); }\n  bar();\n";
+        k << "  if (threadIdx.x == 0) { double s0 = 0.0, s1 = 0.0; for (u32 i = 0; i < " << g << "u; i++) { const double2 t = buf0["
+          << NTHR << "u + i]; s0 += t.x; s1 += t.y; } red[2ull * blockIdx.x] = s0; red[2ull * blockIdx.x + 1ull] = s1; }\n";
+    }
+    k << "}\n";
     return k.str();
 }
 
@@ -1293,8 +1321,17 @@ cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint
     if (tile0 >= n_tiles) return cudaSuccess;
     uint64_t grid = (uint64_t)p.sms * p.per_sm;
     if (grid > n_tiles - tile0) grid = n_tiles - tile0;
-    void *args[] = {&psi, (void *)&blob, &n_tiles, &rank_base, &tile0, (void *)p.cwvals.data()};
+    double *red = p.red;
+    void *args[7] = {&psi, (void *)&blob, &n_tiles, &rank_base, &tile0};
+    int na = 5;
+    if (red) args[na++] = &red;
+    args[na++] = (void *)p.cwvals.data();
     return cudaLaunchKernel(f, dim3((unsigned)grid), dim3(threads), args, smem, s);
+}
+
+uint64_t jit_grid(const JitPass &p, uint64_t n_tiles) {
+    const uint64_t g = (uint64_t)p.sms * p.per_sm;
+    return g < n_tiles ? g : n_tiles;
 }
 
 }  // namespace hhlsv

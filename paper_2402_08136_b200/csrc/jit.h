@@ -24,6 +24,8 @@ struct JitPass {
     // launch configuration, resolved on the first launch (attribute + occupancy queries are host
     // work a launch-bound small program should not repeat)
     mutable int per_sm = 0, sms = 0;
+    // fused marginal (TileArgs::red >= 0): device buffer of 2 doubles per CTA of the launch grid
+    double *red = nullptr;
 };
 
 // Product-state init fused into the first tile pass: the pass computes its tile's amplitudes
@@ -62,6 +64,7 @@ struct JitConfig {
     int diag_merge = -1;      // dmerge: in-phase diagonal merge width (-1 = CompileOptions::diag_merge)
     int eigen_chunk = 0;      // echunk: clock bits per eigen-phase table (0 = front-end default)
     bool init_fuse = true;    // initfuse: product-state init computed inside the first tile pass
+    bool mred = true;         // mred: the last tile pass accumulates the HHL ancilla marginal (fused readout)
 };
 const JitConfig &jit_config();
 
@@ -78,6 +81,8 @@ std::string jit_source_tag(const std::string &src);
 // Launch tiles [tile0, n_tiles) of a pass (tile0 = 0: the whole pass).
 cudaError_t jit_launch(const JitPass &p, double2 *psi, const double2 *blob, uint64_t n_tiles, uint64_t rank_base,
                        int T, cudaStream_t s, uint64_t tile0 = 0);
+// CTAs jit_launch uses for tiles [0, n_tiles) (after the pass's first launch resolved its occupancy).
+uint64_t jit_grid(const JitPass &p, uint64_t n_tiles);
 size_t jit_smem_bytes(int T, size_t extra);
 
 }  // namespace hhlsv

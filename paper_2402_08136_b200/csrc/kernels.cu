@@ -632,6 +632,27 @@ __global__ void k_marginal_final(const double *ws, int logC, uint64_t nbins, dou
     }
 }
 
+__global__ void k_pair_sum(const double *part, int nblocks, double *out) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += 32) {
+        s0 += part[2 * i];
+        s1 += part[2 * i + 1];
+    }
+    for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (threadIdx.x == 0) {
+        out[0] = s0;
+        out[1] = s1;
+    }
+}
+
+cudaError_t launch_pair_sum(const double *part, int nblocks, double *out, cudaStream_t s) {
+    k_pair_sum<<<1, 32, 0, s>>>(part, nblocks, out);
+    return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(1024) k_marginal_final_blocks(const double *ws, int logC, double *out) {
     const uint64_t v = blockIdx.x;
     const uint64_t C = 1ull << logC;

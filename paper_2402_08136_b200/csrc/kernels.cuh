@@ -116,6 +116,10 @@ struct TileArgs {
     // (pipelined pass + exchange). nlift = 0: plain ascending mapping.
     int nlift = 0;
     int lift[8];
+    // Fused readout (JIT passes only): physical bit whose marginal the pass accumulates while it stores
+    // the final amplitudes (per-CTA partials Σ|a|² for bit = 0 / 1, DESIGN.md §6 "Fused marginal");
+    // -1 = none.
+    int red = -1;
 };
 
 // ---- launchers (stream-ordered, no sync) ----
@@ -129,6 +133,9 @@ size_t tile_smem_bytes(int T, int nops);
 
 // Deterministic reductions. partial has >= kRedBlocks doubles; result written to out (device).
 constexpr int kRedBlocks = 1184;   // 148 SMs x 8
+// Fixed-order sum of nblocks (bit 0, bit 1) partial pairs written by a tile pass with a fused marginal:
+// out[0] = Σ part[2i], out[1] = Σ part[2i + 1] (one warp; lane-strided then a shuffle tree).
+cudaError_t launch_pair_sum(const double *part, int nblocks, double *out, cudaStream_t s);
 cudaError_t launch_norm2(const double2 *psi, uint64_t n, double *partial, double *out, cudaStream_t s);
 // Marginal over physical bits S (q = |S| <= 26, bit j of v <- S[j]); others O = remaining local bits.
 // Writes 2^q doubles to out (device). ws must hold 2^q * C doubles (C returned by marginal_chunks).

@@ -56,7 +56,7 @@ class hhl_options(ctypes.Structure):
                 ("recip_snap", ctypes.c_double), ("init_fold", ctypes.c_int), ("tile_jit", ctypes.c_int),
                 ("diag_kmax", ctypes.c_int), ("qpe_mode", ctypes.c_int),
                 ("eig_lambda", ctypes.POINTER(ctypes.c_double)), ("eig_vectors", ctypes.POINTER(ctypes.c_double)),
-                ("fusion_mode", ctypes.c_int)]
+                ("fusion_mode", ctypes.c_int), ("fused_marginal", ctypes.c_int)]
 
 
 class hhl_report(ctypes.Structure):
@@ -78,7 +78,7 @@ EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_
            "sv_reset", "sv_info", "sv_dump", "sv_restore",
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
-           "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_schedule_dump", "sv_probabilities",
+           "sv_program_set_timing", "sv_program_timings", "sv_program_stats", "sv_program_marginal", "sv_schedule_dump", "sv_probabilities",
            "sv_norm2", "sv_postselect_slice", "sv_sample", "hhl_plan_size", "hhl_build_program", "hhl_readout", "hhl_solve",
            "hhl_schedule_dump"]
 
@@ -115,6 +115,7 @@ def load(path: str = LIB_PATH):
         "sv_program_timings": [vp, P(ctypes.c_float), P(c_int), P(c_dbl), P(c_dbl), P(c_int), ctypes.c_size_t,
                                P(ctypes.c_size_t)],
         "sv_program_stats": [vp, P(c_u64), P(c_u64)],
+        "sv_program_marginal": [vp, P(c_dbl)],
         "sv_schedule_dump": [c_int, c_int, P(sv_gate), ctypes.c_size_t, P(sv_fuse_options), ctypes.c_char_p,
                              ctypes.c_size_t, P(sv_plan_report)],
         "sv_probabilities": [vp, P(c_int), c_int, P(c_dbl)],
@@ -357,6 +358,13 @@ class Program:
         _check(load().sv_program_stats(self._h, ctypes.byref(la), ctypes.byref(h2d)))
         return {"launches": la.value, "h2d_bytes": h2d.value}
 
+    def marginal(self):
+        """(P(ancilla = 0), P(ancilla = 1)) of the last run, accumulated by the program's last tile pass
+        (single-GPU HHL programs; raises SVError otherwise)."""
+        out = (ctypes.c_double * 2)()
+        _check(load().sv_program_marginal(self._h, out))
+        return out[0], out[1]
+
     def destroy(self):
         if self._h:
             _check(load().sv_program_destroy(self._h))
@@ -389,10 +397,11 @@ class _Opts:
     """hhl_options plus the buffers its eig_* pointers reference (kept alive with it)."""
 
     def __init__(self, clock_qubits=0, fusion_kmax=0, tile_qubits=0, recip_snap=1e-5, init_fold=0, tile_jit=0,
-                 diag_kmax=0, qpe_mode=0, eig=None, fusion_mode=0):
+                 diag_kmax=0, qpe_mode=0, eig=None, fusion_mode=0, fused_marginal=0):
         self.o = hhl_options(int(clock_qubits), int(fusion_kmax), int(tile_qubits), float(recip_snap),
                              int(init_fold), int(tile_jit), int(diag_kmax), int(qpe_mode))
         self.o.fusion_mode = int(fusion_mode)
+        self.o.fused_marginal = int(fused_marginal)
         if eig is not None:          # (lambda, V): caller-supplied eigendecomposition of the padded A
             self.lam = np.ascontiguousarray(eig[0], dtype=np.float64)
             self.V = np.ascontiguousarray(eig[1], dtype=np.float64)

@@ -177,6 +177,7 @@ int main(int argc, char **argv) {
     g_smem_bytes = (size_t)atoll(argv[8]);
     const unsigned ncta = (unsigned)atoi(argv[9]);
     const bool lazy = strcmp(argv[1], "-") == 0;
+    std::vector<double> red_b(2 * ncta + 2, std::nan(""));   // fused-marginal partials (passes with red)
     double2 *psi;
     if (lazy) {
         g_psi_n = strtoull(argv[10], 0, 10);
@@ -216,6 +217,11 @@ int main(int argc, char **argv) {
     if (!lazy) { FILE *f = fopen(argv[2], "wb"); fwrite(psi, 16, g_psi_n, f); fclose(f); }
     printf("races %ld oob %ld double_writes %ld sync_mismatch %ld barriers %d\n", (long)g_races, (long)g_oob,
            (long)g_double, sync_err, bars[0]);
+    if (HAS_RED) {      // the CTA partials in launch order (the device sums them the same way)
+        double s0 = 0.0, s1 = 0.0;
+        for (unsigned c = 0; c < ncta; c++) { s0 += red_b[2 * c]; s1 += red_b[2 * c + 1]; }
+        fprintf(stderr, "RED %.17g %.17g\n", s0, s1);
+    }
     return 0;
 }
 '''
@@ -230,6 +236,8 @@ def _host_source(src: str) -> tuple[str, bool]:
     s = s.replace("double2 *__restrict__ psi", "double2 *psi").replace("const double2 *__restrict__ blob",
                                                                        "const double2 *blob")
     s = s.replace("psi[addr(base, u)] = cur[swz(u)];", "gstore(&psi[addr(base, u)], cur[swz(u)]);")
+    s = s.replace("psi[ad] = x;", "gstore(&psi[ad], x);")
+    s = s.replace("double *__restrict__ red", "double *red")
     has_cw = "const CWArg cwa" in s
     return s, has_cw
 
@@ -238,9 +246,10 @@ def build_pass(src: str) -> str:
     """Compile one pass source into an emulator executable (cached by content)."""
     os.makedirs(_BUILD_DIR, exist_ok=True)
     body, has_cw = _host_source(src)
-    call = ("hhlsv_tile(psi, blob, n_tiles, rank_base, 0ull, *(const CWArg *)cw_b.data())" if has_cw
-            else "hhlsv_tile(psi, blob, n_tiles, rank_base, 0ull)")
-    full = HOST_PRELUDE + body + MAIN.replace("KERNEL_CALL", call)
+    has_red = "double *red" in body
+    call = "hhlsv_tile(psi, blob, n_tiles, rank_base, 0ull" + (", red_b.data()" if has_red else "") + (
+        ", *(const CWArg *)cw_b.data())" if has_cw else ")")
+    full = HOST_PRELUDE + body + MAIN.replace("KERNEL_CALL", call).replace("HAS_RED", "true" if has_red else "false")
     tag = hashlib.sha1(full.encode()).hexdigest()[:16]
     exe = os.path.join(_BUILD_DIR, f"pass_{tag}")
     if not os.path.exists(exe):
@@ -307,6 +316,9 @@ def run_program(emu_dir: str, psi: np.ndarray, max_cta: int = 3):
             raise RuntimeError(f"emulated pass {i} failed ({out.returncode}):\n{out.stderr[-3000:]}")
         vals = dict(zip(out.stdout.split()[0::2], map(int, out.stdout.split()[1::2])))
         vals.update(T=T, n_tiles=n_tiles, ncta=ncta, log=out.stderr[-2000:])
+        for ln in out.stderr.splitlines():
+            if ln.startswith("RED "):
+                vals["red"] = tuple(float(x) for x in ln.split()[1:3])
         reports.append(vals)
         psi = np.fromfile(pout, dtype=np.complex128)
     return psi, reports

@@ -56,7 +56,7 @@ def check_postselection(st, p, psi_o):
 def test_bench_program_full_state(name, eig):
     A, b, nc = configs.get(name)
     xo, po, psi_o, p = ohhl.solve(A, b, nc)
-    kw = dict(BENCH, clock_qubits=nc)
+    kw = dict(BENCH, clock_qubits=nc, fused_marginal=1)
     if eig == "oracle":
         kw["eig"] = (p.lam, p.V)
     st = pkg.State(p.n)
@@ -73,6 +73,11 @@ def test_bench_program_full_state(name, eig):
     assert abs(ps - po) < max(1e-12, tol)
     assert np.abs(x - xo).max() < max(1e-10, 10 * tol)
     assert abs(st.norm2() - 1.0) < 1e-12
+    # fused marginal of the last tile pass vs the oracle's P(ancilla = 0 / 1) (logical qubit n-1)
+    h = 1 << (p.n - 1)
+    m = prog.marginal()
+    want = (float(np.sum(np.abs(psi_o[:h]) ** 2)), float(np.sum(np.abs(psi_o[h:]) ** 2)))
+    assert np.abs(np.array(m) - want).max() < max(1e-12, tol), (m, want)
 
 
 @pytest.fixture(scope="module")
@@ -101,7 +106,7 @@ def _read_blocks(st, p, B, khs):
 def test_bench_program_s30_blocks(s30_blocks, eig):
     """configs[3] = the bench workload, built exactly as bench.py builds it."""
     A, b, nc, p, B, khs, ref = s30_blocks
-    kw = dict(BENCH, clock_qubits=nc)
+    kw = dict(BENCH, clock_qubits=nc, fused_marginal=1)
     if eig == "oracle":
         kw["eig"] = (p.lam, p.V)
     st = pkg.State(p.n)
@@ -122,6 +127,10 @@ def test_bench_program_s30_blocks(s30_blocks, eig):
     x, ps = prog.readout()
     assert np.abs(x - p.b_norm * xt[: p.n_orig] / p.lam_min).max() < max(1e-10, 10 * tol)
     assert abs(st.norm2() - 1.0) < 1e-11
+    # the fused marginal (accumulated by the last pass) vs the separate marginal kernel over the state
+    m = prog.marginal()
+    assert abs(m[0] + m[1] - 1.0) < 1e-11
+    assert np.abs(np.array(m) - st.probabilities([p.n - 1])).max() < 1e-12
     prog.destroy()
     st.destroy()
 

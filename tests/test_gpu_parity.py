@@ -154,6 +154,8 @@ def test_hhl_solve_end_to_end(name):
     assert abs(rep["p_success"] - po) < 1e-12
     assert abs(rep["norm2"] - 1) < 1e-12
     assert np.abs(x - xo).max() < 1e-10
+    psi_o = ohhl.solve(A, b, nc)[2]
+    assert abs(rep["p_anc1"] - float(np.sum(np.abs(psi_o[1 << (p.n - 1):]) ** 2))) < 1e-12
 
 
 def test_table1_on_gpu():

@@ -45,12 +45,19 @@ def test_bench_program_c3_emulated(tmp_path):
     """The bench options on C3 (15 qubits): fused product init, lazy ancilla (pass 1 skips its tiles,
     pass 2 reads only its zero half), constant-bank tables, direct HBM phases; from NaN memory."""
     A, b, nc = configs.get("C3")
-    d, txt = _export(tmp_path, lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, **configs.BENCH_OPTS)[0])
+    d, txt = _export(tmp_path, lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, fused_marginal=1,
+                                                             **configs.BENCH_OPTS)[0])
     xo, po, psi_o, p = ohhl.solve(A, b, nc)
     out, reps = emu.run_program(d, np.full(1 << p.n, np.nan + 1j * np.nan))
     _clean(reps)
     assert len(reps) >= 2
     assert np.abs(emu.to_logical(out, emu.final_map(txt)) - psi_o).max() < 1e-12
+    # fused marginal of the last pass: P(ancilla = 0 / 1) accumulated while it stores the final state
+    # (the ancilla is logical qubit n-1: the upper half of the logical index space)
+    h = 1 << (p.n - 1)
+    want = (np.sum(np.abs(psi_o[:h]) ** 2), np.sum(np.abs(psi_o[h:]) ** 2))
+    assert "red" in reps[-1] and all("red" not in r for r in reps[:-1])
+    assert np.allclose(reps[-1]["red"], want, rtol=0, atol=1e-13), (reps[-1]["red"], want)
 
 
 def test_small_tile_wide_ops_emulated(tmp_path):
