@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 #include <mutex>
 
@@ -749,6 +750,14 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         return off;
     };
     struct Pending { size_t rec; size_t op0; size_t opbase; };
+    struct GenIn {               // what a JIT pass is generated from (kept for the spill fallback)
+        size_t jit;
+        dev::TileArgs a;
+        std::vector<dev::RegPhase> lph;
+        std::vector<dev::RegOp> lops;
+        bool init;
+    };
+    std::vector<GenIn> gen_in;
     std::vector<Pending> tiles;
     std::vector<size_t> blob_fix;     // recs whose pointer must be rebased (streaming data)
 
@@ -770,6 +779,14 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         p->sched.pass_bytes -= steps[0].bytes;                       // no separate init pass
         p->sched.pass_bytes -= 16.0 * (double)sv->local_amps();       // and the first pass reads nothing
     }
+    auto gen_pass = [&](JitPass &jp, const GenIn &gi, const JitVariant &v) {
+        jp.cwide.clear();
+        jp.cwvals.clear();
+        jp.src = gen_tile_kernel(jp.name, gi.a, gi.lph, gi.lops, &jp.smem_extra, gi.init ? &init_spec : nullptr,
+                                 &jp.cwide, &blob, v);
+        for (auto &c : jp.cwide)
+            jp.cwvals.insert(jp.cwvals.end(), blob.begin() + c.first, blob.begin() + c.first + c.second);
+    };
     // Known-zero ("lazy") qubits, JIT tile programs that start with a product init:
     // a qubit no init factor covers is |0> -- every amplitude with its bit set is 0 -- until the first
     // op that acts on it non-diagonally. If that op runs in a JIT tile pass of this program and every
@@ -964,17 +981,15 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 for (size_t oi = opbase; oi < rops.size(); oi++)
                     rec.flops += regop_flops(rops[oi]) * std::ldexp((double)sv->local_amps(), -a.nskip);
                 if (use_jit) {
-                    std::vector<dev::RegPhase> lph(phases.begin() + ph0, phases.end());
-                    std::vector<dev::RegOp> lops(rops.begin() + opbase, rops.end());
+                    GenIn gi{p->jit.size(), a, std::vector<dev::RegPhase>(phases.begin() + ph0, phases.end()),
+                             std::vector<dev::RegOp>(rops.begin() + opbase, rops.end()), fuse_init && si == 1};
                     JitPass jp;
                     jp.name = "hhlsv_tile";
                     jp.nthr = 1 << (a.T - a.nreg);
-                    jp.src = gen_tile_kernel(jp.name, a, lph, lops, &jp.smem_extra,
-                                             (fuse_init && si == 1) ? &init_spec : nullptr, &jp.cwide, &blob);
-                    for (auto &c : jp.cwide)
-                        jp.cwvals.insert(jp.cwvals.end(), blob.begin() + c.first, blob.begin() + c.first + c.second);
+                    gen_pass(jp, gi, JitVariant());
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
+                    gen_in.push_back(std::move(gi));
                 }
                 a.nphase = (int)(phases.size() - ph0);
                 tiles.push_back({p->recs.size(), ph0, opbase});
@@ -982,6 +997,33 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             }
         }
         p->recs.push_back(rec);
+    }
+    // Register-spill fallback: ptxas output of every pass is checked (in parallel; the cubins are kept
+    // for jit_build); a pass that spills is regenerated without constant-bank tables, then also without
+    // grouped diagonal factors, keeping the variant that spills least (S33 sharded pass 3: 376 B of
+    // spills, 18.6 -> 15.9 ms per rank; the S30 passes do not spill and are unchanged).
+    if (use_jit && jit_config().spillfb && !p->jit.empty()) {
+        std::vector<int> spill(p->jit.size(), 0);
+        std::vector<std::thread> th;
+        for (size_t i = 0; i < p->jit.size(); i++)
+            th.emplace_back([&, i] { spill[i] = jit_spill_bytes(p->jit[i].src); });
+        for (auto &t : th) t.join();
+        for (const GenIn &gi : gen_in) {
+            int best = spill[gi.jit];
+            if (best <= 0) continue;
+            for (const JitVariant v : {JitVariant{true, false}, JitVariant{true, true}}) {
+                JitPass alt;
+                alt.name = p->jit[gi.jit].name;
+                alt.nthr = p->jit[gi.jit].nthr;
+                gen_pass(alt, gi, v);
+                const int s2 = jit_spill_bytes(alt.src);
+                if (s2 >= 0 && s2 < best) {
+                    best = s2;
+                    p->jit[gi.jit] = std::move(alt);
+                }
+                if (best == 0) break;
+            }
+        }
     }
     if (co.dry_run) {       // host-only planning: compile the generated passes, log every launch
         std::string &L = *co.dry_log;

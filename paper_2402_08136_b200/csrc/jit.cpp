@@ -227,6 +227,7 @@ const JitConfig &jit_config() {
             else if (key == "nbuf") x.nbuf = iv == 2 ? 2 : 1;
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "mred") x.mred = iv != 0;
+            else if (key == "spillfb") x.spillfb = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
@@ -253,7 +254,8 @@ bool jit_available(std::string *why) {
 // ---------------------------------------------------------------- codegen ----
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra, const InitSpec *init,
-                            std::vector<std::pair<uint64_t, uint64_t>> *cwide, const std::vector<double2> *hblob) {
+                            std::vector<std::pair<uint64_t, uint64_t>> *cwide, const std::vector<double2> *hblob,
+                            const JitVariant &var) {
     const JitConfig &cfg = jit_config();
     const int T = a.T;
     const int RB = a.nreg, RA = 1 << RB;      // register bits / amplitudes per thread in a phase
@@ -376,7 +378,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (int l = 0; l < op.t_len[r]; l++) v.push_back({op.t_src[r] + l, op.t_dst[r] + l});
         return v;
     };
-    if (cwide && cfg.cw && cfg.ctab) {
+    if (cwide && cfg.cw && cfg.ctab && !var.no_ctab) {
         for (size_t i = 0; i < ops.size(); i++) {
             const auto &op = ops[i];
             if (op.kind != 1 || op.ngr != 0) continue;
@@ -1058,7 +1060,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             k << "      }\n";
         };
-        const bool group_on = cfg.group;
+        const bool group_on = cfg.group && !var.no_group;
         for (int oi = P.op0; oi < P.op1 && !cfg.skeleton; oi++) {
             const DRun *run = nullptr;
             for (auto &dr : druns)
@@ -1182,7 +1184,7 @@ struct CacheEntry {
 std::mutex g_mu;
 std::map<std::string, std::shared_ptr<CacheEntry>> g_cache;
 
-std::vector<char> compile_cubin(const std::string &src, std::string &err) {
+std::vector<char> compile_cubin(const std::string &src, std::string &err, int *spill = nullptr) {
     Nvrtc &n = nvrtc();
     nvrtcProgram_t prog = nullptr;
     const std::string full = std::string(kPrelude) + src;
@@ -1204,7 +1206,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     // prelude): with NVRTC's default 64-bit shared-pointer arithmetic, ptxas -O2/-O3 miscompiled
     // some tile kernels into illegal-address faults (source clean under host emulation with
     // ASan/UBSan, scripts/jit_emulate.py; same PTX fine at -O1).
-    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-O3"};
+    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas=-v", "-Xptxas=-O3"};
     const JitConfig &cfg = jit_config();
     if (!cfg.ptxas_opt.empty()) opts.back() = cfg.ptxas_opt.c_str();
     if (cfg.smem_clobber) opts.push_back("-DHHLSV_SMEM_CLOBBER");
@@ -1217,6 +1219,19 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
         err = std::string("NVRTC: ") + n.errStr(rc) + "\n" + log.substr(0, 2000);
         n.destroy(&prog);
         return {};
+    }
+    if (spill) {        // ptxas -v: "N bytes stack frame, S bytes spill stores, L bytes spill loads"
+        size_t ls = 0;
+        n.logSize(prog, &ls);
+        std::string log(ls, '\0');
+        if (ls) n.log(prog, &log[0]);
+        *spill = 0;
+        const size_t at = log.find(" bytes spill stores");
+        if (at != std::string::npos) {
+            size_t b = log.rfind(',', at);
+            b = (b == std::string::npos) ? 0 : b + 1;
+            *spill = std::atoi(log.c_str() + b);
+        }
     }
     size_t cs = 0;
     n.cubinSize(prog, &cs);
@@ -1231,7 +1246,40 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err) {
     }
     return cubin;
 }
+// Cubins compiled ahead of jit_build (spill probing): source -> (cubin, spill bytes). jit_build and
+// jit_compile_only take their entry (a probed pass is compiled once).
+std::mutex g_cub_mu;
+std::map<std::string, std::pair<std::vector<char>, int>> g_cubins;
+
+std::vector<char> take_or_compile(const std::string &src, std::string &err) {
+    {
+        std::lock_guard<std::mutex> lk(g_cub_mu);
+        auto it = g_cubins.find(src);
+        if (it != g_cubins.end()) {
+            std::vector<char> c = std::move(it->second.first);
+            g_cubins.erase(it);
+            if (!c.empty()) return c;
+        }
+    }
+    return compile_cubin(src, err);
+}
 }  // namespace
+
+int jit_spill_bytes(const std::string &src) {
+    {
+        std::lock_guard<std::mutex> lk(g_cub_mu);
+        auto it = g_cubins.find(src);
+        if (it != g_cubins.end()) return it->second.second;
+    }
+    if (!nvrtc().ok) return -1;
+    std::string err;
+    int spill = 0;
+    std::vector<char> c = compile_cubin(src, err, &spill);
+    if (c.empty()) return -1;
+    std::lock_guard<std::mutex> lk(g_cub_mu);
+    g_cubins[src] = {std::move(c), spill};
+    return spill;
+}
 
 std::string jit_source_tag(const std::string &src) {
     char hx[32];
@@ -1244,7 +1292,7 @@ std::vector<char> jit_compile_only(const std::string &src, std::string &err) {
         err = nvrtc().why;
         return {};
     }
-    return compile_cubin(src, err);
+    return take_or_compile(src, err);
 }
 
 void jit_build(std::vector<JitPass> &passes) {
@@ -1268,7 +1316,7 @@ void jit_build(std::vector<JitPass> &passes) {
     std::vector<std::vector<char>> cubins(passes.size());
     std::vector<std::thread> th;
     for (size_t i : todo)
-        th.emplace_back([&, i] { cubins[i] = compile_cubin(passes[i].src, ents[i]->err); });
+        th.emplace_back([&, i] { cubins[i] = take_or_compile(passes[i].src, ents[i]->err); });
     for (auto &t : th) t.join();
     for (size_t i : todo) {
         CacheEntry &e = *ents[i];

@@ -65,15 +65,27 @@ struct JitConfig {
     int eigen_chunk = 0;      // echunk: clock bits per eigen-phase table (0 = front-end default)
     bool init_fuse = true;    // initfuse: product-state init computed inside the first tile pass
     bool mred = true;         // mred: the last tile pass accumulates the HHL ancilla marginal (fused readout)
+    bool spillfb = true;      // spillfb: regenerate a spilling pass with the JitVariant fallbacks
 };
 const JitConfig &jit_config();
+
+// Per-pass code-generation fallbacks (program_create retries a pass whose ptxas output spills with
+// these, keeping the variant that spills least): both trade a little FP64 / load work for registers.
+struct JitVariant {
+    bool no_ctab = false;      // diagonal tables from L1 (__ldg) instead of per-thread selects of kernel params
+    bool no_group = false;     // no shared per-slot factor products across a phase's diagonal ops
+};
 
 bool jit_available(std::string *why);
 std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, const std::vector<dev::RegPhase> &ph,
                             const std::vector<dev::RegOp> &ops, size_t *smem_extra = nullptr,
                             const InitSpec *init = nullptr,
                             std::vector<std::pair<uint64_t, uint64_t>> *cwide = nullptr,
-                            const std::vector<double2> *hblob = nullptr);   // host blob: structural zeros
+                            const std::vector<double2> *hblob = nullptr,    // host blob: structural zeros
+                            const JitVariant &var = JitVariant());
+// ptxas spill-store bytes of a generated pass (compiles it once; the cubin is kept for jit_build /
+// jit_compile_only). -1 if the compilation fails (jit_build then reports the error).
+int jit_spill_bytes(const std::string &src);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.
