@@ -317,7 +317,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     const int T = std::min(o.tile_qubits, nloc);
     // register bits per phase: o.reg_bits (3 or 4) by default; a pass holding a 4-target op uses 4
     const int RMAX = 4;
-    const bool tiles = o.tile_qubits > 0 && nloc >= RMAX + 3;
+    const bool tiles = o.tile_qubits > 0 && nloc >= RMAX + 1;
     int wmin_opt = o.wmin;   // default 3 (128-byte segments): more tile bits for op targets per pass
     if (jit_config().wmin != 3) wmin_opt = jit_config().wmin;     // developer experiments (HHLSV_JIT=wmin=..)
     const int wmin = std::min(wmin_opt, T - RMAX);

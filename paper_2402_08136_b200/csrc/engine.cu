@@ -1004,10 +1004,16 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     // spills, 18.6 -> 15.9 ms per rank; the S30 passes do not spill and are unchanged).
     if (use_jit && jit_config().spillfb && !p->jit.empty()) {
         std::vector<int> spill(p->jit.size(), 0);
-        std::vector<std::thread> th;
+        std::vector<size_t> unknown;          // sources not probed yet in this process
         for (size_t i = 0; i < p->jit.size(); i++)
-            th.emplace_back([&, i] { spill[i] = jit_spill_bytes(p->jit[i].src); });
-        for (auto &t : th) t.join();
+            if (!jit_spill_cached(p->jit[i].src, &spill[i])) unknown.push_back(i);
+        if (unknown.size() == 1) {
+            spill[unknown[0]] = jit_spill_bytes(p->jit[unknown[0]].src);
+        } else if (!unknown.empty()) {
+            std::vector<std::thread> th;
+            for (size_t i : unknown) th.emplace_back([&, i] { spill[i] = jit_spill_bytes(p->jit[i].src); });
+            for (auto &t : th) t.join();
+        }
         for (const GenIn &gi : gen_in) {
             int best = spill[gi.jit];
             if (best <= 0) continue;
@@ -1102,7 +1108,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     prof_mark("  lower + upload");
     for (const LaunchRec &r : p->recs)
         if (r.kind == StepKind::Tile && r.jit >= 0 && r.tile.red >= 0) {
-            cuda_check(pool_malloc((void **)&p->d_mred, sizeof(double) * (2 * sv_program::kMredCtas + 2), us),
+            cuda_check(pool_malloc_nosync((void **)&p->d_mred, sizeof(double) * (2 * sv_program::kMredCtas + 2), us),
                        "cudaMalloc(marginal partials)");
             p->jit[r.jit].red = p->d_mred;
         }

@@ -1250,6 +1250,7 @@ std::vector<char> compile_cubin(const std::string &src, std::string &err, int *s
 // jit_compile_only take their entry (a probed pass is compiled once).
 std::mutex g_cub_mu;
 std::map<std::string, std::pair<std::vector<char>, int>> g_cubins;
+std::map<size_t, int> g_spill;       // hash of the source -> ptxas spill-store bytes (kept for the process)
 
 std::vector<char> take_or_compile(const std::string &src, std::string &err) {
     {
@@ -1265,19 +1266,25 @@ std::vector<char> take_or_compile(const std::string &src, std::string &err) {
 }
 }  // namespace
 
+bool jit_spill_cached(const std::string &src, int *spill) {
+    std::lock_guard<std::mutex> lk(g_cub_mu);
+    auto it = g_spill.find(std::hash<std::string>()(src));
+    if (it == g_spill.end()) return false;
+    *spill = it->second;
+    return true;
+}
+
 int jit_spill_bytes(const std::string &src) {
-    {
-        std::lock_guard<std::mutex> lk(g_cub_mu);
-        auto it = g_cubins.find(src);
-        if (it != g_cubins.end()) return it->second.second;
-    }
+    int known = 0;
+    if (jit_spill_cached(src, &known)) return known;
     if (!nvrtc().ok) return -1;
     std::string err;
     int spill = 0;
     std::vector<char> c = compile_cubin(src, err, &spill);
     if (c.empty()) return -1;
     std::lock_guard<std::mutex> lk(g_cub_mu);
-    g_cubins[src] = {std::move(c), spill};
+    g_spill[std::hash<std::string>()(src)] = spill;
+    g_cubins[src] = {std::move(c), spill};      // taken by the jit_build that loads it
     return spill;
 }
 

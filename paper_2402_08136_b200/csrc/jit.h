@@ -86,6 +86,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
 // ptxas spill-store bytes of a generated pass (compiles it once; the cubin is kept for jit_build /
 // jit_compile_only). -1 if the compilation fails (jit_build then reports the error).
 int jit_spill_bytes(const std::string &src);
+// The spill bytes of a source already probed in this process (no compilation); false if unknown.
+bool jit_spill_cached(const std::string &src, int *spill);
 void jit_build(std::vector<JitPass> &passes);            // compile (cached) + load; throws on failure
 std::vector<char> jit_compile_only(const std::string &src, std::string &err);
 // Name under which HHLSV_JIT_DUMP stores a pass's full source ("tile_<hash>"), for debug tooling.

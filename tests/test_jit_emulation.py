@@ -60,6 +60,19 @@ def test_bench_program_c3_emulated(tmp_path):
     assert np.allclose(reps[-1]["red"], want, rtol=0, atol=1e-13), (reps[-1]["red"], want)
 
 
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_single_tile_programs_emulated(tmp_path, name):
+    """Table 1 regime: a state no larger than one tile (C1: 5 qubits -> T = 5, 2 threads; C2: 9 qubits)
+    runs the whole HHL circuit as ONE generated pass (one launch)."""
+    A, b, nc = configs.get(name)
+    d, txt = _export(tmp_path, lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, **configs.BENCH_OPTS)[0])
+    xo, po, psi_o, p = ohhl.solve(A, b, nc)
+    out, reps = emu.run_program(d, np.full(1 << p.n, np.nan + 1j * np.nan))
+    _clean(reps)
+    assert len(reps) == 1
+    assert np.abs(emu.to_logical(out, emu.final_map(txt)) - psi_o).max() < 1e-12
+
+
 def test_small_tile_wide_ops_emulated(tmp_path):
     """Random circuit with 3-qubit controlled / diagonal ops at T = 8 (the shapes whose variants gave
     wrong GPU amplitudes in round 1): single-phase passes, controls on thread bits, kernel-parameter
