@@ -245,3 +245,41 @@ def test_cost_model_fusion_width():
     assert ks[0] == r["model_ms"] and ks[0] < ks[1] < ks[2]
     _, rs = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, qpe_mode=1, tile_qubits=-1)
     assert rs["fusion_kmax_used"] == 4
+
+
+def _fused_ops_as_gates(dump: str, seed: int):
+    """Rebuild a fused schedule (one op per line, tile_qubits = -1) as a gate list on the same
+    (physical) supports with fresh random matrices: fusion decisions depend only on kinds and supports."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for ln in dump.splitlines():
+        m = re.match(r"(DENSE|CONTROLLED) k=(\d+) t=([\d,]+) c=([\d,]*)", ln)
+        if m:
+            k = int(m.group(2))
+            t = [int(x) for x in m.group(3).split(",")]
+            c = [int(x) for x in m.group(4).split(",") if x]
+            U, _ = np.linalg.qr(rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k)))
+            g = {"kind": "controlled" if c else "dense", "targets": t, "data": U}
+            if c:
+                g["controls"], g["cvals"] = c, (1 << len(c)) - 1
+            out.append(g)
+            continue
+        m = re.match(r"DIAGONAL q=([\d,]+)", ln)
+        if m:
+            q = [int(x) for x in m.group(1).split(",")]
+            out.append({"kind": "diagonal", "targets": q, "data": np.exp(1j * rng.uniform(0, 6, 1 << len(q)))})
+            continue
+        assert ln.startswith("FINAL_MAP") or not ln.strip(), ln
+    return out
+
+
+@pytest.mark.parametrize("n,seed,kmax", [(8, 5, 3), (10, 7, 4), (10, 9, 2), (12, 3, 5)])
+def test_fusion_is_idempotent(n, seed, kmax):
+    """SURVEY §4 T3 / SPEC S:235: fusing an already fused circuit makes no further fusions (the greedy
+    fuser leaves no two adjacent ops whose union fits k_max)."""
+    g = synthetic.random_circuit(n, 150, seed=seed)
+    s, r = pkg.schedule_dump(n, g, fusion_kmax=kmax, tile_qubits=-1)
+    f = _fused_ops_as_gates(s, seed)
+    assert len(f) == r["n_fused"] < len(g)
+    _, r2 = pkg.schedule_dump(n, f, fusion_kmax=kmax, tile_qubits=-1)
+    assert r2["n_fused"] == len(f)
