@@ -983,10 +983,9 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
                 if (use_jit) {
                     GenIn gi{p->jit.size(), a, std::vector<dev::RegPhase>(phases.begin() + ph0, phases.end()),
                              std::vector<dev::RegOp>(rops.begin() + opbase, rops.end()), fuse_init && si == 1};
-                    JitPass jp;
+                    JitPass jp;           // source generated after the loop (in parallel)
                     jp.name = "hhlsv_tile";
                     jp.nthr = 1 << (a.T - a.nreg);
-                    gen_pass(jp, gi, JitVariant());
                     rec.jit = (int)p->jit.size();
                     p->jit.push_back(std::move(jp));
                     gen_in.push_back(std::move(gi));
@@ -998,6 +997,15 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         }
         p->recs.push_back(rec);
     }
+    prof_mark("  lower");
+    if (gen_in.size() == 1) {
+        gen_pass(p->jit[gen_in[0].jit], gen_in[0], JitVariant());
+    } else if (!gen_in.empty()) {       // independent per pass: shared inputs are read-only here
+        std::vector<std::thread> th;
+        for (const GenIn &gi : gen_in) th.emplace_back([&, pgi = &gi] { gen_pass(p->jit[pgi->jit], *pgi, JitVariant()); });
+        for (auto &t : th) t.join();
+    }
+    prof_mark("  generate");
     // Register-spill fallback: ptxas output of every pass is checked (in parallel; the cubins are kept
     // for jit_build); a pass that spills is regenerated without constant-bank tables, then also without
     // grouped diagonal factors, keeping the variant that spills least (S33 sharded pass 3: 376 B of
@@ -1031,6 +1039,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             }
         }
     }
+    prof_mark("  spill probe");
     if (co.dry_run) {       // host-only planning: compile the generated passes, log every launch
         std::string &L = *co.dry_log;
         char line[512];
