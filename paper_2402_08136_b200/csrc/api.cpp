@@ -454,9 +454,9 @@ static std::vector<Gate> hhl_fused_gates(const HHLPlanHost &p, const hhl_options
     const bool auto_k = (!opt || opt->fusion_kmax == 0) && fo.mode == 0;
     if (!auto_k) {
         std::vector<Gate> f = fuse(rest, fo);
-        if (choice) {
+        if (choice) {       // model time of the fixed width: from the schedule the caller compiles anyway
             choice->kmax = fo.kmax;
-            choice->model_ms = schedule_cost_ms(compile(f, factors.empty() ? nullptr : &factors, p.n, nloc, phys, cc), nloc);
+            choice->model_ms = NAN;
         }
         return f;
     }
@@ -534,7 +534,7 @@ static sv_program *build_hhl(sv_state *sv, const HHLPlanHost &p, const hhl_optio
         rep->h2d_bytes = prog->h2d_bytes;
         rep->d2h_bytes = 16.0 * (double)(1ull << p.n_b) + 8.0;
         rep->fusion_kmax_used = fc.kmax;
-        rep->model_ms = fc.model_ms;
+        rep->model_ms = std::isnan(fc.model_ms) ? schedule_cost_ms(prog->sched, sv->nloc) : fc.model_ms;
         rep->t_frontend_s = now_s() - t0;
     }
     return prog;
@@ -620,7 +620,7 @@ sv_status hhl_schedule_dump(const double *A, const double *b, int N, const hhl_o
             rep->alg_bytes = s.alg_bytes;
             rep->pass_bytes = s.pass_bytes;
             rep->fusion_kmax_used = fc.kmax;
-            rep->model_ms = fc.model_ms;
+            rep->model_ms = std::isnan(fc.model_ms) ? schedule_cost_ms(s, p.n - g) : fc.model_ms;
         }
         if (buf && buf_len) {
             std::string t = "INIT_FACTORS " + std::to_string(factors.size()) + "\n" + dump_schedule(s) + jitlog;
