@@ -120,6 +120,8 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
         for (int b : pnd(ops[i]))
             if (b >= nloc) needs_global[i] = 1;
     bool exchanged = false;        // after the first global op the layout changes: stop deferring
+    const int dalap = jit_config().dalap;      // passes (from the first) that place diagonals ALAP
+    int pass_no = 0;
     std::vector<Gate> out;
     out.reserve(m);
     std::vector<char> done(m, 0);
@@ -158,6 +160,7 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
             continue;
         }
         std::vector<int> cur;
+        const bool dalap_now = pass_no++ < dalap;
         for (;;) {
             // pick the ready op that adds the fewest new tile bits (free ones first), then the
             // earliest in circuit order: keeps room in the pass for ops that become ready later
@@ -178,11 +181,36 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
                         nnew++;
                     }
                 if (!fits(u)) continue;
+                if (dalap_now && g.kind == Kind::Diagonal) continue;    // considered below
                 if (nnew < best_new) {
                     best = i;
                     best_new = nnew;
                     best_u = u;
                     if (nnew == 0) break;      // ready is ordered: the earliest free op
+                }
+            }
+            if (best == SIZE_MAX && dalap_now) {
+                // diagonals as late as possible: one is taken only when no non-diagonal op fits and it
+                // unblocks a non-diagonal op that fits this pass (or only diagonals are left)
+                bool any_nd = false;
+                for (size_t i : ready) any_nd |= ops[i].kind != Kind::Diagonal;
+                for (size_t i : ready) {
+                    if (ops[i].kind != Kind::Diagonal) continue;
+                    bool use = !any_nd;
+                    for (size_t sb : succ[i]) {
+                        if (use) break;
+                        if (indeg[sb] != 1 || ops[sb].kind == Kind::Swap) continue;
+                        if (!exchanged && needs_global[sb]) continue;
+                        std::vector<int> u = cur;
+                        for (int b : pnd(ops[sb]))
+                            if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
+                        use = fits(u);
+                    }
+                    if (use) {
+                        best = i;
+                        best_u = cur;
+                        break;
+                    }
                 }
             }
             if (best == SIZE_MAX) break;

@@ -228,6 +228,7 @@ const JitConfig &jit_config() {
             else if (key == "minb") x.min_blocks = std::max(0, iv);
             else if (key == "mred") x.mred = iv != 0;
             else if (key == "spillfb") x.spillfb = iv != 0;
+            else if (key == "dalap") x.dalap = std::max(0, iv);
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
