@@ -73,6 +73,19 @@ typedef struct {
 /* Fill 128 bytes with a fresh ncclUniqueId (rank 0 only). SV_E_NCCL if NCCL cannot be loaded. */
 sv_status sv_nccl_unique_id(unsigned char out_id[128]);
 
+/* Transport self-test and microbenchmark of the exchange layer (SURVEY §8(d) "NVLink GB/s per
+ * exchange", §5 failure detection): every rank of `world` (one process per GPU, `device`) creates a
+ * communicator from the broadcast `nccl_id` and runs `reps` exchanges of the library's own transport
+ * (grouped ncclSend/ncclRecv, waited on with the asynchronous-error polling of sharded readouts):
+ *   pattern 0 -- pairwise: `bytes` to and from rank ^ 1 (world 1: to itself);
+ *   pattern 1 -- all-to-all: bytes / world to and from every other rank (world 1: to itself).
+ * Received data are checked against the sender's seeded pattern on the device. Outputs (any may be
+ * NULL): ms per exchange (CUDA events on the library stream, median of reps), GB/s = bytes this rank
+ * sends per exchange / time, and the number of mismatching doubles (0 = correct). world must be a
+ * power of two; bytes a multiple of 8 * world. SV_E_NCCL on a transport failure. */
+sv_status sv_comm_bench(int world, int rank, int device, const unsigned char *nccl_id, int pattern, uint64_t bytes,
+                        int reps, double *ms_out, double *gbs_out, uint64_t *mismatches_out);
+
 /* Allocate the (local shard of the) state on `dist->device` (or the current device)
  * and initialise it to |0...0>. cuda_stream: a cudaStream_t (NULL = default stream).
  * SV_E_ARG if n_qubits < 1 or n_qubits - log2(world) < 1; SV_E_OOM if it does not fit. */

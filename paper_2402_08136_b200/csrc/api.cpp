@@ -1,10 +1,12 @@
 // The extern "C" boundary declared in include/sv.h. Argument marshalling and error
 // translation only; all data-path work happens in the CUDA kernels behind engine.cu.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 #include <new>
 
+#include "comm.h"
 #include "engine.h"
 
 using namespace hhlsv;
@@ -82,6 +84,95 @@ sv_status sv_nccl_unique_id(unsigned char out_id[128]) {
     return guard([&] {
         if (!out_id) fail(SV_E_ARG, "null id buffer");
         if (nccl_unique_id(out_id)) fail(SV_E_NCCL, std::string("ncclGetUniqueId: ") + nccl_last_error());
+    });
+}
+
+sv_status sv_comm_bench(int world, int rank, int device, const unsigned char *nccl_id, int pattern, uint64_t bytes,
+                        int reps, double *ms_out, double *gbs_out, uint64_t *mismatches_out) {
+    return guard([&] {
+        if (!nccl_id) fail(SV_E_ARG, "null nccl_id");
+        if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world)
+            fail(SV_E_ARG, "world must be a power of two and 0 <= rank < world");
+        if (pattern != 0 && pattern != 1) fail(SV_E_ARG, "pattern must be 0 (pairwise) or 1 (all-to-all)");
+        if (reps < 1 || bytes == 0 || bytes % (8ull * (uint64_t)world))
+            fail(SV_E_ARG, "reps >= 1 and bytes a positive multiple of 8 * world");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+            cudaGetLastError();
+            fail(SV_E_CUDA, "no CUDA device: this library has no CPU fallback");
+        }
+        if (device >= 0) cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        struct Res {              // released on every exit path
+            Comm c;
+            cudaStream_t s = nullptr;
+            double *sb = nullptr, *rb = nullptr;
+            unsigned long long *bad = nullptr;
+            cudaEvent_t e[2] = {nullptr, nullptr};
+            ~Res() {
+                if (s) cudaStreamSynchronize(s);
+                cudaFree(sb);
+                cudaFree(rb);
+                cudaFree(bad);
+                for (auto ev : e)
+                    if (ev) cudaEventDestroy(ev);
+                if (s) cudaStreamDestroy(s);
+                nccl_destroy(c);
+            }
+        } r;
+        if (nccl_init(r.c, world, rank, nccl_id)) fail(SV_E_NCCL, std::string("ncclCommInitRank: ") + nccl_last_error());
+        cuda_check(cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking), "stream");
+        const uint64_t n = bytes / 8;
+        cuda_check(cudaMalloc((void **)&r.sb, bytes), "cudaMalloc(send)");
+        cuda_check(cudaMalloc((void **)&r.rb, bytes), "cudaMalloc(recv)");
+        cuda_check(cudaMalloc((void **)&r.bad, sizeof(unsigned long long)), "cudaMalloc(count)");
+        cuda_check(cudaMemsetAsync(r.bad, 0, sizeof(unsigned long long), r.s), "memset");
+        cuda_check(cudaMemsetAsync(r.rb, 0xff, bytes, r.s), "memset");       // NaN until received
+        cuda_check(dev::launch_fill_pattern(r.sb, n, (uint64_t)rank, 0, r.s), "fill");
+        // (peer, chunk): pairwise -> the whole buffer with rank ^ 1; all-to-all -> chunk p with rank p
+        std::vector<int> peers;
+        std::vector<const double *> sp;
+        std::vector<double *> rp;
+        std::vector<uint64_t> roff;       // offset of the received chunk in the sender's pattern
+        uint64_t cnt = n;
+        if (pattern == 0) {
+            const int peer = world == 1 ? 0 : (rank ^ 1);
+            peers = {peer};
+            sp = {r.sb};
+            rp = {r.rb};
+            roff = {0};
+        } else {
+            cnt = n / (uint64_t)world;
+            for (int q = 0; q < world; q++) {
+                if (world > 1 && q == rank) continue;
+                peers.push_back(q);
+                sp.push_back(r.sb + (uint64_t)q * cnt);
+                rp.push_back(r.rb + (uint64_t)q * cnt);
+                roff.push_back((uint64_t)rank * cnt);
+            }
+        }
+        for (auto &ev : r.e) cuda_check(cudaEventCreate(&ev), "event");
+        std::vector<float> ms;
+        for (int i = 0; i < reps + 1; i++) {          // one untimed warm-up exchange
+            cuda_check(cudaEventRecord(r.e[0], r.s), "event");
+            if (nccl_alltoall_pairs(r.c, sp.data(), rp.data(), peers.data(), (int)peers.size(), cnt, r.s))
+                fail(SV_E_NCCL, std::string("exchange: ") + nccl_last_error());
+            cuda_check(cudaEventRecord(r.e[1], r.s), "event");
+            if (nccl_wait(r.c, r.s, 300.0)) fail(SV_E_NCCL, std::string("exchange wait: ") + nccl_last_error());
+            float t = 0.0f;
+            cuda_check(cudaEventElapsedTime(&t, r.e[0], r.e[1]), "elapsed");
+            if (i) ms.push_back(t);
+        }
+        for (size_t i = 0; i < peers.size(); i++)
+            cuda_check(dev::launch_check_pattern(rp[i], cnt, (uint64_t)peers[i], roff[i], r.bad, r.s), "check");
+        unsigned long long bad = 0;
+        cuda_check(cudaMemcpyAsync(&bad, r.bad, sizeof bad, cudaMemcpyDeviceToHost, r.s), "count d2h");
+        cuda_check(cudaStreamSynchronize(r.s), "sync");
+        std::sort(ms.begin(), ms.end());
+        const double med = ms[ms.size() / 2];
+        const double sent = 8.0 * (double)cnt * (double)peers.size();
+        if (ms_out) *ms_out = med;
+        if (gbs_out) *gbs_out = med > 0 ? sent / (med * 1e-3) / 1e9 : 0.0;
+        if (mismatches_out) *mismatches_out = bad;
     });
 }
 

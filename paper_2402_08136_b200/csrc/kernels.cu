@@ -632,6 +632,38 @@ __global__ void k_marginal_final(const double *ws, int logC, uint64_t nbins, dou
     }
 }
 
+__device__ __forceinline__ double pattern_value(uint64_t seed, uint64_t i) {
+    uint64_t z = (seed + 1) * 0x9E3779B97F4A7C15ull + i * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 31;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 29;
+    return (double)(z >> 11);           // 53-bit integer: exact in a double
+}
+
+__global__ void k_fill_pattern(double *buf, uint64_t n, uint64_t seed, uint64_t offset) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        buf[i] = pattern_value(seed, offset + i);
+}
+
+__global__ void k_check_pattern(const double *buf, uint64_t n, uint64_t seed, uint64_t offset,
+                                unsigned long long *mismatches) {
+    unsigned long long bad = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        bad += buf[i] != pattern_value(seed, offset + i);
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+cudaError_t launch_fill_pattern(double *buf, uint64_t n, uint64_t seed, uint64_t offset, cudaStream_t s) {
+    k_fill_pattern<<<148 * 8, 256, 0, s>>>(buf, n, seed, offset);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_pattern(const double *buf, uint64_t n, uint64_t seed, uint64_t offset,
+                                 unsigned long long *mismatches, cudaStream_t s) {
+    k_check_pattern<<<148 * 8, 256, 0, s>>>(buf, n, seed, offset, mismatches);
+    return cudaGetLastError();
+}
+
 __global__ void k_pair_sum(const double *part, int nblocks, double *out) {
     double s0 = 0.0, s1 = 0.0;
     for (int i = threadIdx.x; i < nblocks; i += 32) {

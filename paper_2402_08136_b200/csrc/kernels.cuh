@@ -136,6 +136,11 @@ constexpr int kRedBlocks = 1184;   // 148 SMs x 8
 // Fixed-order sum of nblocks (bit 0, bit 1) partial pairs written by a tile pass with a fused marginal:
 // out[0] = Σ part[2i], out[1] = Σ part[2i + 1] (one warp; lane-strided then a shuffle tree).
 cudaError_t launch_pair_sum(const double *part, int nblocks, double *out, cudaStream_t s);
+// Seeded test pattern for transport checks: buf[i] = f(seed, offset + i) (exactly representable);
+// check counts the doubles of buf that differ from the pattern into *mismatches (atomic u64).
+cudaError_t launch_fill_pattern(double *buf, uint64_t n, uint64_t seed, uint64_t offset, cudaStream_t s);
+cudaError_t launch_check_pattern(const double *buf, uint64_t n, uint64_t seed, uint64_t offset,
+                                 unsigned long long *mismatches, cudaStream_t s);
 cudaError_t launch_norm2(const double2 *psi, uint64_t n, double *partial, double *out, cudaStream_t s);
 // Marginal over physical bits S (q = |S| <= 26, bit j of v <- S[j]); others O = remaining local bits.
 // Writes 2^q doubles to out (device). ws must hold 2^q * C doubles (C returned by marginal_chunks).

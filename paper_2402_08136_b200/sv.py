@@ -74,7 +74,7 @@ class hhl_report(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_create", "sv_destroy", "sv_trim_memory",
+EXPORTS = ["sv_last_error", "sv_version", "sv_nccl_unique_id", "sv_comm_bench", "sv_create", "sv_destroy", "sv_trim_memory",
            "sv_reset", "sv_info", "sv_dump", "sv_restore",
            "sv_qubit_map", "sv_sync", "sv_read", "sv_write", "sv_apply_fused", "sv_apply_circuit",
            "sv_program_create", "sv_program_run", "sv_program_destroy", "sv_program_dump",
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
     L.sv_version.restype = ctypes.c_char_p
     sig = {
         "sv_nccl_unique_id": [ctypes.c_char_p],
+        "sv_comm_bench": [c_int, c_int, c_int, ctypes.c_char_p, c_int, c_u64, c_int, P(c_dbl), P(c_dbl), P(c_u64)],
         "sv_create": [c_int, P(sv_dist), vp, P(vp)],
         "sv_destroy": [vp], "sv_reset": [vp], "sv_trim_memory": [c_int],
         "sv_info": [vp, P(c_int), P(c_u64), P(vp)],
@@ -201,6 +202,21 @@ def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load().sv_nccl_unique_id(buf))
     return buf.raw
+
+
+def comm_bench(world: int = 1, rank: int = 0, device: int = -1, nccl_id: bytes | None = None, pattern: int = 0,
+               nbytes: int = 1 << 30, reps: int = 5) -> dict:
+    """sv_comm_bench: the exchange transport between `world` ranks (pattern 0 pairwise, 1 all-to-all;
+    world 1 exchanges with itself). Returns ms per exchange, GB/s sent by this rank, mismatching doubles."""
+    if nccl_id is None:
+        if world != 1:
+            raise SVError(1, "nccl_id required for world > 1")
+        nccl_id = nccl_unique_id()
+    ms, gbs, bad = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    _check(load().sv_comm_bench(int(world), int(rank), int(device), nccl_id, int(pattern), int(nbytes), int(reps),
+                                ctypes.byref(ms), ctypes.byref(gbs), ctypes.byref(bad)))
+    return {"ms": ms.value, "gbs": gbs.value, "mismatches": bad.value, "bytes": int(nbytes), "pattern": int(pattern),
+            "world": int(world)}
 
 
 class State:
