@@ -5,6 +5,7 @@
 #include <numeric>
 #include <thread>
 
+#include <map>
 #include <mutex>
 
 #include <nvtx3/nvToolsExt.h>
@@ -998,8 +999,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
         p->recs.push_back(rec);
     }
     prof_mark("  lower");
-    if (gen_in.size() == 1) {
-        gen_pass(p->jit[gen_in[0].jit], gen_in[0], JitVariant());
+    if (gen_in.size() == 1 || (!gen_in.empty() && sv->nloc < 24)) {     // small programs: threads cost more
+        for (const GenIn &gi : gen_in) gen_pass(p->jit[gi.jit], gi, JitVariant());
     } else if (!gen_in.empty()) {       // independent per pass: shared inputs are read-only here
         std::vector<std::thread> th;
         for (const GenIn &gi : gen_in) th.emplace_back([&, pgi = &gi] { gen_pass(p->jit[pgi->jit], *pgi, JitVariant()); });
@@ -1010,7 +1011,8 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     // for jit_build); a pass that spills is regenerated without constant-bank tables, then also without
     // grouped diagonal factors, keeping the variant that spills least (S33 sharded pass 3: 376 B of
     // spills, 18.6 -> 15.9 ms per rank; the S30 passes do not spill and are unchanged).
-    if (use_jit && jit_config().spillfb && !p->jit.empty()) {
+    // (large states only: a small program is launch- and latency-bound, spills or not)
+    if (use_jit && jit_config().spillfb && !p->jit.empty() && sv->nloc >= 24) {
         std::vector<int> spill(p->jit.size(), 0);
         std::vector<size_t> unknown;          // sources not probed yet in this process
         for (size_t i = 0; i < p->jit.size(); i++)
@@ -1022,21 +1024,39 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
             for (size_t i : unknown) th.emplace_back([&, i] { spill[i] = jit_spill_bytes(p->jit[i].src); });
             for (auto &t : th) t.join();
         }
+        // the variant chosen for a default source is remembered: a repeated program regenerates only it
+        static std::mutex choice_mu;
+        static std::map<size_t, int> choice;        // hash of the default source -> variant (0 = default)
+        const JitVariant variants[3] = {JitVariant{}, JitVariant{true, false}, JitVariant{true, true}};
         for (const GenIn &gi : gen_in) {
             int best = spill[gi.jit];
             if (best <= 0) continue;
-            for (const JitVariant v : {JitVariant{true, false}, JitVariant{true, true}}) {
+            const size_t key = std::hash<std::string>()(p->jit[gi.jit].src);
+            int known = -1;
+            {
+                std::lock_guard<std::mutex> lk(choice_mu);
+                auto it = choice.find(key);
+                if (it != choice.end()) known = it->second;
+            }
+            if (known >= 0) {
+                if (known > 0) gen_pass(p->jit[gi.jit], gi, variants[known]);
+                continue;
+            }
+            int pick = 0;
+            for (int vi = 1; vi < 3 && best > 0; vi++) {
                 JitPass alt;
                 alt.name = p->jit[gi.jit].name;
                 alt.nthr = p->jit[gi.jit].nthr;
-                gen_pass(alt, gi, v);
+                gen_pass(alt, gi, variants[vi]);
                 const int s2 = jit_spill_bytes(alt.src);
                 if (s2 >= 0 && s2 < best) {
                     best = s2;
+                    pick = vi;
                     p->jit[gi.jit] = std::move(alt);
                 }
-                if (best == 0) break;
             }
+            std::lock_guard<std::mutex> lk(choice_mu);
+            choice[key] = pick;
         }
     }
     prof_mark("  spill probe");
