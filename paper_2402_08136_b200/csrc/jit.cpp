@@ -229,6 +229,7 @@ const JitConfig &jit_config() {
             else if (key == "mred") x.mred = iv != 0;
             else if (key == "spillfb") x.spillfb = iv != 0;
             else if (key == "dalap") x.dalap = std::max(0, iv);
+            else if (key == "twiddle") x.twiddle = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
@@ -737,9 +738,40 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             return p + 1 == ph.size() && !dout && oi + 1 == P.op1 && op.kind == 0 && Kq >= 3 && !op.rcm && !op.tcm &&
                    !op.gcm && cfg.tail;
         };
+        // Twiddle-butterfly fusion: the last complex multiply a diagonal group / op applies to the
+        // x1 slot of the butterfly that follows it (Hadamard on the bit the phases are conditioned on,
+        // as in every (I)QFT stage: CP ladder / eigen-phase, then H) is kept pending and folded into
+        // that butterfly: (x0 + w x1, 2 x0 - (x0 + w x1)) costs 6 FP64 ops per pair instead of 8.
+        std::map<int, std::string> pend;          // slot -> pending factor variable
+        auto flush = [&](int j) {
+            auto it = pend.find(j);
+            if (it == pend.end()) return;
+            k << "      v" << j << " = cmul(" << it->second << ", v" << j << ");\n";
+            pend.erase(it);
+        };
+        auto flush_all = [&] {
+            while (!pend.empty()) flush(pend.begin()->first);
+        };
+        int npend = 0;
+        // butterfly bit of op q if it can absorb pending x1 factors (unconditional kind-4 op), else -1
+        auto bfly_bit = [&](int q) {
+            if (!cfg.twiddle || q >= P.op1 || ops[q].kind != 4 || ops[q].gcm || ops[q].tcm) return -1;
+            int A = 0;
+            while (!((ops[q].mask >> A) & 1)) A++;
+            return A;
+        };
         auto emit_single = [&](int oi) {
             tail_in_smem = tail_wide(oi);
             const dev::RegOp &op = ops[oi];
+            if (op.kind != 4) flush_all();
+            else {
+                int A = 0;
+                while (!((op.mask >> A) & 1)) A++;
+                std::vector<int> keep;
+                for (auto &kv : pend)
+                    if (!((kv.first >> A) & 1) || op.gcm || op.tcm) keep.push_back(kv.first);
+                for (int j : keep) flush(j);
+            }
             std::ostringstream cond;
             if (op.gcm) cond << "((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ")";
             if ((op.kind == 0 || op.kind == 1) && op.tcm) {
@@ -747,6 +779,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 cond << "((tb & " << op.tcm << "u) == " << op.tcv << "u)";
             }
             const std::string c = cond.str();
+            // pending factors of a diagonal op folded into the next butterfly (declared outside the block)
+            const int Ab = (op.kind == 1 && c.empty()) ? bfly_bit(oi + 1) : -1;
+            const int pid = npend;
+            if (Ab >= 0) {
+                npend++;
+                for (int j = 0; j < RA; j++)
+                    if ((j & op.rcm) == op.rcv && ((j >> Ab) & 1)) k << "      double2 pw" << pid << "_" << j << ";\n";
+            }
             k << "      " << (c.empty() ? "{" : "if (" + c + ") {") << " // op " << oi << "\n";
             if (op.kind == 3) {          // deferred global scale
                 k << "        const double sc = __ldg(&blob[" << op.data_off << "ull].x);\n";
@@ -757,6 +797,16 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 for (int j = 0; j < RA; j++) {
                     if ((j >> A) & 1) continue;
                     const int j1 = j | (1 << A);
+                    auto pw = pend.find(j1);
+                    if (pw != pend.end()) {      // fused: s = x0 + w x1, x1' = 2 x0 - s
+                        const std::string &w = pw->second;
+                        k << "        { const double2 x0 = v" << j << ", x1 = v" << j1 << "; const double2 s = mk(fma("
+                          << w << ".x, x1.x, fma(-" << w << ".y, x1.y, x0.x)), fma(" << w << ".x, x1.y, fma(" << w
+                          << ".y, x1.x, x0.y))); v" << j1 << " = mk(fma(2.0, x0.x, -s.x), fma(2.0, x0.y, -s.y)); v" << j
+                          << " = s; }\n";
+                        pend.erase(pw);
+                        continue;
+                    }
                     k << "        { const double2 x0 = v" << j << ", x1 = v" << j1 << "; v" << j
                       << " = mk(x0.x + x1.x, x0.y + x1.y); v" << j1 << " = mk(x0.x - x1.x, x0.y - x1.y); }\n";
                 }
@@ -919,11 +969,20 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 k << "        const u64 ib = (" << runs_expr("gbase", op.ngr, op.g_src, op.g_len, op.g_dst) << ") | ("
                   << runs_expr("tb", op.ntr, op.t_src, op.t_len, op.t_dst) << ");\n";
                 if (op.kind == 1) {
+                    const int A = Ab;
                     for (int j = 0; j < RA; j++)
                         if ((j & op.rcm) == op.rcv)
                             k << "        const double2 d" << j << " = " << dval(oi, op.ridx[j], "ib") << ";\n";
-                    for (int j = 0; j < RA; j++)
-                        if ((j & op.rcm) == op.rcv) k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
+                    for (int j = 0; j < RA; j++) {
+                        if ((j & op.rcm) != op.rcv) continue;
+                        if (A >= 0 && ((j >> A) & 1)) {
+                            const std::string w = "pw" + std::to_string(pid) + "_" + std::to_string(j);
+                            k << "        " << w << " = d" << j << ";\n";
+                            pend[j] = w;
+                        } else {
+                            k << "        v" << j << " = cmul(d" << j << ", v" << j << ");\n";
+                        }
+                    }
                 } else {
                     int A = 0;
                     while (!((op.mask >> A) & 1)) A++;
@@ -988,7 +1047,14 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             return c.str();
         };
-        auto emit_group = [&](const std::vector<int> &G) {
+        auto emit_group = [&](const std::vector<int> &G, int A) {
+            flush_all();
+            const int pid = npend;
+            if (A >= 0) {        // pending factors of the x1 slots (declared outside the block)
+                npend++;
+                for (int j = 0; j < RA; j++)
+                    if ((j >> A) & 1) k << "      double2 pw" << pid << "_" << j << ";\n";
+            }
             k << "      { // diagonal group of " << G.size() << " ops\n";
             std::vector<std::vector<std::string>> fac(16);
             std::map<uint32_t, std::vector<int>> uni;
@@ -1057,7 +1123,13 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                     }
                     f = it->second;
                 }
-                k << "        v" << j << " = cmul(" << f << ", v" << j << ");\n";
+                if (A >= 0 && ((j >> A) & 1)) {        // folded into the butterfly that follows
+                    const std::string w = "pw" + std::to_string(pid) + "_" + std::to_string(j);
+                    k << "        " << w << " = " << f << ";\n";
+                    pend[j] = w;
+                } else {
+                    k << "        v" << j << " = cmul(" << f << ", v" << j << ");\n";
+                }
             }
             k << "      }\n";
         };
@@ -1067,6 +1139,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             for (auto &dr : druns)
                 if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;
             if (run) {
+                if (oi == run->a) flush_all();
                 if (oi == run->a) {      // the whole run: one shared lookup + one complex multiply per slot
                     const int nv = (int)run->V.size();
                     k << "      { const u32 bt = 0u";
@@ -1100,7 +1173,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
                 std::vector<int> G, C;
                 for (int q = oi; q < oj; q++) G.push_back(q);
                 if (G.size() >= 2) {
-                    emit_group(G);
+                    emit_group(G, bfly_bit(oj));
                     for (int q : C) emit_single(q);
                     oi = oj - 1;
                     continue;
@@ -1108,6 +1181,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             }
             emit_single(oi);
         }
+        flush_all();
         // hoisted sub-table build for the next phase (or the next tile's phase 0) after this phase's
         // registers are stored (they are dead: no extra register pressure), before the barrier
         auto hoisted = [&] {

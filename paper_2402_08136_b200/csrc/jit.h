@@ -66,6 +66,7 @@ struct JitConfig {
     bool init_fuse = true;    // initfuse: product-state init computed inside the first tile pass
     bool mred = true;         // mred: the last tile pass accumulates the HHL ancilla marginal (fused readout)
     bool spillfb = true;      // spillfb: regenerate a spilling pass with the JitVariant fallbacks
+    bool twiddle = true;      // twiddle: a diagonal's x1 multiplies folded into the following butterfly
     int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible)
 };
 const JitConfig &jit_config();
