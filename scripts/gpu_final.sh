@@ -9,9 +9,4 @@ timeout 900 python bench.py --table1 --steps 20 --warmup 5 --cpu-budget 3 > gpur
 timeout 300 python scripts/stress_bench.py --n 30 --kmax 2 > gpurun_out/stress_p30.json 2>&1; echo "stress rc=$?"
 timeout 900 python scripts/oracle_timing.py > gpurun_out/oracle_timing.json 2>&1; echo "oracle timing rc=$?"
 timeout 300 python scripts/pass_profile.py --qpe 1 --kmax 1 --tile 12 --jit 1 --verbose --reps 5 > gpurun_out/pass_profile.txt 2>&1
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-$CMD > gpurun_out/plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
-HHLSV_JIT_DUMP=gpurun_out/jit timeout 1500 ncu --set full --clock-control none --import-source on -k regex:hhlsv_tile -c 5 \
-  -o gpurun_out/tile_full -f $CMD > gpurun_out/ncu_full.log 2>&1
-echo "ncu rc $?"
+# profiler captures: scripts/gpu_profile.sh (launch list) and scripts/gpu_ncu_full.sh (--set full), one call each
