@@ -94,7 +94,7 @@ Gate gate_from_abi(const sv_gate &a, int n) {
             if (!a.data) fail(SV_E_ARG, "gate matrix missing");
             const int d = 1 << k;
             g.data.resize((size_t)d * d);
-            std::memcpy(g.data.data(), a.data, sizeof(cplx) * d * d);
+            for (size_t i = 0; i < g.data.size(); i++) g.data[i] = cplx(a.data[2 * i], a.data[2 * i + 1]);
             if (unitarity_defect(g.data, d) > 1e-10) fail(SV_E_NOTUNITARY, "gate matrix is not unitary (1e-10)");
             break;
         }
@@ -103,7 +103,7 @@ Gate gate_from_abi(const sv_gate &a, int n) {
             if (!g.controls.empty()) fail(SV_E_ARG, "diagonal gate with controls");
             if (!a.data) fail(SV_E_ARG, "diagonal table missing");
             g.data.resize((size_t)1 << k);
-            std::memcpy(g.data.data(), a.data, sizeof(cplx) << k);
+            for (size_t i = 0; i < g.data.size(); i++) g.data[i] = cplx(a.data[2 * i], a.data[2 * i + 1]);
             for (auto &z : g.data)
                 if (std::abs(std::abs(z) - 1.0) > 1e-10) fail(SV_E_NOTUNITARY, "diagonal entry not unimodular");
             break;
@@ -561,20 +561,6 @@ static std::vector<cplx> embed_dense(const std::vector<cplx> &m, const std::vect
     return E;
 }
 
-static std::vector<cplx> embed_diag(const std::vector<cplx> &d, const std::vector<int> &q,
-                                    const std::vector<int> &u) {
-    const size_t du = (size_t)1 << u.size();
-    std::vector<int> pos(q.size());
-    for (size_t i = 0; i < q.size(); i++) pos[i] = (int)(std::find(u.begin(), u.end(), q[i]) - u.begin());
-    std::vector<cplx> E(du);
-    for (size_t x = 0; x < du; x++) {
-        size_t s = 0;
-        for (size_t i = 0; i < q.size(); i++)
-            if ((x >> pos[i]) & 1) s |= (size_t)1 << i;
-        E[x] = d[s];
-    }
-    return E;
-}
 
 static std::vector<cplx> matmul(const std::vector<cplx> &a, const std::vector<cplx> &b, size_t d) {
     std::vector<cplx> c(d * d, 0.0);
