@@ -66,7 +66,8 @@ for kinds in [("controlled", "diagonal"), ("dense", "controlled"), ("dense", "di
 for name in ("C1", "C2", "C3p", "C3", "S18"):
     A, b, nc = configs.get(name)
     xo, po, psi_o, p = ohhl.solve(A, b, nc)
-    for label, opts in (("bench", configs.BENCH_OPTS), ("jit T=9", dict(tile_jit=1, tile_qubits=9)),
+    for label, opts in (("bench", configs.BENCH_OPTS), ("bench + fused marginal", dict(configs.BENCH_OPTS, fused_marginal=1)),
+                        ("jit T=9", dict(tile_jit=1, tile_qubits=9)),
                         ("textbook k2 T=10", dict(tile_jit=1, tile_qubits=10, fusion_kmax=2))):
         d, txt = export(lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, **opts)[0])
         try:
@@ -75,6 +76,10 @@ for name in ("C1", "C2", "C3p", "C3", "S18"):
             log(f"{name} {label} | not emulated: {str(e).splitlines()[0]}")
             continue
         err = float(np.abs(emu.to_logical(out, emu.final_map(txt)) - psi_o).max())
+        if "red" in reps[-1]:      # fused marginal of the last pass vs the oracle's P(ancilla = 0 / 1)
+            h = 1 << (p.n - 1)
+            want = (np.sum(np.abs(psi_o[:h]) ** 2), np.sum(np.abs(psi_o[h:]) ** 2))
+            err = max(err, float(np.abs(np.array(reps[-1]["red"]) - want).max()))
         c, k = summ(reps)
         bad += sum(c.values()) + (err > 1e-12)
         log(f"HHL {name} ({p.n} q) {label} | {k} | {c['races']} {c['oob']} {c['double_writes']} {c['sync_mismatch']} "
@@ -85,6 +90,14 @@ reps = emu.check_full_size(d, 1 << 30, tiles=3)
 for r in reps:
     bad += r["races"] + r["oob"] + r["double_writes"] + r["sync_mismatch"]
     log(f"S30 bench pass {r['pass_index']} full launch ({r['launch_tiles']} tiles, {r['nthr']} threads, "
+        f"{r['smem']} B smem), first {r['tiles']} tiles | 1 | {r['races']} {r['oob']} {r['double_writes']} "
+        f"{r['sync_mismatch']} | n/a (checks only)")
+A, b, nc = configs.get("S33")       # sharded over 8 ranks: rank 0's passes (lifted bits, spill fallback)
+d, txt = export(lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, world=8, **configs.BENCH_OPTS)[0])
+reps = emu.check_full_size(d, 1 << 30, tiles=3)
+for r in reps:
+    bad += r["races"] + r["oob"] + r["double_writes"] + r["sync_mismatch"]
+    log(f"S33/8 rank-0 pass {r['pass_index']} full launch ({r['launch_tiles']} tiles, {r['nthr']} threads, "
         f"{r['smem']} B smem), first {r['tiles']} tiles | 1 | {r['races']} {r['oob']} {r['double_writes']} "
         f"{r['sync_mismatch']} | n/a (checks only)")
 log(f"# total findings: {bad} ({time.time() - t0:.0f} s)")
