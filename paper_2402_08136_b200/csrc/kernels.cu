@@ -87,21 +87,108 @@ __global__ void __launch_bounds__(kThreads) k_dense(const DenseArgs a) {
         }
 #pragma unroll
         for (int gg = 0; gg < G; gg++) {
-            // r is not unrolled for K >= 3 so the compiler cannot hoist the whole matrix
-            // out of the grid-stride loop into registers.
-#pragma unroll(K >= 3 ? 1 : D)
-            for (int r = 0; r < D; r++) {
-                double2 acc = make_double2(0.0, 0.0);
+            // rows in blocks of RB independent accumulators (FMA latency hidden by 2 RB chains); the
+            // block loop is not unrolled for K >= 3 so the compiler cannot hoist the whole matrix out of
+            // the grid-stride loop into registers
+            constexpr int RB = D < 4 ? D : 4;
+#pragma unroll(K >= 3 ? 1 : D / RB)
+            for (int r0 = 0; r0 < D; r0 += RB) {
+                double2 acc[RB];
 #pragma unroll
-                for (int c = 0; c < D; c++) cfma(acc, sU[r * D + c], v[gg][c]);
-                a.psi[base[gg] | soff[r]] = acc;
+                for (int rr = 0; rr < RB; rr++) acc[rr] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int c = 0; c < D; c++)
+#pragma unroll
+                    for (int rr = 0; rr < RB; rr++) cfma(acc[rr], sU[(r0 + rr) * D + c], v[gg][c]);
+#pragma unroll
+                for (int rr = 0; rr < RB; rr++) a.psi[base[gg] | soff[r0 + rr]] = acc[rr];
             }
         }
     }
 }
 
+// Low-target variant: when every target (and every local control) lies below kChunkBits, the groups of
+// an aligned 2^kChunkBits-amplitude chunk are closed under the op. A CTA loads the chunk with coalesced
+// 16-byte loads into XOR-swizzled shared memory, applies the op to the chunk's groups there and stores
+// it back coalesced -- the thread-per-group kernel reads 2^k consecutive amplitudes per thread, i.e.
+// warp accesses at a 2^k x 16-byte stride (0.42-0.53 of the HBM peak for k = 3, 4 at targets 0..k-1,
+// profiles/r02_op_microbench_before.jsonl).
+// chunk = kThreads groups of 2^K amplitudes (one group per thread): 2^(8 + K) amplitudes, 16 << (8 + K) B
+__device__ __forceinline__ uint32_t chunk_swz(uint32_t i) { return i ^ ((i >> 4) & 7u); }
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_dense_chunk(const DenseArgs a, uint64_t n_chunks) {
+    constexpr int D = 1 << K;
+    constexpr int CB = 8 + K;
+    constexpr uint32_t NC = 1u << CB;
+    __shared__ double2 sU[D * D];
+    __shared__ uint32_t soff[D];
+    extern __shared__ double2 buf[];
+    for (int i = threadIdx.x; i < D * D; i += blockDim.x) sU[i] = a.U[i];
+    if (threadIdx.x < D) {
+        uint32_t o = 0;
+        for (int i = 0; i < K; i++)
+            if ((threadIdx.x >> i) & 1) o |= 1u << a.tpos[i];
+        soff[threadIdx.x] = o;
+    }
+    uint32_t lb = threadIdx.x;                      // this thread's group inside every chunk
+    for (int i = 0; i < a.nins; i++) lb = (uint32_t)insz(lb, a.ins[i]);
+    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        __syncthreads();                            // previous chunk's stores done with buf / sU ready
+        const uint64_t base = c << CB;
+        for (uint32_t i = threadIdx.x; i < NC; i += blockDim.x) buf[chunk_swz(i)] = a.psi[base + i];
+        __syncthreads();
+        double2 v[D];
+#pragma unroll
+        for (int q = 0; q < D; q++) v[q] = buf[chunk_swz(lb | soff[q])];
+        constexpr int RB = D < 4 ? D : 4;
+#pragma unroll 1
+        for (int r0 = 0; r0 < D; r0 += RB) {
+            double2 acc[RB];
+#pragma unroll
+            for (int rr = 0; rr < RB; rr++) acc[rr] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < D; q++)
+#pragma unroll
+                for (int rr = 0; rr < RB; rr++) cfma(acc[rr], sU[(r0 + rr) * D + q], v[q]);
+#pragma unroll
+            for (int rr = 0; rr < RB; rr++) buf[chunk_swz(lb | soff[r0 + rr])] = acc[rr];
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < NC; i += blockDim.x) a.psi[base + i] = buf[chunk_swz(i)];
+    }
+}
+
+template <int K>
+static cudaError_t launch_dense_chunk(const DenseArgs &a, uint64_t n_amps, cudaStream_t s) {
+    const size_t smem = sizeof(double2) << (8 + K);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_dense_chunk<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const uint64_t nch = n_amps >> (8 + K);
+    k_dense_chunk<K><<<grid_for(nch, 1), kThreads, smem, s>>>(a, nch);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_dense(const DenseArgs &a, cudaStream_t s) {
     if (a.n_groups == 0) return cudaSuccess;
+    // chunked shared-memory path: k in 3..4 with every target below bit 8 + k (all groups of a chunk
+    // closed under the op) and no local control (the chunk would move amplitudes the op never touches);
+    // low-target k = 1, 2 ops already read >= 32 contiguous bytes per thread
+    bool low = a.k >= 3 && a.k <= 4 && a.cset == 0 && a.nins == a.k;      // k = 5: FP64-bound, measured slower
+    for (int i = 0; i < a.nins && low; i++) low = a.ins[i] < 8 + a.k;
+    bool all_low_bits = low;                  // worth it only when the targets sit in the low 5 bits
+    for (int i = 0; i < a.nins && all_low_bits; i++) all_low_bits = a.ins[i] < 5;
+    const uint64_t n_amps = a.n_groups << a.nins;
+    if (all_low_bits && n_amps >= (1ull << (8 + a.k))) {
+        switch (a.k) {
+            case 3: return launch_dense_chunk<3>(a, n_amps, s);
+            case 4: return launch_dense_chunk<4>(a, n_amps, s);
+        }
+    }
     switch (a.k) {
         case 1: k_dense<1, 4><<<grid_for(a.n_groups, kThreads * 4), kThreads, 0, s>>>(a); break;
         case 2: k_dense<2, 2><<<grid_for(a.n_groups, kThreads * 2), kThreads, 0, s>>>(a); break;
