@@ -9,3 +9,4 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 900 python bench.py --table1 --steps 20 --warmup 5 --cpu-budget 3 > gpurun_out/bench_table1.jsonl 2> gpurun_out/bench_table1.err; echo "table1 rc=$?"
 timeout 300 python scripts/pass_profile.py --qpe 1 --kmax 1 --tile 12 --jit 1 --verbose --reps 5 > gpurun_out/pass_profile.txt 2>&1
 timeout 900 python scripts/virtual_scaling.py > gpurun_out/virtual_scaling.jsonl 2>&1; echo "virtual rc=$?"
+timeout 1200 python scripts/op_microbench.py 30 > gpurun_out/op_microbench.jsonl 2> gpurun_out/op_microbench.err; echo "op micro rc=$?"
