@@ -6,6 +6,7 @@
 // Reductions are fixed-order trees (warp shuffle -> block -> grid), never fp64 atomics,
 // so two runs are bit-identical.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -107,87 +108,102 @@ __global__ void __launch_bounds__(kThreads) k_dense(const DenseArgs a) {
     }
 }
 
-// Low-target variant: when every target (and every local control) lies below kChunkBits, the groups of
-// an aligned 2^kChunkBits-amplitude chunk are closed under the op. A CTA loads the chunk with coalesced
-// 16-byte loads into XOR-swizzled shared memory, applies the op to the chunk's groups there and stores
-// it back coalesced -- the thread-per-group kernel reads 2^k consecutive amplitudes per thread, i.e.
-// warp accesses at a 2^k x 16-byte stride (0.42-0.53 of the HBM peak for k = 3, 4 at targets 0..k-1,
-// profiles/r02_op_microbench_before.jsonl).
-// chunk = kThreads groups of 2^K amplitudes (one group per thread): 2^(8 + K) amplitudes, 16 << (8 + K) B
-__device__ __forceinline__ uint32_t chunk_swz(uint32_t i) { return i ^ ((i >> 4) & 7u); }
-
+// k = 5 on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): the only dense contraction of the path
+// (256 flop per amplitude, FP64-bound). The 32 x 32 complex matrix is the real 64 x 64
+// block matrix M = [[Ur, -Ui], [Ui, Ur]] in shared memory (rows padded to 68 doubles: 2 wavefronts
+// per A-fragment load). A warp takes 8 groups at a time: lane (n = lane / 4, kk = lane % 4) holds, as
+// its 16 B fragments, re / im of amplitudes kk, kk + 4, ..., kk + 28 of group n; 8 row tiles x 16
+// k-steps = 128 DMMAs give Y = M X (64 x 8), and the lane owning output rows e and e + 32 (re, im of
+// amplitude e) writes them back for its two groups. Each group is read completely into registers
+// before any write (in place, groups disjoint across warps).
 template <int K>
-__global__ void __launch_bounds__(kThreads) k_dense_chunk(const DenseArgs a, uint64_t n_chunks) {
-    constexpr int D = 1 << K;
-    constexpr int CB = 8 + K;
-    constexpr uint32_t NC = 1u << CB;
-    __shared__ double2 sU[D * D];
-    __shared__ uint32_t soff[D];
-    extern __shared__ double2 buf[];
-    for (int i = threadIdx.x; i < D * D; i += blockDim.x) sU[i] = a.U[i];
+__global__ void __launch_bounds__(kThreads) k_dense_dmma(const DenseArgs a, uint64_t n_batches) {
+    constexpr int D = 1 << K;          // complex dimension
+    constexpr int R = 2 * D;           // real dimension of M
+    constexpr int P = R + 4;           // padded row (doubles)
+    __shared__ double sM[R * P];
+    __shared__ uint64_t soff[D];
+    for (int i = threadIdx.x; i < D * D; i += blockDim.x) {
+        const int r = i / D, c = i % D;
+        const double2 u = a.U[i];
+        sM[r * P + c] = u.x;
+        sM[r * P + D + c] = -u.y;
+        sM[(D + r) * P + c] = u.y;
+        sM[(D + r) * P + D + c] = u.x;
+    }
     if (threadIdx.x < D) {
-        uint32_t o = 0;
+        uint64_t o = 0;
         for (int i = 0; i < K; i++)
-            if ((threadIdx.x >> i) & 1) o |= 1u << a.tpos[i];
+            if ((threadIdx.x >> i) & 1) o |= 1ull << a.tpos[i];
         soff[threadIdx.x] = o;
     }
-    uint32_t lb = threadIdx.x;                      // this thread's group inside every chunk
-    for (int i = 0; i < a.nins; i++) lb = (uint32_t)insz(lb, a.ins[i]);
-    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        __syncthreads();                            // previous chunk's stores done with buf / sU ready
-        const uint64_t base = c << CB;
-        for (uint32_t i = threadIdx.x; i < NC; i += blockDim.x) buf[chunk_swz(i)] = a.psi[base + i];
-        __syncthreads();
-        double2 v[D];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, n = lane >> 2, kk = lane & 3;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t bt = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); bt < n_batches; bt += warps) {
+        uint64_t b = bt * 8 + n;                   // this lane's group
+        for (int i = 0; i < a.nins; i++) b = insz(b, a.ins[i]);
+        b |= a.cset;
+        double xr[D / 4], xi[D / 4];               // B fragments: x[4 ks + kk], re for ks < D/4, im after
 #pragma unroll
-        for (int q = 0; q < D; q++) v[q] = buf[chunk_swz(lb | soff[q])];
-        constexpr int RB = D < 4 ? D : 4;
-#pragma unroll 1
-        for (int r0 = 0; r0 < D; r0 += RB) {
-            double2 acc[RB];
-#pragma unroll
-            for (int rr = 0; rr < RB; rr++) acc[rr] = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < D; q++)
-#pragma unroll
-                for (int rr = 0; rr < RB; rr++) cfma(acc[rr], sU[(r0 + rr) * D + q], v[q]);
-#pragma unroll
-            for (int rr = 0; rr < RB; rr++) buf[chunk_swz(lb | soff[r0 + rr])] = acc[rr];
+        for (int q = 0; q < D / 4; q++) {
+            const double2 v = a.psi[b | soff[kk + 4 * q]];
+            xr[q] = v.x;
+            xi[q] = v.y;
         }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < NC; i += blockDim.x) a.psi[base + i] = buf[chunk_swz(i)];
+        const uint64_t b0 = __shfl_sync(0xffffffffu, b, (2 * kk) * 4);        // the lane's two output
+        const uint64_t b1 = __shfl_sync(0xffffffffu, b, (2 * kk + 1) * 4);    // groups (D columns)
+#pragma unroll
+        for (int rt = 0; rt < D / 8; rt++) {       // output amplitudes 8 rt .. 8 rt + 7: re rows, im rows
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int r0 = 8 * rt + D * h;
+#pragma unroll
+                for (int ks = 0; ks < R / 4; ks++) {
+                    const double av = sM[(r0 + n) * P + 4 * ks + kk];
+                    const double bv = ks < D / 4 ? xr[ks] : xi[ks - D / 4];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(d[h][0]), "+d"(d[h][1])
+                                 : "d"(av), "d"(bv));
+                }
+            }
+            const uint64_t o = soff[8 * rt + n];
+            a.psi[b0 | o] = make_double2(d[0][0], d[1][0]);
+            a.psi[b1 | o] = make_double2(d[0][1], d[1][1]);
+        }
     }
 }
 
-template <int K>
-static cudaError_t launch_dense_chunk(const DenseArgs &a, uint64_t n_amps, cudaStream_t s) {
-    const size_t smem = sizeof(double2) << (8 + K);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_dense_chunk<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
+// Which dense / controlled ops take the DMMA kernel (measured, profiles/r02_op_microbench.jsonl): k = 5
+// always (FP64-bound: 0.43 -> 0.55 of the HBM peak); k = 3, 4 when a target sits in the low 5 bits (the
+// thread-per-group kernel then reads 2^k x 16 B per thread at a warp stride: k = 4 low 0.52 -> 0.86).
+// HHLSV_DMMA = 0 disables it (A/B experiments).
+static bool dmma_pick(const DenseArgs &a) {
+    static const bool on = [] {
+        const char *e = getenv("HHLSV_DMMA");
+        return !e || atoi(e) != 0;
+    }();
+    if (!on || a.k < 3) return false;
+    if (a.k == 5) return true;
+    int lo = 64, hi = 0;
+    for (int i = 0; i < a.k; i++) {
+        lo = a.tpos[i] < lo ? a.tpos[i] : lo;
+        hi = a.tpos[i] > hi ? a.tpos[i] : hi;
     }
-    const uint64_t nch = n_amps >> (8 + K);
-    k_dense_chunk<K><<<grid_for(nch, 1), kThreads, smem, s>>>(a, nch);
-    return cudaGetLastError();
+    return a.k == 4 ? lo < 5 : hi < 5;          // k = 3: only when every target is low (split: a tie)
 }
 
 cudaError_t launch_dense(const DenseArgs &a, cudaStream_t s) {
     if (a.n_groups == 0) return cudaSuccess;
-    // chunked shared-memory path: k in 3..4 with every target below bit 8 + k (all groups of a chunk
-    // closed under the op) and no local control (the chunk would move amplitudes the op never touches);
-    // low-target k = 1, 2 ops already read >= 32 contiguous bytes per thread
-    bool low = a.k >= 3 && a.k <= 4 && a.cset == 0 && a.nins == a.k;      // k = 5: FP64-bound, measured slower
-    for (int i = 0; i < a.nins && low; i++) low = a.ins[i] < 8 + a.k;
-    bool all_low_bits = low;                  // worth it only when the targets sit in the low 5 bits
-    for (int i = 0; i < a.nins && all_low_bits; i++) all_low_bits = a.ins[i] < 5;
-    const uint64_t n_amps = a.n_groups << a.nins;
-    if (all_low_bits && n_amps >= (1ull << (8 + a.k))) {
+    if (a.k >= 3 && a.n_groups % 8 == 0 && dmma_pick(a)) {
+        const uint64_t nb = a.n_groups / 8;
         switch (a.k) {
-            case 3: return launch_dense_chunk<3>(a, n_amps, s);
-            case 4: return launch_dense_chunk<4>(a, n_amps, s);
+            case 3: k_dense_dmma<3><<<grid_for(nb, kThreads / 32), kThreads, 0, s>>>(a, nb); break;
+            case 4: k_dense_dmma<4><<<grid_for(nb, kThreads / 32), kThreads, 0, s>>>(a, nb); break;
+            case 5: k_dense_dmma<5><<<grid_for(nb, kThreads / 32), kThreads, 0, s>>>(a, nb); break;
         }
+        return cudaGetLastError();
     }
     switch (a.k) {
         case 1: k_dense<1, 4><<<grid_for(a.n_groups, kThreads * 4), kThreads, 0, s>>>(a); break;
