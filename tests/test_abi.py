@@ -283,3 +283,29 @@ def test_fusion_is_idempotent(n, seed, kmax):
     assert len(f) == r["n_fused"] < len(g)
     _, r2 = pkg.schedule_dump(n, f, fusion_kmax=kmax, tile_qubits=-1)
     assert r2["n_fused"] == len(f)
+
+
+def _jit_sources(cfg, world, env_jit):
+    """The generated pass source tags of a host-only schedule dump, in a subprocess with HHLSV_JIT set
+    (the JIT configuration is read once per process)."""
+    import subprocess
+    import sys
+    code = ("import paper_2402_08136_b200 as pkg, re\n"
+            "from workloads import configs\n"
+            f"A, b, nc = configs.get('{cfg}')\n"
+            f"s, r = pkg.hhl_schedule_dump(A, b, clock_qubits=nc, world={world}, **configs.BENCH_OPTS)\n"
+            "print(' '.join(re.findall(r'src=(\\S+)', s)))\n")
+    env = dict(os.environ, HHLSV_JIT=env_jit)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return out.stdout.split()
+
+
+def test_spill_fallback_regenerates_spilling_passes():
+    """The register-spill fallback regenerates the passes whose ptxas report shows spills
+    (three of the 8-way sharded S33 passes at 128 registers; S30's pass 3, 8 B) and keeps the rest."""
+    a, b = _jit_sources("S33", 8, ""), _jit_sources("S33", 8, "spillfb=0")
+    assert len(a) == len(b) and 1 <= sum(x != y for x, y in zip(a, b)) < len(a)
+    a, b = _jit_sources("S30", 1, ""), _jit_sources("S30", 1, "spillfb=0")
+    assert len(a) == len(b) == 5 and sum(x != y for x, y in zip(a, b)) <= 1
