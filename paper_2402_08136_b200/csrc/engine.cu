@@ -1016,7 +1016,7 @@ sv_program *program_create(sv_state *sv, const std::vector<Gate> &ops, const std
     // Register-spill fallback: ptxas output of every pass is checked (in parallel; the cubins are kept
     // for jit_build); a pass that spills is regenerated without constant-bank tables, then also without
     // grouped diagonal factors, keeping the variant that spills least (S33 sharded pass 3: 376 B of
-    // spills, 18.6 -> 15.9 ms per rank; the S30 passes do not spill and are unchanged).
+    // spills, 18.6 -> 16.1 ms per rank; of the S30 passes only pass 3 spills, 8 B, at equal speed).
     // (large states only: a small program is launch- and latency-bound, spills or not)
     if (use_jit && jit_config().spillfb && !p->jit.empty() && sv->nloc >= 24) {
         std::vector<int> spill(p->jit.size(), 0);
