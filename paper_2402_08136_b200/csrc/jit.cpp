@@ -230,6 +230,7 @@ const JitConfig &jit_config() {
             else if (key == "spillfb") x.spillfb = iv != 0;
             else if (key == "dalap") x.dalap = std::max(0, iv);
             else if (key == "twiddle") x.twiddle = iv != 0;
+            else if (key == "dmma") x.dmma = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;

@@ -67,6 +67,7 @@ struct JitConfig {
     bool mred = true;         // mred: the last tile pass accumulates the HHL ancilla marginal (fused readout)
     bool spillfb = true;      // spillfb: regenerate a spilling pass with the JitVariant fallbacks
     bool twiddle = true;      // twiddle: a diagonal's x1 multiplies folded into the following butterfly
+    bool dmma = true;         // dmma: streaming dense k = 5 / low-target k = 3, 4 on the FP64 tensor cores
     int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible)
 };
 const JitConfig &jit_config();

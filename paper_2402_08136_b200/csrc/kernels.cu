@@ -6,8 +6,8 @@
 // Reductions are fixed-order trees (warp shuffle -> block -> grid), never fp64 atomics,
 // so two runs are bit-identical.
 #include <cstdio>
-#include <cstdlib>
 
+#include "jit.h"
 #include "kernels.cuh"
 
 namespace hhlsv {
@@ -178,13 +178,9 @@ __global__ void __launch_bounds__(kThreads) k_dense_dmma(const DenseArgs a, uint
 // Which dense / controlled ops take the DMMA kernel (measured, profiles/r02_op_microbench.jsonl): k = 5
 // always (FP64-bound: 0.43 -> 0.55 of the HBM peak); k = 3, 4 when a target sits in the low 5 bits (the
 // thread-per-group kernel then reads 2^k x 16 B per thread at a warp stride: k = 4 low 0.52 -> 0.86).
-// HHLSV_DMMA = 0 disables it (A/B experiments).
+// HHLSV_JIT=dmma=0 disables it (A/B experiments).
 static bool dmma_pick(const DenseArgs &a) {
-    static const bool on = [] {
-        const char *e = getenv("HHLSV_DMMA");
-        return !e || atoi(e) != 0;
-    }();
-    if (!on || a.k < 3) return false;
+    if (!jit_config().dmma || a.k < 3) return false;
     if (a.k == 5) return true;
     int lo = 64, hi = 0;
     for (int i = 0; i < a.k; i++) {
