@@ -12,6 +12,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <charconv>
+#include <type_traits>
 #include <functional>
 #include <atomic>
 #include <cstdio>
@@ -178,6 +180,34 @@ int dep_slot(int c, int M) {   // deposit bits of c into the set bits of M (4-bi
         }
     return out;
 }
+
+// Append-only source buffer for the generator (std::ostringstream formatting was ~half of a program's
+// host front end): strings and characters appended as is, integers via std::to_chars, doubles as %g
+// (the ostringstream defaults), so the generated text is unchanged.
+struct SrcBuf {
+    std::string s;
+    SrcBuf() { s.reserve(1 << 16); }
+    SrcBuf &operator<<(const std::string &x) { s += x; return *this; }
+    SrcBuf &operator<<(const char *x) { s += x; return *this; }
+    SrcBuf &operator<<(char c) { s += c; return *this; }
+    SrcBuf &operator<<(signed char c) { s += (char)c; return *this; }
+    SrcBuf &operator<<(unsigned char c) { s += (char)c; return *this; }
+    SrcBuf &operator<<(bool b) { s += b ? '1' : '0'; return *this; }
+    SrcBuf &operator<<(double v) {
+        char b[32];
+        const int n = snprintf(b, sizeof b, "%g", v);
+        s.append(b, (size_t)n);
+        return *this;
+    }
+    template <class T, std::enable_if_t<std::is_integral_v<T>, int> = 0>
+    SrcBuf &operator<<(T v) {
+        char b[24];
+        const auto r = std::to_chars(b, b + sizeof b, v);
+        s.append(b, r.ptr);
+        return *this;
+    }
+    std::string str() const { return s; }
+};
 
 std::string u64s(uint64_t x) {
     std::ostringstream o;
@@ -492,7 +522,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     // k_pair_sum). Saves the readout's separate full-state read (16 B/amplitude).
     const bool red = a.red >= 0;
     const std::string rbs = std::to_string(a.red);
-    std::ostringstream k;
+    SrcBuf k;
     if (ctot) k << "struct CWArg { double2 w[" << ctot << "]; };\n";
     k << "extern \"C\" __global__ void __launch_bounds__(" << NTHR << ", " << min_blocks << ") " << name
       << "(double2 *__restrict__ psi, const double2 *__restrict__ blob, u64 n_tiles, u64 rank_base, u64 tile0"
