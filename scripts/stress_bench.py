@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=30)
 ap.add_argument("--kmax", type=int, default=2)
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--profile", action="store_true", help="also print per-step times and the schedule to stderr")
 a = ap.parse_args()
 from oracle import hhl as ohhl  # noqa: E402  (input generation: the 15-qubit logical list)
 A, b, nc = configs.get("C3")
@@ -41,6 +42,13 @@ for _ in range(a.steps):
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1))
 t = sorted(ms)[len(ms) // 2]
+if a.profile:
+    prog.set_timing(True)
+    st.reset()
+    prog.run()
+    for i, (m, kind, by, la, fl) in enumerate(prog.timings(with_flops=True)):
+        print(f"step {i}: kind {kind} {m:8.3f} ms {by / 1e9:6.2f} GB {fl / 1e9:8.1f} GF", file=sys.stderr)
+    print(prog.dump(), file=sys.stderr)
 rep = prog.report
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 print(json.dumps({"workload": f"P{a.n}", "n_logical_gates": len(gates), "n_fused": rep["n_fused"],
