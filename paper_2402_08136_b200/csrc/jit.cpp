@@ -133,6 +133,8 @@ struct SRef {
     u32 a;
     __device__ __forceinline__ operator double2() const { return lds(a); }
     __device__ __forceinline__ void operator=(double2 v) const { sts(a, v); }
+    // element copy (a = b between two slots copies the value, not the proxy)
+    __device__ __forceinline__ void operator=(const SRef &o) const { sts(a, lds(o.a)); }
 };
 struct SArr {      // double2 array in shared memory
     u32 b;
@@ -261,6 +263,7 @@ const JitConfig &jit_config() {
             else if (key == "dalap") x.dalap = std::max(0, iv);
             else if (key == "twiddle") x.twiddle = iv != 0;
             else if (key == "dmma") x.dmma = iv != 0;
+            else if (key == "wrun") x.wrun = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
@@ -307,14 +310,11 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         for (size_t i = 0; i < ops.size(); i++) {
             const auto &op = ops[i];
             const int Kk = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
-            if (op.kind == 0 && Kk >= 3) {
+            // as many as fit the kernel parameter space (32764 bytes); the rest read through L1
+            if (op.kind == 0 && Kk >= 3 && ctot + ((size_t)1 << (2 * Kk)) <= 2040) {
                 cstage[(int)i] = ctot;
                 ctot += (size_t)1 << (2 * Kk);
             }
-        }
-        if (ctot > 2040) {      // kernel parameter space: 32764 bytes
-            cstage.clear();
-            ctot = 0;
         }
         // small (1-, 2-qubit) dense matrices too, while space remains: their entries become constant-bank
         // DFMA operands instead of 2^2k preloaded registers (a pass of many 2-qubit ops -- Fig. 4 fused
@@ -473,13 +473,49 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             dsub_max = tot;
         }
     }
+    // Wide runs: >= 3 consecutive 4-qubit dense / controlled ops of a phase on exactly its 4 register bits
+    // (e.g. the textbook QPE chain c-U^(2^j), all on the system register) whose conditions are only
+    // out-of-tile (uniform per tile) and thread-bit controls over <= 2 thread bits. The CTA multiplies
+    // the run's matrices per tile, for each assignment of those thread bits, into a 16 x 16 product
+    // (one entry per thread per op: 16 complex FMAs, double-buffered tables in shared memory); each
+    // thread then applies ONE matrix instead of up to N.
+    struct WRun { int p, a, b; std::vector<int> V; };
+    std::vector<WRun> wruns;
+    if (cfg.wrun && RB == 4 && NTHR == 256 && !init)
+        for (size_t p = 0; p < ph.size(); p++)
+            for (int oi = ph[p].op0; oi < ph[p].op1;) {
+                auto ok = [&](int q) {
+                    const auto &op = ops[q];
+                    return op.kind == 0 && op.mask == 15 && op.rcm == 0;
+                };
+                int oj = oi;
+                std::vector<int> V;
+                while (oj < ph[p].op1 && ok(oj)) {
+                    for (int b = 0; b < 16; b++)
+                        if (((ops[oj].tcm >> b) & 1) && std::find(V.begin(), V.end(), b) == V.end()) V.push_back(b);
+                    if (V.size() > 2) break;
+                    oj++;
+                }
+                if (oj - oi >= 3) {
+                    std::vector<int> W;       // the thread bits of the ops actually in the run
+                    for (int q = oi; q < oj; q++)
+                        for (int b = 0; b < 16; b++)
+                            if (((ops[q].tcm >> b) & 1) && std::find(W.begin(), W.end(), b) == W.end()) W.push_back(b);
+                    wruns.push_back({(int)p, oi, oj, W});
+                    oi = oj;
+                } else {
+                    oi = std::max(oi + 1, oj);
+                }
+            }
+    size_t wtab_bytes = 0;            // 2 buffers x C combos x (256 + 1 pad) entries x 16 B
+    for (auto &w : wruns) wtab_bytes = std::max(wtab_bytes, (size_t)2 * ((size_t)1 << w.V.size()) * 257 * 16);
     // Tile buffers: 1 = single buffer with several CTAs per SM overlapping each other's load and
     // compute phases (default; measured faster than double buffering at half the occupancy),
     // 2 = cp.async double buffering. Registers capped at 128/thread (16 warps per SM).
     int nbuf = (cfg.nbuf == 2 && !a.zload) ? 2 : 1;
     if (init) nbuf = 1;
     const size_t smem_cta = nbuf * 16 * ((size_t)1 << T) + 8 * (((size_t)1 << SA) + ((size_t)1 << SB)) + wtot * 16 +
-                            dsub_max * 16;
+                            dsub_max * 16 + wtab_bytes;
     if (smem_extra) *smem_extra = smem_cta;      // total dynamic shared memory of the kernel
     // resident CTAs per SM for __launch_bounds__: limited by shared memory, and by registers -- 128 per
     // thread for the 16 register amplitudes, allocated per WARP (a CTA smaller than a warp still takes
@@ -555,6 +591,8 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
     }
     if (dsub_max)
         k << "  const SArr dsub{depB.b + " << (8 << SB) << "u + " << wtot * 16 << "u};\n";
+    if (wtab_bytes)
+        k << "  const SArr wtab{depB.b + " << (8 << SB) << "u + " << (wtot * 16 + dsub_max * 16) << "u};\n";
     {   // tile index -> base: zeros inserted at the tile bits and at the skipped known-zero bits; lifted
         // bits (if any) take the top bits of the tile index
         std::vector<int> ins(a.tbits, a.tbits + T);
@@ -1166,6 +1204,72 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         };
         const bool group_on = cfg.group && !var.no_group;
         for (int oi = P.op0; oi < P.op1 && !cfg.skeleton; oi++) {
+            const WRun *wr = nullptr;
+            for (auto &w : wruns)
+                if (w.p == (int)p && w.a == oi) wr = &w;
+            if (wr) {
+                flush_all();
+                tail_in_smem = false;
+                const int C = 1 << wr->V.size();
+                auto ent = [&](int q, const std::string &idx) {      // entry idx of op q's matrix
+                    auto cs = cstage.find(q);
+                    if (cs != cstage.end()) return "cwa.w[" + std::to_string(cs->second) + "u + " + idx + "]";
+                    return "__ldg(blob + " + std::to_string(ops[q].data_off) + "ull + " + idx + ")";
+                };
+                k << "      { // wide run of " << (wr->b - wr->a) << " ops: per-tile products over " << C << " thread-bit combos\n";
+                k << "        const u32 we = threadIdx.x, wr_ = we >> 4, wc_ = we & 15u;\n";
+                k << "        bar();      // a previous run's readers are done with the tables\n";
+                for (int c = 0; c < C; c++)
+                    k << "        wtab[" << c * 257 << "u + we] = (wr_ == wc_) ? mk(1.0, 0.0) : mk(0.0, 0.0);\n";
+                k << "        u32 pb = 0u;\n        bar();\n";
+                for (int q = wr->a; q < wr->b; q++) {
+                    const auto &op = ops[q];
+                    if (op.gcm) k << "        if ((gbase & " << u64s(op.gcm) << ") == " << u64s(op.gcv) << ") {\n";
+                    else k << "        {\n";
+                    k << "          const u32 po = pb * " << C * 257 << "u, pn = (pb ^ 1u) * " << C * 257 << "u;\n";
+                    bool any = false;
+                    for (int c = 0; c < C; c++) {
+                        uint32_t ctb = 0;
+                        for (size_t i = 0; i < wr->V.size(); i++)
+                            if ((c >> i) & 1) ctb |= 1u << wr->V[i];
+                        const bool act = (ctb & op.tcm) == op.tcv;
+                        if (act) {
+                            if (!any) {      // this thread's matrix row, shared by the combos
+                                for (int kk = 0; kk < 16; kk++)
+                                    k << "          const double2 u" << kk << " = " << ent(q, "wr_ * 16u + " + std::to_string(kk) + "u") << ";\n";
+                                any = true;
+                            }
+                            k << "          { double ax = 0.0, ay = 0.0;";
+                            for (int kk = 0; kk < 16; kk++)
+                                k << " { const double2 t = wtab[po + " << c * 257 + kk * 16 << "u + wc_]; ax = fma(u" << kk
+                                  << ".x, t.x, ax); ax = fma(-u" << kk << ".y, t.y, ax); ay = fma(u" << kk << ".x, t.y, ay); ay = fma(u"
+                                  << kk << ".y, t.x, ay); }";
+                            k << " wtab[pn + " << c * 257 << "u + we] = mk(ax, ay); }\n";
+                        } else {
+                            // (a value copy: a bare wtab[] = wtab[] would assign the shared-memory proxy itself)
+                            k << "          wtab[pn + " << c * 257 << "u + we] = (double2)wtab[po + " << c * 257 << "u + we];\n";
+                        }
+                    }
+                    k << "          pb ^= 1u;\n          bar();\n        }\n";
+                }
+                // apply this thread's product (combo from its thread bits), rows to its own smem slots
+                k << "        const u32 mc = 0u";
+                for (size_t i = 0; i < wr->V.size(); i++) k << " | (((tb >> " << wr->V[i] << ") & 1u) << " << i << ")";
+                k << ";\n        const u32 pm = pb * " << C * 257 << "u + mc * 257u;\n";
+                k << "        #pragma unroll 1\n        for (u32 r = 0; r < 16u; r++) { double ax = 0.0, ay = 0.0;";
+                for (int kk = 0; kk < 16; kk++)
+                    k << " { const double2 w = wtab[pm + r * 16u + " << kk << "u]; ax = fma(w.x, v" << kk << ".x, ax); ax = fma(-w.y, v"
+                      << kk << ".y, ax); ay = fma(w.x, v" << kk << ".y, ay); ay = fma(w.y, v" << kk << ".x, ay); }";
+                k << " const u32 slot = " << rd[0] << "u";
+                for (int i = 0; i < 4; i++) k << " | ((r >> " << i << ") & 1u) << " << P.R[i];
+                k << "; cur[swz(tb | slot)] = mk(ax, ay); }\n";
+                for (int r = 0; r < 16; r++) k << "        v" << r << " = " << sref(rd[r]) << ";\n";
+                // the tables are rewritten by the next run / tile only after a barrier: the end of this
+                // phase (or tile) has one, and a following run starts with one after its init
+                k << "      }\n";
+                oi = wr->b - 1;
+                continue;
+            }
             const DRun *run = nullptr;
             for (auto &dr : druns)
                 if (dr.p == (int)p && oi >= dr.a && oi < dr.b) run = &dr;

@@ -68,6 +68,7 @@ struct JitConfig {
     bool spillfb = true;      // spillfb: regenerate a spilling pass with the JitVariant fallbacks
     bool twiddle = true;      // twiddle: a diagonal's x1 multiplies folded into the following butterfly
     bool dmma = true;         // dmma: streaming dense k = 5 / low-target k = 3, 4 on the FP64 tensor cores
+    bool wrun = true;         // wrun: per-tile products of runs of 4-qubit ops on a phase's register bits
     int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible)
 };
 const JitConfig &jit_config();

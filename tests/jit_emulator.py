@@ -127,6 +127,7 @@ struct SRef {
     u32 a;
     operator double2() const { return lds(a); }
     void operator=(double2 v) const { sts(a, v); }
+    void operator=(const SRef &o) const { sts(a, lds(o.a)); }
 };
 struct SArr {
     u32 b;

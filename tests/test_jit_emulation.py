@@ -119,3 +119,44 @@ def test_paper_mode_fusion_emulated(tmp_path):
     out, reps = emu.run_program(d, psi0)
     _clean(reps)
     assert np.abs(emu.to_logical(out, emu.final_map(txt)) - sim.run(t, n, psi0)).max() < 1e-12
+
+
+@pytest.mark.parametrize("ctrls", ["d,d,11", "12,11,10", "d,11,12,10,13"])
+def test_wide_run_products_emulated(tmp_path, ctrls):
+    """Per-tile products of a run of 4-qubit dense / controlled ops on the phase's register bits (controls
+    out of the tile and on <= 2 thread bits): the CTA multiplies the matrices per thread-bit combination
+    and every thread applies one product."""
+    n = 15
+    rng = np.random.default_rng(5)
+
+    def unitary():
+        z = rng.normal(size=(16, 16)) + 1j * rng.normal(size=(16, 16))
+        return np.linalg.qr(z)[0]
+    gates = []
+    for c in ctrls.split(","):
+        if c == "d":
+            gates.append({"kind": "dense", "targets": [0, 1, 2, 3], "data": unitary()})
+        else:
+            gates.append({"kind": "controlled", "targets": [0, 1, 2, 3], "controls": [int(c)], "cvals": 1,
+                          "data": unitary()})
+    psi0 = synthetic.random_state(n, 2)
+    d, txt = _export(tmp_path, lambda: pkg.schedule_dump(n, gates, fusion_kmax=1, tile_qubits=12, tile_jit=1)[0])
+    srcs = [open(os.path.join(d, f)).read() for f in os.listdir(d) if f.startswith("src_")]
+    assert sum(s.count("wide run") for s in srcs) == 1
+    out, reps = emu.run_program(d, psi0)
+    _clean(reps)
+    assert np.abs(emu.to_logical(out, emu.final_map(txt)) - sim.run(gates, n, psi0)).max() < 1e-12
+
+
+def test_textbook_hhl_wide_run_emulated(tmp_path):
+    """C3's textbook circuit (controlled-U^(2^j) chain on the system register) as 12-qubit tile passes:
+    the chain runs as per-tile products; the state matches the oracle."""
+    A, b, nc = configs.get("C3")
+    xo, po, psi_o, p = ohhl.solve(A, b, nc)
+    d, txt = _export(tmp_path, lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, tile_jit=1, tile_qubits=12,
+                                                             fusion_kmax=4, qpe_mode=0)[0])
+    srcs = [open(os.path.join(d, f)).read() for f in os.listdir(d) if f.startswith("src_")]
+    assert sum(s.count("wide run") for s in srcs) >= 1
+    out, reps = emu.run_program(d, np.full(1 << p.n, np.nan + 1j * np.nan))
+    _clean(reps)
+    assert np.abs(emu.to_logical(out, emu.final_map(txt)) - psi_o).max() < 1e-12
