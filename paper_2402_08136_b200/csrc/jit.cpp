@@ -157,6 +157,11 @@ __device__ __forceinline__ void cp_async16s(u32 s, const void *gmem) {
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ double2 mk(double x, double y) { double2 r; r.x = x; r.y = y; return r; }
+// FP64 tensor-core MMA, m8n8k4 (warp-collective): {d0, d1} += A (8x4, row) x B (4x8, col)
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
 __device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
     return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
@@ -264,6 +269,7 @@ const JitConfig &jit_config() {
             else if (key == "twiddle") x.twiddle = iv != 0;
             else if (key == "dmma") x.dmma = iv != 0;
             else if (key == "wrun") x.wrun = iv != 0;
+            else if (key == "vdmma") x.vdmma = iv != 0;
             else if (key == "rb") x.reg_bits = (iv == 3) ? 3 : 4;
             else if (key == "skeleton") x.skeleton = iv != 0;
             else if (key == "xoverlap") x.xoverlap = iv != 0;
@@ -761,7 +767,47 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             if (emit_pre(p, "gbase")) k << "      bar();\n";
         }
 
-        if (p == 0 && din && init) {
+        // Tail on the FP64 tensor cores: the last phase (stored through shared memory) holds ONE real,
+        // unconditioned 4-qubit dense op on exactly its register bits (the final V of the HHL program).
+        // Per warp it is Y = V X with X = the 32 groups' 16 amplitudes as 64 real columns (re, im):
+        // 2 row tiles x 4 k-steps x 8 column tiles of mma.m8n8k4.f64, operands straight from the tile in
+        // shared memory (lane (n, kk) reads amplitude kk + 4 ks of group (8 ct + n) / 2), results written
+        // back in place (a column tile's groups are read only by its own mma) for the final store loop.
+        bool vdm = false;
+        if (cfg.vdmma && p + 1 == ph.size() && !dout && P.op1 - P.op0 == 1 && NTHR == 256 && RB == 4) {
+            const dev::RegOp &op = ops[P.op0];
+            vdm = op.kind == 0 && op.mask == 15 && op.is_signed && !op.rcm && !op.tcm && !op.gcm;
+        }
+        if (vdm) {
+            const dev::RegOp &op = ops[P.op0];
+            auto cs = cstage.find(P.op0);
+            auto ventry = [&](const std::string &idx) {
+                if (cs != cstage.end()) return "cwa.w[" + std::to_string(cs->second) + "u + " + idx + "].x";
+                return "__ldg(&blob[" + std::to_string(op.data_off) + "ull + " + idx + "].x)";
+            };
+            k << "      { // op " << P.op0 << " on the FP64 tensor cores (DMMA)\n";
+            k << "        auto tbf = [](u32 t) { return 0u";
+            for (int i = 0; i < T - RB; i++) k << " | (((t >> " << i << ") & 1u) << " << P.tpos[i] << ")";
+            k << "; };\n";
+            k << "        const u32 lane = threadIdx.x & 31u, wbase = threadIdx.x & ~31u, n = lane >> 2, kk = lane & 3u;\n";
+            k << "        double a[2][4];\n";
+            for (int rt = 0; rt < 2; rt++)
+                for (int ks = 0; ks < 4; ks++)
+                    k << "        a[" << rt << "][" << ks << "] = " << ventry("(" + std::to_string(8 * rt) + "u + n) * 16u + " + std::to_string(4 * ks) + "u + kk") << ";\n";
+            k << "        auto rdf = [](u32 j) { return 0u";        // register slot j -> tile-local offset
+            for (int i = 0; i < 4; i++) k << " | (((j >> " << i << ") & 1u) << " << P.R[i] << ")";
+            k << "; };\n";
+            k << "        #pragma unroll 1\n        for (u32 ct = 0; ct < 8u; ct++) {\n";
+            k << "          const u32 gi = tbf(wbase + 4u * ct + (n >> 1));      // this lane's B column: group, part\n";
+            k << "          double b[4];\n";
+            k << "          #pragma unroll\n          for (int ks = 0; ks < 4; ks++) { const double2 x = cur[swz(gi | rdf(4u * ks + kk))]; b[ks] = (n & 1u) ? x.y : x.x; }\n";
+            k << "          const u32 go = tbf(wbase + 4u * ct + kk);            // this lane's D columns: group (re, im)\n";
+            k << "          #pragma unroll\n          for (int rt = 0; rt < 2; rt++) {\n";
+            k << "            double d0 = 0.0, d1 = 0.0;\n";
+            k << "            #pragma unroll\n            for (int ks = 0; ks < 4; ks++) dmma884(d0, d1, a[rt][ks], b[ks]);\n";
+            k << "            cur[swz(go | rdf(8u * rt + n))] = mk(d0, d1);\n";
+            k << "          }\n        }\n      }\n";
+        } else if (p == 0 && din && init) {
             for (int j = 0; j < RA; j++) {
                 k << "      double2 v" << j << " = mk(0.0, 0.0);\n      { const u64 gi = gbase | pd_in | " << u64s(phys_slot(P, j))
                   << ";\n        if (!(gi & " << u64s(init->zero_mask) << ")) {\n";
@@ -800,7 +846,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
         // The last op of a last phase that stores through shared memory is a wide dense op without
         // controls: its rows are written to their final shared-memory slots, so neither the register
         // reload nor the end-of-phase stores are needed.
-        bool tail_in_smem = false;
+        bool tail_in_smem = vdm;      // the DMMA tail wrote its results to their smem slots
         auto tail_wide = [&](int oi) {
             const dev::RegOp &op = ops[oi];
             const int Kq = (op.mask & 1) + ((op.mask >> 1) & 1) + ((op.mask >> 2) & 1) + ((op.mask >> 3) & 1);
@@ -1203,7 +1249,7 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "      }\n";
         };
         const bool group_on = cfg.group && !var.no_group;
-        for (int oi = P.op0; oi < P.op1 && !cfg.skeleton; oi++) {
+        for (int oi = P.op0; oi < P.op1 && !cfg.skeleton && !vdm; oi++) {
             const WRun *wr = nullptr;
             for (auto &w : wruns)
                 if (w.p == (int)p && w.a == oi) wr = &w;

@@ -69,6 +69,7 @@ struct JitConfig {
     bool twiddle = true;      // twiddle: a diagonal's x1 multiplies folded into the following butterfly
     bool dmma = true;         // dmma: streaming dense k = 5 / low-target k = 3, 4 on the FP64 tensor cores
     bool wrun = true;         // wrun: per-tile products of runs of 4-qubit ops on a phase's register bits
+    bool vdmma = false;       // vdmma: a last phase holding one real 4-qubit op (V) on the FP64 tensor cores
     int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible)
 };
 const JitConfig &jit_config();

@@ -32,6 +32,7 @@ import numpy as np
 HOST_PRELUDE = r'''
 #include <atomic>
 #include <barrier>
+#include <memory>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -49,13 +50,18 @@ struct Dim { unsigned x = 0, y = 0, z = 0; };
 static thread_local Dim threadIdx;
 static Dim blockIdx, gridDim;
 static thread_local int g_tid = 0, g_epoch = 0, g_bars = 0;
+// warp-synchronous ordering (mma.sync): accesses of two lanes of one warp separated by a warp-collective
+// MMA are ordered even inside one barrier epoch; g_wsync counts the MMAs a thread passed
+static thread_local int g_wsync = 0;
 static std::barrier<> *g_bar = nullptr;
 static unsigned char *g_smem = nullptr;
 static size_t g_smem_bytes = 0;
 static const double2 *g_psi = nullptr, *g_blob = nullptr;
 static size_t g_psi_n = 0, g_blob_n = 0;
 static std::unordered_set<u64> g_written;
-struct Shadow { int we = -1, wt = -1, re = -1, rt = -1; };
+// per 8-byte word: last write (epoch, thread, warp-sync count) and the reads of the current epoch
+// (one reader's thread or -2, the readers' warp or -3 when several warps, the largest warp-sync count)
+struct Shadow { int we = -1, wt = -1, wws = -1, re = -1, rt = -1, rwarp = -1, rws = -1; };
 static std::vector<Shadow> g_sh;
 static std::mutex g_mu;
 static std::atomic<long> g_races{0}, g_oob{0}, g_double{0};
@@ -69,13 +75,24 @@ static void sm_access(u32 a, unsigned bytes, bool write) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (u32 w = a / 8; w < (a + bytes + 7) / 8; w++) {
         Shadow &s = g_sh[w];
-        if (s.we == g_epoch && s.wt != g_tid) { g_races++; report(write ? "RACE_WAW" : "RACE_RAW", w * 8ull); }
+        const int warp = g_tid >> 5;
+        if (s.we == g_epoch && s.wt != g_tid && !((s.wt >> 5) == warp && s.wws < g_wsync)) {
+            g_races++;
+            report(write ? "RACE_WAW" : "RACE_RAW", w * 8ull);
+        }
         if (write) {
-            if (s.re == g_epoch && s.rt != g_tid) { g_races++; report("RACE_WAR", w * 8ull); }
-            s.we = g_epoch; s.wt = g_tid;
+            if (s.re == g_epoch && s.rt != g_tid && !(s.rwarp == warp && s.rws < g_wsync)) {
+                g_races++;
+                report("RACE_WAR", w * 8ull);
+            }
+            s.we = g_epoch; s.wt = g_tid; s.wws = g_wsync;
         } else {
-            if (s.re != g_epoch) { s.re = g_epoch; s.rt = g_tid; }
-            else if (s.rt != g_tid) s.rt = -2;      // several readers this epoch
+            if (s.re != g_epoch) { s.re = g_epoch; s.rt = g_tid; s.rwarp = warp; s.rws = g_wsync; }
+            else {
+                if (s.rt != g_tid) s.rt = -2;      // several readers this epoch
+                if (s.rwarp != warp) s.rwarp = -3;
+                if (g_wsync > s.rws) s.rws = g_wsync;
+            }
         }
     }
 }
@@ -146,6 +163,22 @@ struct SArr64 {
 };
 static inline double2 mk(double x, double y) { double2 r; r.x = x; r.y = y; return r; }
 static inline double2 cmul(const double2 a, const double2 b) { return mk(std::fma(a.x, b.x, -a.y * b.y), std::fma(a.x, b.y, a.y * b.x)); }
+// mma.sync.m8n8k4.f64 as a warp collective: lane l holds A[l / 4][l % 4], B[l % 4][l / 4] and
+// D[l / 4][2 (l % 4) + {0, 1}] (PTX fragment layouts)
+static std::vector<std::unique_ptr<std::barrier<>>> g_wbars;
+static double g_wa[64][32], g_wb[64][32];
+static inline void dmma884(double &d0, double &d1, double a, double b) {
+    const int w = g_tid >> 5, l = g_tid & 31;
+    g_wa[w][l] = a; g_wb[w][l] = b;
+    g_wbars[w]->arrive_and_wait();
+    g_wsync++;
+    const int row = l >> 2, c0 = 2 * (l & 3);
+    for (int q = 0; q < 4; q++) {
+        d0 = std::fma(g_wa[w][row * 4 + q], g_wb[w][c0 * 4 + q], d0);
+        d1 = std::fma(g_wa[w][row * 4 + q], g_wb[w][(c0 + 1) * 4 + q], d1);
+    }
+    g_wbars[w]->arrive_and_wait();
+}
 static inline double __ddiv_rn(double a, double b) { return a / b; }
 using std::fma; using std::sqrt; using std::fabs;
 static inline double recip_s(u64 m, int n_c, double dL, int sg, double snap) {
@@ -204,10 +237,12 @@ int main(int argc, char **argv) {
         std::fill(g_sh.begin(), g_sh.end(), Shadow{});
         std::barrier<> br(nthr);
         g_bar = &br;
+        g_wbars.clear();
+        for (int w = 0; w * 32 < nthr; w++) g_wbars.emplace_back(new std::barrier<>(std::min(32, nthr - 32 * w)));
         std::vector<std::thread> th;
         for (int t = 0; t < nthr; t++)
             th.emplace_back([&, t] {
-                threadIdx.x = (unsigned)t; g_tid = t; g_epoch = 0; g_bars = 0;
+                threadIdx.x = (unsigned)t; g_tid = t; g_epoch = 0; g_bars = 0; g_wsync = 0;
                 KERNEL_CALL;
                 bars[t] = g_bars;
                 br.arrive_and_drop();
