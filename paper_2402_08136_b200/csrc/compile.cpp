@@ -115,6 +115,15 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
         for (int b : v) high += b >= wmin;
         return (int)v.size() <= T && high <= T - wmin;
     };
+    // the same on bit masks of physical bits (< 64): the greedy packing below tests every ready op
+    // against the open pass many times; masks avoid a vector per test
+    std::vector<uint64_t> ndm(m, 0);
+    for (size_t i = 0; i < m; i++)
+        for (int b : pnd(ops[i])) ndm[i] |= 1ull << b;
+    const uint64_t lowm = wmin >= 64 ? ~0ull : ((1ull << wmin) - 1ull);
+    auto fitsm = [&](uint64_t u) {
+        return __builtin_popcountll(u) <= T && __builtin_popcountll(u & ~lowm) <= T - wmin;
+    };
     std::vector<char> needs_global(m, 0);
     for (size_t i = 0; i < m; i++)
         for (int b : pnd(ops[i]))
@@ -159,28 +168,23 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
             take(first);
             continue;
         }
-        std::vector<int> cur;
+        uint64_t cur = 0;
         const bool dalap_now = pass_no++ < dalap;
         for (;;) {
             // pick the ready op that adds the fewest new tile bits (free ones first), then the
             // earliest in circuit order: keeps room in the pass for ops that become ready later
             size_t best = SIZE_MAX;
             int best_new = 1 << 20;
-            std::vector<int> best_u;
+            uint64_t best_u = 0;
             for (size_t i : ready) {
                 const Gate &g = ops[i];
                 if (g.kind == Kind::Swap ||
                     ((g.kind == Kind::Dense || g.kind == Kind::Controlled) && (int)g.targets.size() > R))
                     continue;
                 if (!exchanged && needs_global[i]) continue;
-                std::vector<int> u = cur;
-                int nnew = 0;
-                for (int b : pnd(g))
-                    if (std::find(u.begin(), u.end(), b) == u.end()) {
-                        u.push_back(b);
-                        nnew++;
-                    }
-                if (!fits(u)) continue;
+                const uint64_t u = cur | ndm[i];
+                const int nnew = __builtin_popcountll(ndm[i] & ~cur);
+                if (!fitsm(u)) continue;
                 if (dalap_now && g.kind == Kind::Diagonal) continue;    // considered below
                 if (nnew < best_new) {
                     best = i;
@@ -201,10 +205,7 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
                         if (use) break;
                         if (indeg[sb] != 1 || ops[sb].kind == Kind::Swap) continue;
                         if (!exchanged && needs_global[sb]) continue;
-                        std::vector<int> u = cur;
-                        for (int b : pnd(ops[sb]))
-                            if (std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
-                        use = fits(u);
+                        use = fitsm(cur | ndm[sb]);
                     }
                     if (use) {
                         best = i;
@@ -354,6 +355,7 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
     // input order so exchanges follow the circuit)
     const bool reorder = tiles && o.reorder;
     const std::vector<Gate> ops = reorder ? reorder_for_tiles(ops_in, phys_in, T, wmin, R, nloc) : ops_in;
+    prof_mark("    compile: reorder");
 
     // Precompute, for Belady eviction, the op index list per logical qubit used as nd target.
     std::vector<std::vector<size_t>> uses(n);
@@ -382,7 +384,9 @@ Schedule compile(const std::vector<Gate> &ops_in, const std::vector<ProductFacto
         for (const Gate &g : tile.tile_ops)
             if (g.kind == Kind::Dense || g.kind == Kind::Controlled) Rp = std::max(Rp, (int)g.targets.size());
         tile.reg_bits = Rp;
+        prof_mark("    compile: pack");
         phase_schedule(tile.tile_ops, Rp, tile.phase_R, tile.phase_start);
+        prof_mark("    compile: phases");
         const int dm = jit_config().diag_merge >= 0 ? jit_config().diag_merge : o.diag_merge;
         if (dm > 0) merge_phase_diagonals(tile, dm);
         // Fill each phase's register set up to R bits with the highest tile bits (lanes keep the
