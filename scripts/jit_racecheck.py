@@ -68,7 +68,8 @@ for name in ("C1", "C2", "C3p", "C3", "S18"):
     xo, po, psi_o, p = ohhl.solve(A, b, nc)
     for label, opts in (("bench", configs.BENCH_OPTS), ("bench + fused marginal", dict(configs.BENCH_OPTS, fused_marginal=1)),
                         ("jit T=9", dict(tile_jit=1, tile_qubits=9)),
-                        ("textbook k2 T=10", dict(tile_jit=1, tile_qubits=10, fusion_kmax=2))):
+                        ("textbook k2 T=10", dict(tile_jit=1, tile_qubits=10, fusion_kmax=2)),
+                        ("textbook k4 T=12 (wide-run products)", dict(tile_jit=1, tile_qubits=12, fusion_kmax=4, qpe_mode=0))):
         d, txt = export(lambda: pkg.hhl_schedule_dump(A, b, clock_qubits=nc, **opts)[0])
         try:
             out, reps = emu.run_program(d, np.full(1 << p.n, np.nan + 1j * np.nan))
