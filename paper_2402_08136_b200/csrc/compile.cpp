@@ -110,13 +110,9 @@ static std::vector<Gate> reorder_for_tiles(const std::vector<Gate> &ops, const s
         for (int &q : nd) q = phys[q];
         return nd;
     };
-    auto fits = [&](const std::vector<int> &v) {
-        int high = 0;
-        for (int b : v) high += b >= wmin;
-        return (int)v.size() <= T && high <= T - wmin;
-    };
-    // the same on bit masks of physical bits (< 64): the greedy packing below tests every ready op
-    // against the open pass many times; masks avoid a vector per test
+    // a pass holds at most T tile bits, at most T - wmin of them above the wmin always-held low bits;
+    // tested on bit masks of physical bits (< 64): the greedy packing below tests every ready op
+    // against the open pass many times
     std::vector<uint64_t> ndm(m, 0);
     for (size_t i = 0; i < m; i++)
         for (int b : pnd(ops[i])) ndm[i] |= 1ull << b;
