@@ -119,6 +119,11 @@ __device__ __forceinline__ u64 lds64(u32 a) {
 }
 __device__ __forceinline__ void sts64(u32 a, u64 v) { asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v)); }
 __device__ __forceinline__ void stsd(u32 a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+__device__ __forceinline__ double ldsd(u32 a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) HHLSV_CLB);
+    return v;
+}
 // Streaming HBM loads of tile data: not allocated in L1 (an SM must never keep lines another SM
 // writes during the pass: a stale line would survive into the next pass), volatile with a memory
 // clobber (never moved across this thread's own stores or re-executed by the compiler)
@@ -797,15 +802,20 @@ std::string gen_tile_kernel(const std::string &name, const dev::TileArgs &a, con
             k << "        auto rdf = [](u32 j) { return 0u";        // register slot j -> tile-local offset
             for (int i = 0; i < 4; i++) k << " | (((j >> " << i << ") & 1u) << " << P.R[i] << ")";
             k << "; };\n";
-            k << "        #pragma unroll 1\n        for (u32 ct = 0; ct < 8u; ct++) {\n";
-            k << "          const u32 gi = tbf(wbase + 4u * ct + (n >> 1));      // this lane's B column: group, part\n";
-            k << "          double b[4];\n";
-            k << "          #pragma unroll\n          for (int ks = 0; ks < 4; ks++) { const double2 x = cur[swz(gi | rdf(4u * ks + kk))]; b[ks] = (n & 1u) ? x.y : x.x; }\n";
-            k << "          const u32 go = tbf(wbase + 4u * ct + kk);            // this lane's D columns: group (re, im)\n";
-            k << "          #pragma unroll\n          for (int rt = 0; rt < 2; rt++) {\n";
-            k << "            double d0 = 0.0, d1 = 0.0;\n";
-            k << "            #pragma unroll\n            for (int ks = 0; ks < 4; ks++) dmma884(d0, d1, a[rt][ks], b[ks]);\n";
-            k << "            cur[swz(go | rdf(8u * rt + n))] = mk(d0, d1);\n";
+            // two column tiles per iteration: 4 independent accumulator chains; B fragments as single
+            // 8-byte shared loads (re or im of one amplitude)
+            k << "        #pragma unroll 1\n        for (u32 ct = 0; ct < 8u; ct += 2u) {\n";
+            k << "          double b[2][4], d[2][2][2];\n";
+            k << "          #pragma unroll\n          for (int c2 = 0; c2 < 2; c2++) {\n";
+            k << "            const u32 gi = tbf(wbase + 4u * (ct + c2) + (n >> 1));   // B column: group, part\n";
+            k << "            #pragma unroll\n            for (int ks = 0; ks < 4; ks++) b[c2][ks] = ldsd(cur.b + (swz(gi | rdf(4u * ks + kk)) << 4) + ((n & 1u) << 3));\n";
+            k << "            d[c2][0][0] = d[c2][0][1] = d[c2][1][0] = d[c2][1][1] = 0.0;\n          }\n";
+            k << "          #pragma unroll\n          for (int ks = 0; ks < 4; ks++)\n";
+            k << "            #pragma unroll\n            for (int c2 = 0; c2 < 2; c2++)\n";
+            k << "              #pragma unroll\n              for (int rt = 0; rt < 2; rt++) dmma884(d[c2][rt][0], d[c2][rt][1], a[rt][ks], b[c2][ks]);\n";
+            k << "          #pragma unroll\n          for (int c2 = 0; c2 < 2; c2++) {\n";
+            k << "            const u32 go = tbf(wbase + 4u * (ct + c2) + kk);      // D columns: group (re, im)\n";
+            k << "            #pragma unroll\n            for (int rt = 0; rt < 2; rt++) cur[swz(go | rdf(8u * rt + n))] = mk(d[c2][rt][0], d[c2][rt][1]);\n";
             k << "          }\n        }\n      }\n";
         } else if (p == 0 && din && init) {
             for (int j = 0; j < RA; j++) {

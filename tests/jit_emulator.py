@@ -112,6 +112,7 @@ static inline void sts(u32 a, double2 v) { sm_access(a, 16, true); memcpy(g_smem
 static inline u64 lds64(u32 a) { sm_access(a, 8, false); u64 v; memcpy(&v, g_smem + a, 8); return v; }
 static inline void sts64(u32 a, u64 v) { sm_access(a, 8, true); memcpy(g_smem + a, &v, 8); }
 static inline void stsd(u32 a, double v) { sm_access(a, 8, true); memcpy(g_smem + a, &v, 8); }
+static inline double ldsd(u32 a) { sm_access(a, 8, false); double v; memcpy(&v, g_smem + a, 8); return v; }
 static inline void cp_async16s(u32 s, const void *g) {
     if (!in_psi(g, 16)) { g_oob++; report("GLOBAL_READ_OOB(cp.async)", (unsigned long long)g); return; }
     sm_access(s, 16, true); memcpy(g_smem + s, g, 16);
