@@ -293,10 +293,23 @@ def build_pass(src: str) -> str:
         cpp = exe + ".cpp"
         with open(cpp, "w") as f:
             f.write(full)
-        subprocess.check_call(["g++", "-std=c++20", "-O1", "-g", "-ffp-contract=off", "-fsanitize=address,undefined",
+        subprocess.check_call(["g++", "-std=c++20", "-O1", "-ffp-contract=off", "-fsanitize=address,undefined",
                                "-fno-omit-frame-pointer", "-pthread", cpp, "-o", exe + ".tmp"])
         os.replace(exe + ".tmp", exe)
     return exe
+
+
+def prebuild(emu_dir: str):
+    """Compile every exported pass of a program concurrently (the builds dominate the tests' time)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with open(os.path.join(emu_dir, "launches.txt")) as f:
+        idx = [ln.split()[1] for ln in f if ln.startswith("TILE")]
+    srcs = []
+    for i in idx:
+        with open(os.path.join(emu_dir, f"src_{i}.cu")) as f:
+            srcs.append(f.read())
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        list(ex.map(build_pass, srcs))
 
 
 def check_full_size(emu_dir: str, n_amps: int, tiles: int = 4, max_cta: int = 2):
@@ -304,6 +317,7 @@ def check_full_size(emu_dir: str, n_amps: int, tiles: int = 4, max_cta: int = 2)
     first `tiles` tiles (a prefix of the real persistent-loop schedule) on a lazily mapped zero state of
     n_amps amplitudes: the bench's own S30 kernels, without needing 16 GiB of host memory."""
     reports = []
+    prebuild(emu_dir)
     with open(os.path.join(emu_dir, "launches.txt")) as f:
         lines = [ln.split() for ln in f if ln.strip()]
     for t in lines:
@@ -331,6 +345,7 @@ def run_program(emu_dir: str, psi: np.ndarray, max_cta: int = 3):
     init are not supported (the tests choose programs made of tile passes)."""
     psi = np.ascontiguousarray(psi, dtype=np.complex128).copy()
     reports = []
+    prebuild(emu_dir)
     with open(os.path.join(emu_dir, "launches.txt")) as f:
         lines = [ln.split() for ln in f if ln.strip()]
     for t in lines:
