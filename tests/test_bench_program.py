@@ -20,6 +20,8 @@ Observed errors are printed (run with -s) and recorded by bench.py as config.par
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -184,3 +186,37 @@ def test_small_program_graph_replay(name):
         assert abs(ps - po) < 1e-12
     assert np.abs(outs[0] - psi_o).max() < 1e-10
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+def test_marginal_requires_the_fused_option():
+    """sv_program_marginal is only available when the program was built with fused_marginal (or by
+    hhl_solve): a plain bench program raises instead of reading stale memory."""
+    A, b, nc = configs.get("C3")
+    st = pkg.State(15)
+    prog = pkg.HHLProgram.build(st, A, b, **dict(BENCH, clock_qubits=nc))
+    prog.run()
+    with pytest.raises(pkg.SVError):
+        prog.marginal()
+    prog.destroy()
+    st.destroy()
+
+
+def test_bench_json_contract():
+    """bench.py prints one JSON line with the driver's keys (small config so it runs in seconds)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--config", "S18", "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["gpu_launches"] > 0 and d["value"] > 0
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.2
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["config"]["workload"] == "S18"
