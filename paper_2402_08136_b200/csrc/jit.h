@@ -48,8 +48,8 @@ struct JitConfig {
     bool sparse = true;       // sparse: exact structural zeros of wide matrices skipped at codegen
     bool tail = true;         // tail: a trailing wide dense op writes straight into the store buffer
     bool cw = true;           // cw: >= 3-target matrices as by-value kernel parameters (constant bank)
-    bool ctab = true;
-    int ctab_bits = 2;        // ctabbits: max thread bits of a constant-bank table index (selected per thread)         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
+    bool ctab = true;         // ctab: small diagonal tables (no out-of-tile index bits, <= 2 thread bits) too
+    int ctab_bits = 2;        // ctabbits: max thread bits of a constant-bank table index (selected per thread)
     int nbuf = 1;             // nbuf: 1 single tile buffer (occupancy), 2 cp.async double buffering
     int min_blocks = 0;       // minb: __launch_bounds__ min blocks per SM (0 = from shared memory)
     int reg_bits = 4;         // rb: register bits per phase (4: 16 amplitudes per thread, 3: 8)
@@ -70,7 +70,9 @@ struct JitConfig {
     bool dmma = true;         // dmma: streaming dense k = 5 / low-target k = 3, 4 on the FP64 tensor cores
     bool wrun = true;         // wrun: per-tile products of runs of 4-qubit ops on a phase's register bits
     bool vdmma = false;       // vdmma: a last phase holding one real 4-qubit op (V) on the FP64 tensor cores
-    int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible)
+                              //        (correct, measured slower: DESIGN §6.2)
+    int dalap = 0;            // dalap: the first N tile passes defer their diagonal ops (as late as possible;
+                              //        measured slower: profiles/r02_experiments.txt)
 };
 const JitConfig &jit_config();
 
