@@ -65,5 +65,7 @@ for cfg, world in (("S31", 2), ("S32", 4), ("S33", 8)):
                       "virtual_exchange_ms": [round(e[0], 3) for e in ex], "modelled_nvlink_ms": round(xfer, 3),
                       "projected_ms_per_rank": round(proj, 3), "projected_weak_scaling_E": round(T30 / proj, 3),
                       "one_gpu_ms": round(T1, 3), "projected_speedup_vs_one_gpu": round(T1 / proj, 3),
+                      # SURVEY §8(d) "pass-normalized E": the same circuit on 1 GPU vs world GPUs
+                      "projected_same_circuit_efficiency": round(T1 / proj / world, 3),
                       "how": "per-rank passes measured (virtual shards, one GPU), exchange modelled at 770 GB/s "
                              "and overlapped with the pass before it"}), flush=True)
