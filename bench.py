@@ -449,7 +449,9 @@ def run_ours(args):
                                   else f"state ({16 << (n - int(math.log2(world))) >> 20} MiB/GPU) >> 126 MB L2; no flush"),
                            "hhl_circuit_time_ms": ms_step, "p_success": ps,
                            "hbm_bytes_per_step": step_bytes, "hbm_frac_of_peak": value / peak_gbs,
-                           "textbook_unfused": textbook, "parity_max_abs": parity},
+                           "textbook_unfused": textbook, "parity_max_abs": parity,
+                           # context only (another machine, end to end incl. Python): Table 1
+                           "paper_sv_sim_a100_s": {"C3p": 13.0, "B30": 234.0}.get(cfg)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(stats["launches"] + 1), "clocks": clocks.summary()}
         if nvlink:
