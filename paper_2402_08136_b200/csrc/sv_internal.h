@@ -147,7 +147,7 @@ struct CompileOptions {
     bool reorder = true;       // commutation-aware op reordering for tile packing (single rank)
     int red_qubit = -1;        // >= 0: the last tile pass also accumulates P(logical qubit = 0 / 1) while
                                // it stores the final state (single-rank JIT programs; sv_program::d_mred)
-    int diag_merge = 8;        // tile passes: merge consecutive diagonal ops of a register phase into
+    int diag_merge = 7;        // tile passes: merge consecutive diagonal ops of a register phase into
                                // one table of <= this many qubits after scheduling (0 = off)
     std::vector<int> phys_init;  // programs that start with their own initialisation: logical->physical
                                  // map at program start (empty = identity)
